@@ -1,0 +1,174 @@
+/* impm_gpu.h — C ABI of the B200-native implicit MPM Newton step.
+ *
+ * Drop-in boundary for the reference's hot path. The
+ * reference has no FFI; its seams are the C++ class `impm::MpmSim<D>`
+ * (/root/reference/proj/include/impm/mpm_solver.hpp:51-478), the coupled
+ * `impm::CoupledSim` (include/impm/porous.hpp:48-125) and the link-level
+ * `impm::sparse_lu_solve` (include/impm/sparse.hpp:43). Each entry point below
+ * names the reference member it replaces. Plain pointers and sizes only; every
+ * call returns an impm_status and is synchronous to the host (stream-ordered
+ * inside). Errors keep the reference's exception classes (errors.hpp:9-50) as
+ * status codes; the message and a NonConvergenceError's residual history are
+ * read back with impm_sim_last_error. The C++ facade in include/impm_gpu.hpp
+ * rethrows them as impm:: exceptions.
+ *
+ * Particle records are exchanged in the reference's own AoS layout
+ * `impm::Particle<D>` (include/impm/particle.hpp:10-29): all doubles, in order
+ *   X[D] x[D] m V0 V F[D*D] sigma[9] lp0[D] lp[D] B_e[9] alpha traction_force[D] point_load[D]
+ * i.e. 6D+22+D*D doubles (232/304/392 bytes for D = 1/2/3).
+ */
+#ifndef IMPM_GPU_H
+#define IMPM_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum impm_status {
+  IMPM_OK = 0,
+  IMPM_ERR_CONFIG = 1,          /* impm::ConfigError */
+  IMPM_ERR_DOMAIN = 2,          /* impm::DomainError */
+  IMPM_ERR_OUT_OF_DOMAIN = 3,   /* impm::OutOfDomainError */
+  IMPM_ERR_NONCONVERGENCE = 4,  /* impm::NonConvergenceError */
+  IMPM_ERR_LINEAR_SOLVER = 5,   /* impm::LinearSolverError */
+  IMPM_ERR_CUDA = 6,
+  IMPM_ERR_NCCL = 7,
+  IMPM_ERR_SEEDING = 8,         /* impm::SeedingFault */
+  IMPM_ERR_UNSUPPORTED = 9      /* impm::UnsupportedOperation */
+} impm_status;
+
+/* impm::Grid<D> (grid.hpp:18-58): nodes at origin + index*h, axis 0 slowest. */
+typedef struct impm_grid {
+  int32_t dim;        /* 1, 2 or 3 */
+  int32_t nodes[3];   /* node count per axis (unused axes: 1) */
+  double origin[3];
+  double h;
+} impm_grid;
+
+/* impm::MaterialKind (materials.hpp:47) + extensions (parity unpinned). */
+typedef enum impm_material_kind {
+  IMPM_HENCKY = 0,
+  IMPM_HENCKY_J2 = 1,
+  IMPM_NEO_HOOKEAN = 2
+} impm_material_kind;
+
+/* impm::MaterialSpec (mpm_solver.hpp:21-25) */
+typedef struct impm_material {
+  int32_t kind;       /* impm_material_kind */
+  int32_t pad_;
+  double E, nu;       /* ElasticParams (materials.hpp:12-23) */
+  double kappa;       /* J2 yield strength */
+} impm_material;
+
+/* Transfer functions: impm::ShapeFunctionKind (gimp.hpp:11). */
+typedef enum impm_shape_kind { IMPM_SHAPE_GIMP = 1, IMPM_SHAPE_BSPLINE2 = 2 } impm_shape_kind;
+
+/* Linear solver behind the sparse_lu_solve seam (src/linear_solver.cpp:11-88). */
+typedef enum impm_krylov_kind { IMPM_KRYLOV_AUTO = 0, IMPM_KRYLOV_CG = 1, IMPM_KRYLOV_BICGSTAB = 2 } impm_krylov_kind;
+
+/* impm::SolverOptions (mpm_solver.hpp:27-36) + GPU linear-solver knobs. */
+typedef struct impm_options {
+  double tol;                 /* relative residual (1e-11) */
+  double abs_floor;           /* 1e-14 */
+  int32_t max_iterations;     /* 20 */
+  int32_t total_lagrangian;   /* 0/1 */
+  int32_t shape;              /* impm_shape_kind, GIMP default */
+  int32_t krylov;             /* impm_krylov_kind */
+  double krylov_rtol;         /* relative true-residual target (1e-12) */
+  int32_t krylov_max_iter;    /* 0 => 10*n_dofs capped at 20000 */
+  int32_t profile;            /* 1: per-kernel-class CUDA-event timing */
+} impm_options;
+
+/* impm::StepRecord (mpm_solver.hpp:38-46) + GPU counters. rel_residuals is
+ * caller-owned storage of rel_capacity doubles. */
+typedef struct impm_step_record {
+  int32_t step;
+  int32_t iterations;
+  double r0_norm;
+  double seconds;
+  double diff_seconds;          /* Jacobian assembly time (JacobianStats::seconds) */
+  int32_t backward_passes;      /* reference-equivalent pass count fields*b^D per iteration */
+  int32_t n_rel;
+  double* rel_residuals;
+  int32_t rel_capacity;
+  int32_t krylov_iterations;    /* total over the step */
+  double solve_seconds;
+  double residual_seconds;
+  int64_t nnz_assembled;        /* reference-pattern scalar nnz x iterations */
+} impm_step_record;
+
+typedef struct impm_sim impm_sim; /* opaque: one MpmSim<D> on one device */
+
+/* version / capability */
+const char* impm_version(void);
+int32_t impm_particle_doubles(int32_t dim); /* 6D+22+D*D */
+
+/* MpmSim(Grid, particles, MaterialSpec, SolverOptions) (mpm_solver.hpp:63-68) */
+impm_status impm_sim_create(const impm_grid* grid, const impm_material* mat, const impm_options* opt,
+                            int32_t device, impm_sim** out);
+impm_status impm_sim_destroy(impm_sim* sim);
+/* Runs all work on this CUDA stream (cudaStream_t, NULL = the sim's own). */
+impm_status impm_sim_set_stream(impm_sim* sim, void* stream);
+
+/* public members particles / fixed / gravity (mpm_solver.hpp:56-61) */
+impm_status impm_sim_set_particles(impm_sim* sim, const double* aos, int64_t n, int64_t stride_bytes);
+impm_status impm_sim_get_particles(impm_sim* sim, double* aos, int64_t n, int64_t stride_bytes);
+impm_status impm_sim_set_particle_field(impm_sim* sim, int32_t field, const double* vals /*[n]*/);
+impm_status impm_sim_n_particles(impm_sim* sim, int64_t* n);
+impm_status impm_sim_set_fixed(impm_sim* sim, const uint8_t* fixed /* [node*D + comp] */);
+impm_status impm_sim_set_gravity(impm_sim* sim, const double* g /* [D] */);
+impm_status impm_sim_set_options(impm_sim* sim, const impm_options* opt);
+
+/* begin_step (mpm_solver.hpp:93-138): binning + counting sort, node mass,
+ * active set, DofMap, BSR pattern. */
+impm_status impm_sim_begin_step(impm_sim* sim);
+/* n_dofs / dofs() / node_mass() / total_node_mass() (mpm_solver.hpp:80-88) */
+impm_status impm_sim_n_dofs(impm_sim* sim, int32_t* n);
+impm_status impm_sim_dof_map(impm_sim* sim, int32_t* dof_of /*[N*D]*/, int32_t* node_of /*[n]*/,
+                             int32_t* field_of /*[n]*/);
+impm_status impm_sim_node_mass(impm_sim* sim, double* mass /*[N]*/);
+/* JacobianAssembler colouring (jacobian.hpp:101-110): group id per DOF. */
+impm_status impm_sim_colour_groups(impm_sim* sim, int32_t* group_of_dof /*[n]*/, int32_t* n_groups);
+/* p2g_map (mpm_solver.hpp:142-152) */
+impm_status impm_sim_p2g_map(impm_sim* sim, const double* per_particle, double* out /*[N]*/);
+
+/* residual (mpm_solver.hpp:213-218): r(u) over free DOFs. */
+impm_status impm_sim_residual(impm_sim* sim, const double* u /*[n]*/, double load_scale, double* r /*[n]*/);
+/* record_residual + JacobianAssembler::sparse (mpm_solver.hpp:223-242,
+ * jacobian.hpp:95-137): J(u) exported in the reference CSR pattern
+ * (jacobian.hpp:36-65). Call with row_ptr/cols/vals NULL to get nnz first. */
+impm_status impm_sim_jacobian_csr(impm_sim* sim, const double* u, double load_scale, int64_t* nnz,
+                                  int64_t* row_ptr /*[n+1]*/, int32_t* cols /*[nnz]*/, double* vals /*[nnz]*/);
+/* the linear solve seam: delta = J(u)^-1 rhs on the device Krylov path */
+impm_status impm_sim_linear_solve(impm_sim* sim, const double* u, double load_scale, const double* rhs,
+                                  double* delta, int32_t* krylov_iterations);
+
+/* newton_solve / newton_attempt (mpm_solver.hpp:248-355) */
+impm_status impm_sim_newton_solve(impm_sim* sim, double load_scale, impm_step_record* rec);
+/* commit_step (mpm_solver.hpp:359-400): G2P + particle update */
+impm_status impm_sim_commit_step(impm_sim* sim);
+/* step (mpm_solver.hpp:402-407) */
+impm_status impm_sim_step(impm_sim* sim, double load_scale, impm_step_record* rec);
+
+/* nodal_solution / set_nodal_solution (mpm_solver.hpp:409-410) */
+impm_status impm_sim_nodal_solution(impm_sim* sim, double* u /*[n]*/);
+impm_status impm_sim_set_nodal_solution(impm_sim* sim, const double* u /*[n]*/);
+
+/* Last error of this sim: message, and for NONCONVERGENCE the residual history. */
+impm_status impm_sim_last_error(impm_sim* sim, char* msg, size_t cap, double* history, int32_t* hist_len);
+
+/* Per-kernel-class device time accumulated since the last reset (profile=1):
+ * names[i] (static strings), ms[i], launches[i]; returns count in *n. */
+impm_status impm_sim_kernel_times(impm_sim* sim, const char** names, double* ms, int64_t* launches,
+                                  int32_t* n, int32_t reset);
+/* Bytes of the stored BSR (values) and algorithmic per-launch traffic figures. */
+impm_status impm_sim_matrix_info(impm_sim* sim, int64_t* n_rows, int64_t* row_values, int64_t* ref_nnz);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* IMPM_GPU_H */

@@ -1,0 +1,1222 @@
+// sm_100a kernels of the implicit MPM Newton step (fp64, HBM-bound).
+//
+// Data layout in HBM:
+//   particles   SoA pd[field * cap + i], fields in impm::Particle<D> order,
+//               kept cell-sorted (counting sort on the first support node);
+//   grid vectors [node][field] over ALL grid nodes, zero at non-free DOFs, so
+//               a node's D components are one 8*D-byte record;
+//   Jacobian    "box BSR": one row per active node, 5^D implicit block
+//               columns (the reference pattern, jacobian.hpp:36-65), F x F
+//               blocks, row length padded to a multiple of 4 doubles;
+//   tangent     per-particle dP/dG, AoS [P][D^4] (read by 3^D rows).
+//
+// Reductions are deterministic: per-block partials in fixed order + one
+// finalize block. No global float atomics anywhere on the path.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "impm_math.cuh"
+
+namespace impm_gpu {
+
+__host__ __device__ constexpr int ipow_c(int b, int e) { return e == 0 ? 1 : b * ipow_c(b, e - 1); }
+__host__ __device__ constexpr int pad4(int x) { return (x + 3) / 4 * 4; }
+
+// Particle<D> field offsets (particle.hpp:10-29)
+template <int D>
+struct PF {
+  static constexpr int X = 0, x = D, m = 2 * D, V0 = 2 * D + 1, V = 2 * D + 2, F = 2 * D + 3,
+                       sigma = 2 * D + 3 + D * D, lp0 = 2 * D + 12 + D * D, lp = 3 * D + 12 + D * D,
+                       Be = 4 * D + 12 + D * D, alpha = 4 * D + 21 + D * D,
+                       trac = 4 * D + 22 + D * D, pload = 5 * D + 22 + D * D,
+                       N = 6 * D + 22 + D * D;
+};
+
+struct GridC {
+  int nodes[3];
+  int stride[3];
+  double origin[3];
+  double h;
+  int N;
+};
+
+template <int D>
+__device__ __forceinline__ void unflat(const GridC& g, int n, int* idx) {
+#pragma unroll
+  for (int a = 0; a < D; ++a) idx[a] = (n / g.stride[a]) % g.nodes[a];
+}
+
+__device__ __forceinline__ double node_coord(const GridC& g, int a, int i) {
+  return __dadd_rn(g.origin[a], __dmul_rn(static_cast<double>(i), g.h));  // grid.hpp:180-185
+}
+
+// packed support counts: 2 bits per axis
+__device__ __forceinline__ int sup_cnt(int s, int a) { return (s >> (2 * a)) & 3; }
+
+// weights of one axis for a particle at its support nodes [first, first+cnt)
+struct AxisW {
+  double w[3], dw[3];
+};
+
+template <int SHAPE>
+__device__ __forceinline__ WeightValue weight_1d(double xi, double lp, double h) {
+  if constexpr (SHAPE == 2) return bspline2_weight_1d(xi, h);
+  return gimp_weight_1d(xi, lp, h);
+}
+
+// gimp_weight<D> (gimp.hpp:37-52): w = prod w_a, grad_a = dw_a prod_{b!=a} w_b
+template <int D>
+__device__ __forceinline__ void tensor_weight(const double* w, const double* dw, double& W, double* grad) {
+  W = 1.0;
+#pragma unroll
+  for (int a = 0; a < D; ++a) W *= w[a];
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    double gg = dw[a];
+#pragma unroll
+    for (int b = 0; b < D; ++b)
+      if (b != a) gg *= w[b];
+    grad[a] = gg;
+  }
+}
+
+// ------------------------------------------------------------ layout io --
+__global__ void k_aos_to_soa(const double* __restrict__ aos, int64_t stride_dbl, int n, int nd,
+                             double* __restrict__ soa, int64_t cap, int* __restrict__ orig) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int f = 0; f < nd; ++f) soa[f * cap + i] = aos[i * stride_dbl + f];
+  orig[i] = i;
+}
+
+__global__ void k_soa_to_aos(const double* __restrict__ soa, int64_t cap, int n, int nd,
+                             const int* __restrict__ orig, double* __restrict__ aos, int64_t stride_dbl) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t o = orig[i];
+  for (int f = 0; f < nd; ++f) aos[o * stride_dbl + f] = soa[f * cap + i];
+}
+
+// per-particle field in ORIGINAL order -> sorted slot
+__global__ void k_set_field(double* __restrict__ col, const double* __restrict__ vals,
+                            const int* __restrict__ orig, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) col[i] = vals[orig[i]];
+}
+
+// ------------------------------------------------------------ K1 binning --
+// Device status words (one small struct read back per host decision).
+struct DevStatus {
+  double norm2;       // last reduction
+  double max_mass;    // max particle mass (as ordered bits)
+  int err_domain;     // min original particle id with det <= 0 (INT_MAX none)
+  int err_ood;        // min (orig*4 + axis) with support outside the grid
+  int err_cfg;        // min original id with lp outside (0, h/2)
+  int perm_moved;     // counting sort moved at least one particle
+  int err_lp;         // commit: min original id with lp >= h/2 or <= 0
+  int pad;
+};
+
+template <int D, int SHAPE>
+__global__ void k_support(const double* __restrict__ pd, int64_t cap, int P, GridC g,
+                          const int* __restrict__ orig, int* __restrict__ key, int* __restrict__ sup,
+                          double* __restrict__ xs, DevStatus* st) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  int k = 0, packed = 0;
+  bool ok = true;
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    const double x = pd[(PF<D>::x + a) * cap + i];
+    const double lp = pd[(PF<D>::lp + a) * cap + i];
+    xs[a * cap + i] = x;
+    int first, count;
+    if constexpr (SHAPE == 2) {
+      // quadratic B-spline: nodes with |x - x_i| < 1.5 h
+      const double lo = __dsub_rn(__dsub_rn(x, g.origin[a]), 1.5 * g.h);
+      const double hi = __dadd_rn(__dsub_rn(x, g.origin[a]), 1.5 * g.h);
+      first = static_cast<int>(floor(__ddiv_rn(lo, g.h))) + 1;
+      count = static_cast<int>(ceil(__ddiv_rn(hi, g.h))) - 1 - first + 1;
+    } else {
+      gimp_support_1d(x, lp, g.origin[a], g.h, first, count);
+    }
+    if (ok && (first < 0 || first + count > g.nodes[a])) {
+      atomicMin(&st->err_ood, orig[i] * 4 + a);  // mpm_solver.hpp:105-110
+      ok = false;
+    }
+    if (SHAPE != 2 && (!(lp > 0.0) || lp >= 0.5 * g.h)) atomicMin(&st->err_cfg, orig[i]);  // gimp.cpp:28-30
+    if (count < 1) count = 1;
+    if (count > 3) count = 3;
+    if (first < 0) first = 0;
+    if (first + count > g.nodes[a]) first = g.nodes[a] - count;
+    k += first * g.stride[a];
+    packed |= count << (2 * a);
+  }
+  key[i] = k;
+  sup[i] = packed;
+}
+
+__global__ void k_bin_count(const int* __restrict__ key, int P, int* __restrict__ count, int* __restrict__ rank) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < P) rank[i] = atomicAdd(&count[key[i]], 1);
+}
+
+__global__ void k_bin_scatter(const int* __restrict__ key, const int* __restrict__ rank,
+                              const int* __restrict__ start, int P, int* __restrict__ perm) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < P) perm[start[key[i]] + rank[i]] = i;
+}
+
+// stable order inside each bin (by previous slot) => deterministic sort
+__global__ void k_bin_sort(const int* __restrict__ start, int N, int* __restrict__ perm) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= N) return;
+  const int s = start[b], e = start[b + 1];
+  for (int i = s + 1; i < e; ++i) {
+    const int v = perm[i];
+    int j = i - 1;
+    while (j >= s && perm[j] > v) {
+      perm[j + 1] = perm[j];
+      --j;
+    }
+    perm[j + 1] = v;
+  }
+}
+
+__global__ void k_perm_check(const int* __restrict__ perm, int P, DevStatus* st) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < P && perm[i] != i) st->perm_moved = 1;
+}
+
+// dst[f][i] = src[f][perm[i]] for all fields (blockIdx.y = field)
+__global__ void k_gather_fields(const double* __restrict__ src, double* __restrict__ dst, int64_t cap,
+                                const int* __restrict__ perm, int P) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t f = blockIdx.y;
+  if (i < P) dst[f * cap + i] = src[f * cap + perm[i]];
+}
+__global__ void k_gather_int(const int* __restrict__ src, int* __restrict__ dst, const int* __restrict__ perm, int P) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < P) dst[i] = src[perm[i]];
+}
+
+// external load per particle at unit schedule (mpm_solver.hpp:205-206) and max mass
+template <int D>
+__global__ void k_bext(const double* __restrict__ pd, int64_t cap, int P, double gx, double gy, double gz,
+                       double* __restrict__ bext, DevStatus* st) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double m = 0.0;
+  if (i < P) {
+    m = pd[PF<D>::m * cap + i];
+    const double g[3] = {gx, gy, gz};
+#pragma unroll
+    for (int c = 0; c < D; ++c)
+      bext[c * cap + i] = m * g[c] + pd[(PF<D>::trac + c) * cap + i] + pd[(PF<D>::pload + c) * cap + i];
+  }
+  // block max, then one atomicMax on the (positive) double's bit pattern
+  __shared__ double red[32];
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_down_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_down_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0 && m > 0.0)
+      atomicMax(reinterpret_cast<unsigned long long*>(&st->max_mass), __double_as_longlong(m));
+  }
+}
+
+// Visits the particles whose support contains node `idx`, in fixed order
+// (3^D candidate bins lexicographic, then sorted slot order): fn(p, off[]).
+template <int D, class Fn>
+__device__ __forceinline__ void for_each_particle_of_node(const GridC& g, const int* idx,
+                                                          const int* __restrict__ bin_start,
+                                                          const int* __restrict__ sup, Fn&& fn) {
+  constexpr int NB = ipow_c(3, D);
+  for (int ob = 0; ob < NB; ++ob) {
+    int off[3] = {0, 0, 0};
+    int r = ob, b = 0;
+    bool ok = true;
+#pragma unroll
+    for (int a = D - 1; a >= 0; --a) {
+      off[a] = r % 3;
+      r /= 3;
+      const int bi = idx[a] - off[a];
+      ok = ok && bi >= 0;
+      b += bi * g.stride[a];
+    }
+    if (!ok) continue;
+    const int s = bin_start[b], e = bin_start[b + 1];
+    for (int p = s; p < e; ++p) {
+      const int sp = sup[p];
+      bool in = true;
+#pragma unroll
+      for (int a = 0; a < D; ++a) in = in && off[a] < sup_cnt(sp, a);
+      if (in) fn(p, off);
+    }
+  }
+}
+
+// K2: node mass (pull, deterministic) + active flag + free flags
+template <int D, int F, int SHAPE>
+__global__ void k_node_mass(GridC g, const double* __restrict__ pd, int64_t cap, const double* __restrict__ xs,
+                            const int* __restrict__ bin_start, const int* __restrict__ sup,
+                            const uint8_t* __restrict__ fixed, const DevStatus* st, double* __restrict__ mass,
+                            int* __restrict__ act_flag, int* __restrict__ free_flag) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= g.N) return;
+  int idx[3];
+  unflat<D>(g, n, idx);
+  double M = 0.0;
+  for_each_particle_of_node<D>(g, idx, bin_start, sup, [&](int p, const int*) {
+    double w[3], dw[3];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      const WeightValue wv = weight_1d<SHAPE>(xs[a * cap + p] - node_coord(g, a, idx[a]),
+                                              pd[(PF<D>::lp + a) * cap + p], g.h);
+      w[a] = wv.w;
+      dw[a] = wv.dw;
+    }
+    double W, grad[3];
+    tensor_weight<D>(w, dw, W, grad);
+    M += W * pd[PF<D>::m * cap + p];
+  });
+  mass[n] = M;
+  const int active = M > 1e-12 * st->max_mass ? 1 : 0;  // mpm_solver.hpp:131-133
+  act_flag[n] = active;
+#pragma unroll
+  for (int c = 0; c < F; ++c) free_flag[n * F + c] = active && !fixed[n * F + c];
+}
+
+// K3: DofMap::build (grid.hpp:69-86) from exclusive scans
+__global__ void k_dof_finalize(int NF, int F, const int* __restrict__ free_flag, const int* __restrict__ free_scan,
+                               int* __restrict__ dof_of, int* __restrict__ node_of, int* __restrict__ field_of,
+                               uint8_t* __restrict__ freem) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= NF) return;
+  const int f = free_flag[j];
+  freem[j] = static_cast<uint8_t>(f);
+  if (f) {
+    const int d = free_scan[j];
+    dof_of[j] = d;
+    node_of[d] = j / F;
+    field_of[d] = j % F;
+  } else {
+    dof_of[j] = -1;
+  }
+}
+
+__global__ void k_act_finalize(int N, const int* __restrict__ act_flag, const int* __restrict__ act_scan,
+                               int* __restrict__ act_idx, int* __restrict__ act_list) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  if (act_flag[n]) {
+    const int r = act_scan[n];
+    act_idx[n] = r;
+    act_list[r] = n;
+  } else {
+    act_idx[n] = -1;
+  }
+}
+
+// ------------------------------------------------------ block reductions --
+template <int NV>
+__device__ __forceinline__ void block_sum_store(double (&v)[NV], double* __restrict__ partials) {
+  __shared__ double red[NV][32];
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+    for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_down_sync(0xffffffffu, v[k], o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0)
+#pragma unroll
+    for (int k = 0; k < NV; ++k) red[k][w] = v[k];
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x >> 5;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      double s = l < nw ? red[k][l] : 0.0;
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+      if (l == 0) partials[k * gridDim.x + blockIdx.x] = s;
+    }
+  }
+}
+
+// sums NV rows of `nb` partials in fixed order into out[0..NV)
+template <int NV>
+__global__ void k_finalize_sum(const double* __restrict__ partials, int nb, double* __restrict__ out) {
+  double v[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    double s = 0.0;
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) s += partials[k * nb + i];
+    v[k] = s;
+  }
+  __shared__ double red[NV][32];
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+    for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_down_sync(0xffffffffu, v[k], o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0)
+#pragma unroll
+    for (int k = 0; k < NV; ++k) red[k][w] = v[k];
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x >> 5;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      double s = l < nw ? red[k][l] : 0.0;
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+      if (l == 0) out[k] = s;
+    }
+  }
+}
+
+// ---------------------------------------------------------- K5 residual --
+// Displacement gradient at a particle from its support (mpm_solver.hpp:164-171),
+// lexicographic support order, last axis fastest.
+template <int D, int SHAPE>
+__device__ __forceinline__ void particle_weights(const GridC& g, const double* __restrict__ pd, int64_t cap,
+                                                 const double* __restrict__ xs, int p, int key, int sp,
+                                                 int* first, int* cnt, AxisW* aw) {
+  int rem = key;
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    first[a] = rem / g.stride[a];
+    rem -= first[a] * g.stride[a];
+    cnt[a] = sup_cnt(sp, a);
+    const double x = xs[a * cap + p];
+    const double lp = pd[(PF<D>::lp + a) * cap + p];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      if (i < cnt[a]) {
+        const WeightValue wv = weight_1d<SHAPE>(x - node_coord(g, a, first[a] + i), lp, g.h);
+        aw[a].w[i] = wv.w;
+        aw[a].dw[i] = wv.dw;
+      } else {
+        aw[a].w[i] = 0.0;
+        aw[a].dw[i] = 0.0;
+      }
+    }
+  }
+}
+
+// iterate the support of a particle: fn(node, W, grad)
+template <int D, class Fn>
+__device__ __forceinline__ void for_each_support(const GridC& g, const int* first, const int* cnt, const AxisW* aw,
+                                                 Fn&& fn) {
+  const int c0 = cnt[0], c1 = D > 1 ? cnt[1] : 1, c2 = D > 2 ? cnt[2] : 1;
+  for (int i = 0; i < c0; ++i)
+    for (int j = 0; j < c1; ++j)
+      for (int k = 0; k < c2; ++k) {
+        const int li[3] = {i, j, k};
+        double w[3], dw[3];
+        int node = 0;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          w[a] = aw[a].w[li[a]];
+          dw[a] = aw[a].dw[li[a]];
+          node += (first[a] + li[a]) * g.stride[a];
+        }
+        double W, grad[3];
+        tensor_weight<D>(w, dw, W, grad);
+        fn(node, W, grad);
+      }
+}
+
+struct MatParams {
+  int kind;
+  double lam, mu, kappa;
+};
+
+// update_stress (mpm_solver.hpp:445-454) over scalar T
+template <class T, int D>
+__device__ __forceinline__ StressOut<T> update_stress(const MatParams& mp, const Mat<T, D>& F_new,
+                                                      const Mat<T, D>& f_inc, const double* Be_n,
+                                                      double* Be_out = nullptr, double* dg_out = nullptr) {
+  const T lam = T(mp.lam), mu = T(mp.mu);
+  if (mp.kind == kNeoHookean) return neo_hookean_update<T, D>(F_new, lam, mu);
+  if constexpr (D <= 2) {
+    if (mp.kind == kHencky) return hencky_update<T, D>(F_new, lam, mu);
+    return j2_update<T, D>(f_inc, Be_n, lam, mu, mp.kappa, Be_out, dg_out);
+  }
+  return neo_hookean_update<T, D>(F_new, lam, mu);
+}
+
+// Residual phase A (particles): G, f_inc, F_new, det check, sigma, V and the
+// nominal stress P = V sigma f_inc^{-T} so that the node-side gather is
+// r_{k,c} = sum_b grad_{k,b} P_{cb} - w_k b_c s  (mpm_solver.hpp:164-208).
+template <int D, int SHAPE>
+__global__ void k_residual_particles(GridC g, const double* __restrict__ pd, int64_t cap, int P,
+                                     const double* __restrict__ xs, const int* __restrict__ key,
+                                     const int* __restrict__ sup, const int* __restrict__ orig,
+                                     const double* __restrict__ u, MatParams mp, int tl,
+                                     double* __restrict__ Pst, DevStatus* st) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  int first[3], cnt[3];
+  AxisW aw[3];
+  particle_weights<D, SHAPE>(g, pd, cap, xs, p, key[p], sup[p], first, cnt, aw);
+  Mat<double, D> G = Mat<double, D>::zero();
+  for_each_support<D>(g, first, cnt, aw, [&](int node, double, const double* grad) {
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      const double uc = u[node * D + c];
+#pragma unroll
+      for (int a = 0; a < D; ++a) G(c, a) += uc * grad[a];
+    }
+  });
+  Mat<double, D> f_inc = G;
+#pragma unroll
+  for (int a = 0; a < D; ++a) f_inc(a, a) += 1.0;
+  Mat<double, D> F_new;
+  if (tl) {
+    F_new = f_inc;
+  } else {
+    Mat<double, D> Fn;
+#pragma unroll
+    for (int i = 0; i < D * D; ++i) Fn.e[i] = pd[(PF<D>::F + i) * cap + p];
+    F_new = matmul(f_inc, Fn);
+  }
+  double* out = Pst + static_cast<int64_t>(p) * D * D;
+  if (!(det(F_new) > 0.0)) {  // mpm_solver.hpp:183-184
+    atomicMin(&st->err_domain, orig[p]);
+#pragma unroll
+    for (int i = 0; i < D * D; ++i) out[i] = 0.0;
+    return;
+  }
+  double Be_n[9];
+  if (mp.kind == kHenckyJ2)
+#pragma unroll
+    for (int i = 0; i < 9; ++i) Be_n[i] = pd[(PF<D>::Be + i) * cap + p];
+  const StressOut<double> su = update_stress<double, D>(mp, F_new, f_inc, Be_n);
+  const double V = su.J * pd[PF<D>::V0 * cap + p];
+  const Mat<double, D> fi = inverse(f_inc);
+#pragma unroll
+  for (int c = 0; c < D; ++c)
+#pragma unroll
+    for (int b = 0; b < D; ++b) {
+      double s = su.sigma(c, 0) * fi(b, 0);
+#pragma unroll
+      for (int a = 1; a < D; ++a) s += su.sigma(c, a) * fi(b, a);
+      out[c * D + b] = V * s;
+    }
+}
+
+// Residual phase B (nodes): deterministic pull over the particles of the
+// 3^D candidate bins, masked to free DOFs, + partial sums of r.r
+template <int D, int SHAPE>
+__global__ void k_residual_nodes(GridC g, const double* __restrict__ pd, int64_t cap,
+                                 const double* __restrict__ xs, const int* __restrict__ bin_start,
+                                 const int* __restrict__ sup, const double* __restrict__ Pst,
+                                 const double* __restrict__ bext, const int* __restrict__ act_flag,
+                                 const uint8_t* __restrict__ freem, double load_scale, double* __restrict__ r,
+                                 double* __restrict__ partials) {
+  double rr[1] = {0.0};
+  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < g.N; n += gridDim.x * blockDim.x) {
+    double acc[3] = {0.0, 0.0, 0.0};
+    if (act_flag[n]) {
+      int idx[3];
+      unflat<D>(g, n, idx);
+      for_each_particle_of_node<D>(g, idx, bin_start, sup, [&](int p, const int*) {
+        double w[3], dw[3];
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          const WeightValue wv = weight_1d<SHAPE>(xs[a * cap + p] - node_coord(g, a, idx[a]),
+                                                  pd[(PF<D>::lp + a) * cap + p], g.h);
+          w[a] = wv.w;
+          dw[a] = wv.dw;
+        }
+        double W, grad[3];
+        tensor_weight<D>(w, dw, W, grad);
+        const double* Pp = Pst + static_cast<int64_t>(p) * D * D;
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          double fint = grad[0] * Pp[c * D];
+#pragma unroll
+          for (int b = 1; b < D; ++b) fint += grad[b] * Pp[c * D + b];
+          const double fext = W * bext[c * cap + p] * load_scale;
+          acc[c] += fint - fext;
+        }
+      });
+    }
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      const double v = freem[n * D + c] ? acc[c] : 0.0;
+      r[n * D + c] = v;
+      rr[0] += v * v;
+    }
+  }
+  block_sum_store<1>(rr, partials);
+}
+
+// ------------------------------------------------------- K6 tangent (AD) --
+// dP/dG per particle by forward-mode duals over the same expression graph as
+// the residual (hand-written AD replacing the tape, tape.hpp:107-122):
+// A[p][(c*D+b)*D*D + (d*D+f)] = dP_cb / dG_df.
+template <int D, int SHAPE, int K>
+__global__ void k_tangent(GridC g, const double* __restrict__ pd, int64_t cap, int P,
+                          const double* __restrict__ xs, const int* __restrict__ key,
+                          const int* __restrict__ sup, const double* __restrict__ u, MatParams mp, int tl,
+                          double* __restrict__ A) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  using T = Dual<K>;
+  constexpr int DD = D * D;
+  int first[3], cnt[3];
+  AxisW aw[3];
+  particle_weights<D, SHAPE>(g, pd, cap, xs, p, key[p], sup[p], first, cnt, aw);
+  Mat<double, D> G = Mat<double, D>::zero();
+  for_each_support<D>(g, first, cnt, aw, [&](int node, double, const double* grad) {
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      const double uc = u[node * D + c];
+#pragma unroll
+      for (int a = 0; a < D; ++a) G(c, a) += uc * grad[a];
+    }
+  });
+  double Fn[DD];
+#pragma unroll
+  for (int i = 0; i < DD; ++i) Fn[i] = pd[(PF<D>::F + i) * cap + p];
+  double Be_n[9];
+  if (mp.kind == kHenckyJ2)
+#pragma unroll
+    for (int i = 0; i < 9; ++i) Be_n[i] = pd[(PF<D>::Be + i) * cap + p];
+  const double V0 = pd[PF<D>::V0 * cap + p];
+  double* out = A + static_cast<int64_t>(p) * DD * DD;
+#pragma unroll 1
+  for (int pass = 0; pass < DD / K; ++pass) {
+    Mat<T, D> f_inc;
+#pragma unroll
+    for (int i = 0; i < DD; ++i) {
+      f_inc.e[i] = T(G.e[i]);
+      const int j = i - pass * K;
+      if (j >= 0 && j < K) f_inc.e[i].d[j] = 1.0;
+    }
+#pragma unroll
+    for (int a = 0; a < D; ++a) f_inc(a, a) += 1.0;
+    Mat<T, D> F_new;
+    if (tl) {
+      F_new = f_inc;
+    } else {
+      Mat<T, D> FnT;
+#pragma unroll
+      for (int i = 0; i < DD; ++i) FnT.e[i] = T(Fn[i]);
+      F_new = matmul(f_inc, FnT);
+    }
+    if (!(value_of(det(F_new)) > 0.0)) {
+#pragma unroll
+      for (int i = 0; i < DD * DD; ++i) out[i] = 0.0;
+      return;
+    }
+    const StressOut<T> su = update_stress<T, D>(mp, F_new, f_inc, Be_n);
+    const T V = su.J * V0;
+    const Mat<T, D> fi = inverse(f_inc);
+#pragma unroll
+    for (int c = 0; c < D; ++c)
+#pragma unroll
+      for (int b = 0; b < D; ++b) {
+        T s = su.sigma(c, 0) * fi(b, 0);
+#pragma unroll
+        for (int a = 1; a < D; ++a) s += su.sigma(c, a) * fi(b, a);
+        const T Pcb = V * s;
+#pragma unroll
+        for (int j = 0; j < K; ++j) out[(c * D + b) * DD + pass * K + j] = Pcb.d[j];
+      }
+  }
+}
+
+// Jacobian assembly (K6 phase B): one warp per active node row k. For every
+// particle p whose support contains k (fixed order), lane t < |supp(p)|
+// adds the block (k, l_t) = sum_f H_k[c][d][f] grad_{l_t, f}, with
+// H_k[c][d][f] = sum_b grad_{k,b} A_p[c b][d f], into a shared-memory row
+// accumulator. Rows are written once, coalesced; no atomics. The row's
+// diagonal block inverse (block-Jacobi, masked to free components) is fused.
+template <int D, int SHAPE, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_assemble(GridC g, const double* __restrict__ pd, int64_t cap,
+                                                         const double* __restrict__ xs, const int* __restrict__ bin_start,
+                                                         const int* __restrict__ sup, const double* __restrict__ A,
+                                                         const int* __restrict__ act_list, int n_act,
+                                                         const uint8_t* __restrict__ freem, double* __restrict__ vals,
+                                                         int64_t row_len, double* __restrict__ dinv) {
+  constexpr int DD = D * D;
+  constexpr int S = ipow_c(5, D);
+  constexpr int ACC = S * DD;
+  constexpr int NH = D * D * D;
+  extern __shared__ double smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* acc = smem + warp * (ACC + NH);
+  double* H = acc + ACC;
+  const int row = blockIdx.x * WARPS + warp;
+  if (row >= n_act) return;
+  const int k = act_list[row];
+  int kidx[3];
+  unflat<D>(g, k, kidx);
+  for (int j = lane; j < ACC; j += 32) acc[j] = 0.0;
+  __syncwarp();
+  for_each_particle_of_node<D>(g, kidx, bin_start, sup, [&](int p, const int* off) {
+    // lanes a*3+i evaluate the 1D weights of axis a at support node i
+    int cnt[3], bfirst[3];
+    const int sp = sup[p];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      cnt[a] = sup_cnt(sp, a);
+      bfirst[a] = kidx[a] - off[a];
+    }
+    double w1 = 0.0, dw1 = 0.0;
+    if (lane < 3 * D) {
+      const int a = lane / 3, i = lane % 3;
+      int ca = cnt[0], fa = bfirst[0];
+#pragma unroll
+      for (int b = 1; b < D; ++b)
+        if (a == b) {
+          ca = cnt[b];
+          fa = bfirst[b];
+        }
+      if (i < ca) {
+        const WeightValue wv = weight_1d<SHAPE>(xs[a * cap + p] - node_coord(g, a, fa + i),
+                                                pd[(PF<D>::lp + a) * cap + p], g.h);
+        w1 = wv.w;
+        dw1 = wv.dw;
+      }
+    }
+    double wa[3][3], dwa[3][3];
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        wa[a][i] = __shfl_sync(0xffffffffu, w1, a * 3 + i);
+        dwa[a][i] = __shfl_sync(0xffffffffu, dw1, a * 3 + i);
+      }
+    // gradient of node k
+    double gk[3];
+    {
+      double w[3], dw[3], W;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        w[a] = wa[a][off[a]];
+        dw[a] = dwa[a][off[a]];
+      }
+      tensor_weight<D>(w, dw, W, gk);
+    }
+    const double* Ap = A + static_cast<int64_t>(p) * DD * DD;
+    if (lane < NH) {
+      const int c = lane / DD, df = lane % DD;
+      double s = 0.0;
+#pragma unroll
+      for (int b = 0; b < D; ++b) s += gk[b] * Ap[(c * D + b) * DD + df];
+      H[lane] = s;
+    }
+    __syncwarp();
+    const int nsup = cnt[0] * (D > 1 ? cnt[1] : 1) * (D > 2 ? cnt[2] : 1);
+    if (lane < nsup) {
+      int li[3] = {0, 0, 0};
+      int rem = lane;
+#pragma unroll
+      for (int a = D - 1; a >= 0; --a) {
+        li[a] = rem % cnt[a];
+        rem /= cnt[a];
+      }
+      double w[3], dw[3], W, gl[3];
+      int slot = 0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        w[a] = wa[a][li[a]];
+        dw[a] = dwa[a][li[a]];
+        slot = slot * 5 + (li[a] - off[a] + 2);
+      }
+      tensor_weight<D>(w, dw, W, gl);
+      double* blk = acc + slot * DD;
+#pragma unroll
+      for (int c = 0; c < D; ++c)
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          double s = 0.0;
+#pragma unroll
+          for (int f = 0; f < D; ++f) s += H[(c * D + d) * D + f] * gl[f];
+          blk[c * D + d] += s;
+        }
+    }
+    __syncwarp();
+  });
+  double* dst = vals + static_cast<int64_t>(row) * row_len;
+  for (int j = lane; j < row_len; j += 32) dst[j] = j < ACC ? acc[j] : 0.0;
+  if (lane == 0) {
+    // masked diagonal block inverse: [D_ff 0; 0 I]^-1
+    const double* blk = acc + (S - 1) / 2 * DD;
+    bool fr[3];
+#pragma unroll
+    for (int c = 0; c < D; ++c) fr[c] = freem[k * D + c] != 0;
+    Mat<double, D> Mb;
+#pragma unroll
+    for (int c = 0; c < D; ++c)
+#pragma unroll
+      for (int d = 0; d < D; ++d) Mb(c, d) = (fr[c] && fr[d]) ? blk[c * D + d] : (c == d ? 1.0 : 0.0);
+    const Mat<double, D> Mi = inverse(Mb);
+#pragma unroll
+    for (int i = 0; i < DD; ++i) dinv[static_cast<int64_t>(row) * DD + i] = Mi.e[i];
+  }
+}
+
+// -------------------------------------------------------------- K7 SpMV --
+// y = J x on the box BSR (warp per row, coalesced row streaming, x gathered
+// from L1/L2), masked to free DOFs, fused partial of dotv . y.
+template <int D, int F, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_spmv(GridC g, const int* __restrict__ act_list, int n_act,
+                                                     const double* __restrict__ vals, int64_t row_len,
+                                                     const double* __restrict__ x, const uint8_t* __restrict__ freem,
+                                                     double* __restrict__ y, const double* __restrict__ dotv,
+                                                     double* __restrict__ partials, const int* __restrict__ done) {
+  constexpr int S = ipow_c(5, D);
+  constexpr int FF = F * F;
+  double part[1] = {0.0};
+  if (done == nullptr || *done == 0) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int row = blockIdx.x * WARPS + warp; row < n_act; row += gridDim.x * WARPS) {
+      const int k = act_list[row];
+      int kidx[3];
+      unflat<D>(g, k, kidx);
+      double acc[F];
+#pragma unroll
+      for (int c = 0; c < F; ++c) acc[c] = 0.0;
+      const double* rv = vals + static_cast<int64_t>(row) * row_len;
+      for (int j = lane; j < S * FF; j += 32) {
+        const int s = j / FF, rem = j - s * FF, c = rem / F, d = rem - c * F;
+        int rs = s, nb = k;
+        bool ok = true;
+#pragma unroll
+        for (int a = D - 1; a >= 0; --a) {
+          const int rel = rs % 5 - 2;
+          rs /= 5;
+          const int ia = kidx[a] + rel;
+          ok = ok && ia >= 0 && ia < g.nodes[a];
+          nb += rel * g.stride[a];
+        }
+        if (ok) {
+          const double v = rv[j] * x[static_cast<int64_t>(nb) * F + d];
+#pragma unroll
+          for (int cc = 0; cc < F; ++cc)
+            if (cc == c) acc[cc] += v;
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < F; ++c)
+        for (int o = 16; o > 0; o >>= 1) acc[c] += __shfl_down_sync(0xffffffffu, acc[c], o);
+      if (lane == 0) {
+#pragma unroll
+        for (int c = 0; c < F; ++c) {
+          const double v = freem[k * F + c] ? acc[c] : 0.0;
+          y[static_cast<int64_t>(k) * F + c] = v;
+          if (dotv) part[0] += v * dotv[static_cast<int64_t>(k) * F + c];
+        }
+      }
+    }
+  }
+  if (partials) block_sum_store<1>(part, partials);
+}
+
+// ------------------------------------------------------- K7 PCG vectors --
+// scalar slots of the device-resident CG state
+enum CgSlot { kRz = 0, kPq, kRzNew, kRr, kBb, kAlpha, kBeta, kIters, kDone, kNSlots };
+
+// r = b, x = 0, z = Minv r, p = z; partials of r.z and b.b
+template <int F>
+__global__ void k_cg_init(int N, const int* __restrict__ act_idx, const double* __restrict__ dinv,
+                          const double* __restrict__ b, double* __restrict__ x, double* __restrict__ r,
+                          double* __restrict__ z, double* __restrict__ p, double* __restrict__ partials) {
+  double v[2] = {0.0, 0.0};
+  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
+    const int row = act_idx[n];
+    double rl[F], zl[F];
+#pragma unroll
+    for (int c = 0; c < F; ++c) rl[c] = row >= 0 ? b[n * F + c] : 0.0;
+#pragma unroll
+    for (int c = 0; c < F; ++c) {
+      double s = 0.0;
+      if (row >= 0)
+#pragma unroll
+        for (int d = 0; d < F; ++d) s += dinv[static_cast<int64_t>(row) * F * F + c * F + d] * rl[d];
+      zl[c] = s;
+    }
+#pragma unroll
+    for (int c = 0; c < F; ++c) {
+      x[n * F + c] = 0.0;
+      r[n * F + c] = rl[c];
+      z[n * F + c] = zl[c];
+      p[n * F + c] = zl[c];
+      v[0] += rl[c] * zl[c];
+      v[1] += rl[c] * rl[c];
+    }
+  }
+  block_sum_store<2>(v, partials);
+}
+
+__global__ void k_cg_start(const double* __restrict__ sums, double* __restrict__ sc, double rtol) {
+  // sums = {r.z, b.b}
+  sc[kRz] = sums[0];
+  sc[kBb] = sums[1];
+  sc[kRr] = sums[1];
+  sc[kIters] = 0.0;
+  sc[kDone] = (sums[1] == 0.0) ? 1.0 : 0.0;
+  (void)rtol;
+}
+
+// alpha = rz / (p.q); breakdown (p.q <= 0) -> done = 2
+__global__ void k_cg_alpha(const double* __restrict__ sums, double* __restrict__ sc, int* __restrict__ done) {
+  if (*done) return;
+  const double pq = sums[0];
+  sc[kPq] = pq;
+  if (!(pq > 0.0)) {
+    sc[kDone] = 2.0;
+    *done = 2;
+    return;
+  }
+  sc[kAlpha] = sc[kRz] / pq;
+}
+
+// x += a p; r -= a q; z = Minv r; partials of r.z and r.r
+template <int F>
+__global__ void k_cg_update(int N, const int* __restrict__ act_idx, const double* __restrict__ dinv,
+                            const double* __restrict__ sc, const int* __restrict__ done, double* __restrict__ x,
+                            double* __restrict__ r, double* __restrict__ z, const double* __restrict__ p,
+                            const double* __restrict__ q, double* __restrict__ partials) {
+  double v[2] = {0.0, 0.0};
+  if (*done == 0) {
+    const double alpha = sc[kAlpha];
+    for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
+      const int row = act_idx[n];
+      if (row >= 0) {
+        double rl[F];
+#pragma unroll
+        for (int c = 0; c < F; ++c) {
+          x[n * F + c] += alpha * p[n * F + c];
+          rl[c] = r[n * F + c] - alpha * q[n * F + c];
+          r[n * F + c] = rl[c];
+        }
+#pragma unroll
+        for (int c = 0; c < F; ++c) {
+          double s = 0.0;
+#pragma unroll
+          for (int d = 0; d < F; ++d) s += dinv[static_cast<int64_t>(row) * F * F + c * F + d] * rl[d];
+          z[n * F + c] = s;
+          v[0] += rl[c] * s;
+          v[1] += rl[c] * rl[c];
+        }
+      }
+    }
+  }
+  block_sum_store<2>(v, partials);
+}
+
+__global__ void k_cg_beta(const double* __restrict__ sums, double* __restrict__ sc, int* __restrict__ done,
+                          double rtol2, int max_iter) {
+  if (*done) return;
+  const double rz_new = sums[0], rr = sums[1];
+  sc[kIters] += 1.0;
+  sc[kRr] = rr;
+  if (!(rr == rr)) {  // NaN
+    sc[kDone] = 3.0;
+    *done = 3;
+    return;
+  }
+  if (rr <= rtol2 * sc[kBb]) {
+    sc[kDone] = 1.0;
+    *done = 1;
+    return;
+  }
+  if (sc[kIters] >= max_iter) {
+    sc[kDone] = 4.0;
+    *done = 4;
+    return;
+  }
+  sc[kBeta] = rz_new / sc[kRz];
+  sc[kRz] = rz_new;
+}
+
+template <int F>
+__global__ void k_cg_p(int N, const int* __restrict__ act_idx, const double* __restrict__ sc,
+                       const int* __restrict__ done, const double* __restrict__ z, double* __restrict__ p) {
+  if (*done) return;
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N || act_idx[n] < 0) return;
+  const double beta = sc[kBeta];
+#pragma unroll
+  for (int c = 0; c < F; ++c) p[n * F + c] = z[n * F + c] + beta * p[n * F + c];
+}
+
+// generic BLAS-1 on grid vectors (nonsymmetric Krylov path)
+__global__ void k_dot2(int64_t n, const double* __restrict__ a, const double* __restrict__ b,
+                       const double* __restrict__ c, const double* __restrict__ d, double* __restrict__ partials) {
+  double v[2] = {0.0, 0.0};
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    v[0] += a[i] * b[i];
+    if (c) v[1] += c[i] * d[i];
+  }
+  block_sum_store<2>(v, partials);
+}
+
+// y = a*x + b*y + c*z  (z optional)
+__global__ void k_axpbypcz(int64_t n, double a, const double* __restrict__ x, double b, double* __restrict__ y,
+                           double c, const double* __restrict__ z) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    y[i] = a * x[i] + b * y[i] + (z ? c * z[i] : 0.0);
+}
+
+// z = Minv r (block Jacobi on active rows)
+template <int F>
+__global__ void k_precond(int N, const int* __restrict__ act_idx, const double* __restrict__ dinv,
+                          const double* __restrict__ r, double* __restrict__ z) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  const int row = act_idx[n];
+#pragma unroll
+  for (int c = 0; c < F; ++c) {
+    double s = 0.0;
+    if (row >= 0)
+#pragma unroll
+      for (int d = 0; d < F; ++d) s += dinv[static_cast<int64_t>(row) * F * F + c * F + d] * r[n * F + d];
+    z[n * F + c] = s;
+  }
+}
+
+// --------------------------------------------------------------- K9 G2P --
+template <int D, int SHAPE>
+__global__ void k_commit(GridC g, double* __restrict__ pd, int64_t cap, int P, const double* __restrict__ xs,
+                         const int* __restrict__ key, const int* __restrict__ sup, const int* __restrict__ orig,
+                         const double* __restrict__ u, MatParams mp, int tl, DevStatus* st) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  int first[3], cnt[3];
+  AxisW aw[3];
+  particle_weights<D, SHAPE>(g, pd, cap, xs, p, key[p], sup[p], first, cnt, aw);
+  double du[3] = {0.0, 0.0, 0.0};
+  Mat<double, D> G = Mat<double, D>::zero();
+  for_each_support<D>(g, first, cnt, aw, [&](int node, double W, const double* grad) {
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      const double uv = u[node * D + c];
+      du[c] += W * uv;
+#pragma unroll
+      for (int a = 0; a < D; ++a) G(c, a) += uv * grad[a];
+    }
+  });
+  Mat<double, D> f_inc = G;
+#pragma unroll
+  for (int a = 0; a < D; ++a) f_inc(a, a) += 1.0;
+  if (!(det(f_inc) > 0.0)) {  // mpm_solver.hpp:377-379
+    atomicMin(&st->err_domain, orig[p]);
+    return;
+  }
+  Mat<double, D> F_new;
+  if (tl) {
+    F_new = f_inc;
+  } else {
+    Mat<double, D> Fn;
+#pragma unroll
+    for (int i = 0; i < D * D; ++i) Fn.e[i] = pd[(PF<D>::F + i) * cap + p];
+    F_new = matmul(f_inc, Fn);
+  }
+  double Be_n[9], Be_new[9], dg = 0.0;
+  if (mp.kind == kHenckyJ2)
+#pragma unroll
+    for (int i = 0; i < 9; ++i) Be_n[i] = pd[(PF<D>::Be + i) * cap + p];
+  const StressOut<double> su = update_stress<double, D>(mp, F_new, f_inc, Be_n, Be_new, &dg);
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    if (tl)
+      pd[(PF<D>::x + a) * cap + p] = pd[(PF<D>::X + a) * cap + p] + du[a];
+    else
+      pd[(PF<D>::x + a) * cap + p] += du[a];
+  }
+#pragma unroll
+  for (int i = 0; i < D * D; ++i) pd[(PF<D>::F + i) * cap + p] = F_new.e[i];
+  pd[PF<D>::V * cap + p] = su.J * pd[PF<D>::V0 * cap + p];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) pd[(PF<D>::sigma + i) * cap + p] = su.sigma.e[i];
+  if (mp.kind == kHenckyJ2) {
+#pragma unroll
+    for (int i = 0; i < 9; ++i) pd[(PF<D>::Be + i) * cap + p] = Be_new[i];
+    pd[PF<D>::alpha * cap + p] += dg;
+  }
+  if (!tl) {  // update_particle_domain (gimp.hpp:65-77)
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      const double lp = pd[(PF<D>::lp0 + a) * cap + p] * F_new(a, a);
+      if (!(lp > 0.0) || lp >= 0.5 * g.h) atomicMin(&st->err_lp, orig[p]);
+      pd[(PF<D>::lp + a) * cap + p] = lp;
+    }
+  }
+}
+
+// -------------------------------------------------- parity taps / export --
+// dof vector <-> grid vector
+__global__ void k_dof_to_grid(int n, const double* __restrict__ v, const int* __restrict__ node_of,
+                              const int* __restrict__ field_of, int F, double* __restrict__ gvec) {
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d < n) gvec[static_cast<int64_t>(node_of[d]) * F + field_of[d]] = v[d];
+}
+__global__ void k_grid_to_dof(int n, const double* __restrict__ gvec, const int* __restrict__ node_of,
+                              const int* __restrict__ field_of, int F, double* __restrict__ v) {
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d < n) v[d] = gvec[static_cast<int64_t>(node_of[d]) * F + field_of[d]];
+}
+
+// reference CSR pattern row lengths: free DOFs in the +-2 node box (jacobian.hpp:38-63)
+template <int D>
+__device__ __forceinline__ int box_slot_node(const GridC& g, const int* kidx, int s, int& nb) {
+  int rs = s;
+  nb = 0;
+  bool ok = true;
+  int rel[3];
+#pragma unroll
+  for (int a = D - 1; a >= 0; --a) {
+    rel[a] = rs % 5 - 2;
+    rs /= 5;
+  }
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    const int ia = kidx[a] + rel[a];
+    ok = ok && ia >= 0 && ia < g.nodes[a];
+    nb += ia * g.stride[a];
+  }
+  return ok;
+}
+
+template <int D, int F>
+__global__ void k_csr_count(GridC g, int n, const int* __restrict__ node_of, const int* __restrict__ dof_of,
+                            int64_t* __restrict__ rowlen) {
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= n) return;
+  constexpr int S = ipow_c(5, D);
+  int kidx[3];
+  unflat<D>(g, node_of[d], kidx);
+  int64_t c = 0;
+  for (int s = 0; s < S; ++s) {
+    int nb;
+    if (!box_slot_node<D>(g, kidx, s, nb)) continue;
+    for (int f = 0; f < F; ++f) c += dof_of[nb * F + f] >= 0;
+  }
+  rowlen[d] = c;
+}
+
+template <int D, int F>
+__global__ void k_csr_fill(GridC g, int n, const int* __restrict__ node_of, const int* __restrict__ field_of,
+                           const int* __restrict__ dof_of, const int* __restrict__ act_idx,
+                           const double* __restrict__ vals, int64_t row_len, const int64_t* __restrict__ row_ptr,
+                           int* __restrict__ cols, double* __restrict__ out) {
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= n) return;
+  constexpr int S = ipow_c(5, D);
+  const int k = node_of[d], c = field_of[d];
+  int kidx[3];
+  unflat<D>(g, k, kidx);
+  const int64_t row = act_idx[k];
+  int64_t o = row_ptr[d];
+  for (int s = 0; s < S; ++s) {
+    int nb;
+    if (!box_slot_node<D>(g, kidx, s, nb)) continue;
+    for (int f = 0; f < F; ++f) {
+      const int col = dof_of[nb * F + f];
+      if (col < 0) continue;
+      cols[o] = col;
+      if (out) out[o] = vals[row * row_len + s * F * F + c * F + f];
+      ++o;
+    }
+  }
+}
+
+// p2g_map (mpm_solver.hpp:142-152), pull form
+template <int D, int SHAPE>
+__global__ void k_p2g_map(GridC g, const double* __restrict__ pd, int64_t cap, const double* __restrict__ xs,
+                          const int* __restrict__ bin_start, const int* __restrict__ sup,
+                          const double* __restrict__ mass, const double* __restrict__ f, double* __restrict__ out) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= g.N) return;
+  int idx[3];
+  unflat<D>(g, n, idx);
+  double acc = 0.0;
+  for_each_particle_of_node<D>(g, idx, bin_start, sup, [&](int p, const int*) {
+    double w[3], dw[3];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      const WeightValue wv = weight_1d<SHAPE>(xs[a * cap + p] - node_coord(g, a, idx[a]),
+                                              pd[(PF<D>::lp + a) * cap + p], g.h);
+      w[a] = wv.w;
+      dw[a] = wv.dw;
+    }
+    double W, grad[3];
+    tensor_weight<D>(w, dw, W, grad);
+    acc += W * pd[PF<D>::m * cap + p] * f[p];
+  });
+  out[n] = mass[n] > 0.0 ? acc / mass[n] : acc;
+}
+
+// ------------------------------------------------------------ scans (int) --
+// exclusive scan, 1024 threads x 4 items per block, then block sums
+template <class T>
+__global__ void k_scan_block(const int* __restrict__ in, int64_t n, T* __restrict__ out, T* __restrict__ block_sums) {
+  __shared__ T s[1024];
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * 4096 + threadIdx.x * 4;
+  T v[4];
+  T t = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    v[i] = base + i < n ? static_cast<T>(in[base + i]) : 0;
+    t += v[i];
+  }
+  s[threadIdx.x] = t;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {
+    T add = threadIdx.x >= off ? s[threadIdx.x - off] : 0;
+    __syncthreads();
+    s[threadIdx.x] += add;
+    __syncthreads();
+  }
+  T run = s[threadIdx.x] - t;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (base + i < n) out[base + i] = run;
+    run += v[i];
+  }
+  if (threadIdx.x == 1023) block_sums[blockIdx.x] = s[1023];
+}
+
+template <class T>
+__global__ void k_scan_sums(T* __restrict__ sums, int nb, T* __restrict__ total) {
+  // single block, sequential per thread chunk (nb is small: n / 4096)
+  __shared__ T s[1024];
+  const int per = (nb + 1023) / 1024;
+  const int lo = threadIdx.x * per, hi = min(nb, lo + per);
+  T t = 0;
+  for (int i = lo; i < hi; ++i) t += sums[i];
+  s[threadIdx.x] = t;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {
+    T add = threadIdx.x >= off ? s[threadIdx.x - off] : 0;
+    __syncthreads();
+    s[threadIdx.x] += add;
+    __syncthreads();
+  }
+  T run = s[threadIdx.x] - t;
+  for (int i = lo; i < hi; ++i) {
+    const T v = sums[i];
+    sums[i] = run;
+    run += v;
+  }
+  if (threadIdx.x == 1023) *total = s[1023];
+}
+
+template <class T>
+__global__ void k_scan_add(T* __restrict__ out, int64_t n, const T* __restrict__ sums, const T* __restrict__ total,
+                           T* __restrict__ out_total_slot) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] += sums[i / 4096];
+  if (i == 0 && out_total_slot) *out_total_slot = *total;
+}
+
+}  // namespace impm_gpu

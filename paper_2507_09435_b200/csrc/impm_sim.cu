@@ -1,0 +1,1201 @@
+// Host side of the B200 implicit MPM Newton step: device state, the Newton
+// controller (a line-for-line behavioural restatement of
+// /root/reference/proj/include/impm/mpm_solver.hpp:93-407 over device
+// kernels), the Krylov solve that replaces sparse_lu_solve
+// (src/linear_solver.cpp:11-88), and the C ABI of include/impm_gpu.h.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "../../include/impm_gpu.h"
+#include "impm_kernels.cuh"
+
+using namespace impm_gpu;
+
+namespace {
+
+// ----------------------------------------------------------- errors -----
+struct SimError : std::runtime_error {
+  impm_status code;
+  std::vector<double> history;
+  SimError(impm_status c, const std::string& m, std::vector<double> h = {})
+      : std::runtime_error(m), code(c), history(std::move(h)) {}
+};
+
+#define CK(call)                                                                              \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      throw SimError(IMPM_ERR_CUDA, std::string("CUDA error ") + cudaGetErrorString(e_) +     \
+                                        " at " + __FILE__ + ":" + std::to_string(__LINE__)); \
+  } while (0)
+
+#define CKL() CK(cudaGetLastError())
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t cap = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() {
+    if (p) cudaFree(p);
+  }
+  void ensure(size_t n) {
+    if (n <= cap && p) return;
+    if (p) CK(cudaFree(p));
+    p = nullptr;
+    size_t c = std::max<size_t>(n, 1);
+    CK(cudaMalloc(&p, c * sizeof(T)));
+    cap = c;
+  }
+  T* get() const { return p; }
+};
+
+constexpr int kThreads = 256;
+constexpr int kRedBlocks = 148 * 4;  // fixed partial count for deterministic reductions
+inline unsigned blocks_for(int64_t n, int t = kThreads) { return static_cast<unsigned>(std::max<int64_t>(1, (n + t - 1) / t)); }
+
+template <int V>
+using IC = std::integral_constant<int, V>;
+
+// ---------------------------------------------------------- profiling ---
+enum KClass { kcSort = 0, kcMass, kcDof, kcResP, kcResN, kcTangent, kcAssemble, kcSpmv, kcKrylov, kcCommit, kcCount };
+const char* kClassNames[kcCount] = {"support_sort", "node_mass", "dof_map",  "residual_particles", "residual_nodes",
+                                    "tangent",      "assemble",  "spmv",     "krylov_vector",      "commit"};
+
+struct Prof {
+  bool on = false;
+  cudaStream_t s = nullptr;
+  std::vector<cudaEvent_t> pool;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+  double ms[kcCount] = {};
+  int64_t launches[kcCount] = {};
+  size_t used = 0;
+  cudaEvent_t ev() {
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      pool.push_back(e);
+    }
+    return pool[used++];
+  }
+  struct Scope {
+    Prof* p;
+    int cls;
+    cudaEvent_t b{}, e{};
+    Scope(Prof* pr, int c) : p(pr), cls(c) {
+      if (p->on) {
+        b = p->ev();
+        e = p->ev();
+        CK(cudaEventRecord(b, p->s));
+      }
+    }
+    ~Scope() {
+      if (p->on) {
+        cudaEventRecord(e, p->s);
+        p->pending.push_back({cls, {b, e}});
+      }
+    }
+  };
+  void flush() {  // caller has synchronized the stream
+    for (auto& q : pending) {
+      float t = 0.f;
+      if (cudaEventElapsedTime(&t, q.second.first, q.second.second) == cudaSuccess) {
+        ms[q.first] += t;
+        launches[q.first] += 1;
+      }
+    }
+    pending.clear();
+    used = 0;
+  }
+  ~Prof() {
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+};
+
+// ------------------------------------------------------------ the sim ---
+struct Sim {
+  // configuration
+  int D = 2, F = 2, shape = 1;
+  GridC g{};
+  impm_material mat{};
+  impm_options opt{};
+  double gravity[3] = {0, 0, 0};
+  int device = 0;
+  cudaStream_t own_stream = nullptr, s = nullptr;
+
+  // particles
+  int P = 0;
+  int64_t cap = 0;
+  int ND = 0;
+  DBuf<double> pd, pd_tmp, xs, bext, Pst, Atan;
+  DBuf<int> orig, orig_tmp, key, sup, rank, perm, bin_count, bin_start;
+  // grid / dofs
+  DBuf<uint8_t> fixed, freem;
+  DBuf<int> act_flag, act_scan, act_idx, act_list, free_flag, free_scan, dof_of, node_of, field_of;
+  DBuf<int> scan_sums_i;
+  DBuf<int64_t> scan_sums_l, rowlen, rowptr;
+  DBuf<double> mass;
+  int n_dofs = 0, n_act = 0;
+  // vectors (grid layout [N][F])
+  DBuf<double> u, r, delta, utry, rtry, prev, tmp1, tmp2;
+  DBuf<double> kx, kr, kz, kp, kq, kv, ks, kt, khat;
+  // matrix
+  DBuf<double> vals, dinv;
+  int64_t row_len = 0;
+  bool matrix_valid = false;
+  // reductions / status
+  DBuf<double> partials, sums, sc;
+  DBuf<DevStatus> st;
+  DBuf<int> dflag;
+  DevStatus* h_st = nullptr;  // pinned mirror
+  double* h_sc = nullptr;
+
+  // controller state (mpm_solver.hpp:466-477)
+  bool step_built = false;
+  bool have_prev = false;
+  bool have_uwarm = false;
+  int step_counter = 0;
+
+  // last error
+  std::string err_msg;
+  std::vector<double> err_hist;
+  Prof prof;
+
+  int64_t NF() const { return static_cast<int64_t>(g.N) * F; }
+
+  template <class Fn>
+  void dispatch(Fn&& fn) {
+    const int key_ = D * 10 + shape;
+    switch (key_) {
+      case 11: fn(IC<1>{}, IC<1>{}); break;
+      case 12: fn(IC<1>{}, IC<2>{}); break;
+      case 21: fn(IC<2>{}, IC<1>{}); break;
+      case 22: fn(IC<2>{}, IC<2>{}); break;
+      case 31: fn(IC<3>{}, IC<1>{}); break;
+      case 32: fn(IC<3>{}, IC<2>{}); break;
+      default: throw SimError(IMPM_ERR_CONFIG, "unsupported dimension/shape");
+    }
+  }
+
+  MatParams matp() const {
+    MatParams m;
+    m.kind = mat.kind;
+    const double E = mat.E, nu = mat.nu;
+    m.lam = E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu));  // materials.hpp:16-17
+    m.mu = E / (2.0 * (1.0 + nu));
+    m.kappa = mat.kappa;
+    return m;
+  }
+
+  Sim(const impm_grid* gr, const impm_material* m, const impm_options* o, int dev) {
+    D = gr->dim;
+    if (D < 1 || D > 3) throw SimError(IMPM_ERR_CONFIG, "grid dimension must be 1, 2 or 3");
+    F = D;
+    device = dev;
+    CK(cudaSetDevice(device));
+    int N = 1;
+    for (int a = 0; a < 3; ++a) {
+      g.nodes[a] = a < D ? gr->nodes[a] : 1;
+      g.origin[a] = a < D ? gr->origin[a] : 0.0;
+      if (g.nodes[a] < 1) throw SimError(IMPM_ERR_CONFIG, "grid node counts must be positive");
+      N *= g.nodes[a];
+    }
+    g.stride[D - 1] = 1;
+    for (int a = D - 2; a >= 0; --a) g.stride[a] = g.stride[a + 1] * g.nodes[a + 1];
+    for (int a = D; a < 3; ++a) g.stride[a] = 0;
+    g.h = gr->h;
+    g.N = N;
+    if (!(g.h > 0.0)) throw SimError(IMPM_ERR_CONFIG, "grid spacing must be positive");
+    set_material(m);
+    set_options(o);
+    CK(cudaStreamCreateWithFlags(&own_stream, cudaStreamNonBlocking));
+    s = own_stream;
+    prof.s = s;
+    fixed.ensure(NF());
+    CK(cudaMemsetAsync(fixed.p, 0, NF(), s));
+    st.ensure(1);
+    dflag.ensure(4);
+    sc.ensure(kNSlots);
+    partials.ensure(8 * kRedBlocks);
+    sums.ensure(8);
+    CK(cudaMallocHost(&h_st, sizeof(DevStatus)));
+    CK(cudaMallocHost(&h_sc, sizeof(double) * kNSlots));
+    ND = 6 * D + 22 + D * D;
+    CK(cudaStreamSynchronize(s));
+  }
+  ~Sim() {
+    if (h_st) cudaFreeHost(h_st);
+    if (h_sc) cudaFreeHost(h_sc);
+    if (own_stream) cudaStreamDestroy(own_stream);
+  }
+
+  void set_material(const impm_material* m) {
+    mat = *m;
+    if (!(mat.E > 0.0)) throw SimError(IMPM_ERR_CONFIG, "Young's modulus must be positive");
+    if (!(mat.nu > -1.0 && mat.nu < 0.5)) throw SimError(IMPM_ERR_CONFIG, "Poisson's ratio must lie in (-1, 0.5)");
+    if (mat.kind != kHencky && mat.kind != kHenckyJ2 && mat.kind != kNeoHookean)
+      throw SimError(IMPM_ERR_CONFIG, "unknown material kind");
+    if (D == 3 && mat.kind != kNeoHookean)  // mpm_solver.hpp:448-453
+      throw SimError(IMPM_ERR_CONFIG, "material kind not available in 3D");
+    if (mat.kind == kHenckyJ2 && !(mat.kappa > 0.0)) throw SimError(IMPM_ERR_CONFIG, "yield strength must be positive");
+  }
+  void set_options(const impm_options* o) {
+    opt = *o;
+    if (opt.max_iterations <= 0) opt.max_iterations = 20;
+    if (!(opt.tol > 0.0)) opt.tol = 1e-11;
+    if (!(opt.abs_floor >= 0.0)) opt.abs_floor = 1e-14;
+    if (!(opt.krylov_rtol > 0.0)) opt.krylov_rtol = 1e-12;
+    shape = opt.shape == IMPM_SHAPE_BSPLINE2 ? 2 : 1;
+    if (opt.total_lagrangian && mat.kind == kHenckyJ2)  // mpm_solver.hpp:66-67
+      throw SimError(IMPM_ERR_CONFIG, "total-Lagrangian stepping supports elastic materials only");
+    prof.on = opt.profile != 0;
+  }
+
+  void sync() { CK(cudaStreamSynchronize(s)); }
+
+  void reset_status() {
+    DevStatus z{};
+    z.err_domain = INT_MAX;
+    z.err_ood = INT_MAX;
+    z.err_cfg = INT_MAX;
+    z.err_lp = INT_MAX;
+    z.max_mass = 0.0;
+    *h_st = z;
+    CK(cudaMemcpyAsync(st.p, h_st, sizeof(DevStatus), cudaMemcpyHostToDevice, s));
+  }
+  void read_status() {
+    CK(cudaMemcpyAsync(h_st, st.p, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
+    sync();
+  }
+  void clear_errors_only() {
+    // reset the error words, keep max_mass
+    const int big = INT_MAX;
+    CK(cudaMemcpyAsync(&st.p->err_domain, &big, sizeof(int), cudaMemcpyHostToDevice, s));
+  }
+
+  // ---------------------------------------------------------- particles
+  void set_particles(const double* aos, int64_t n, int64_t stride) {
+    if (stride % 8 != 0 || stride < ND * 8) throw SimError(IMPM_ERR_CONFIG, "bad particle stride");
+    if (n > INT_MAX / 2) throw SimError(IMPM_ERR_CONFIG, "too many particles");
+    P = static_cast<int>(n);
+    cap = std::max<int64_t>(P, 1);
+    pd.ensure(cap * ND);
+    pd_tmp.ensure(cap * ND);
+    xs.ensure(cap * 3);
+    bext.ensure(cap * 3);
+    orig.ensure(cap);
+    orig_tmp.ensure(cap);
+    key.ensure(cap);
+    sup.ensure(cap);
+    rank.ensure(cap);
+    perm.ensure(cap);
+    Pst.ensure(cap * D * D);
+    Atan.ensure(cap * D * D * D * D);
+    DBuf<double> staging;
+    staging.ensure(std::max<int64_t>(1, n * (stride / 8)));
+    if (n > 0) {
+      CK(cudaMemcpyAsync(staging.p, aos, n * stride, cudaMemcpyHostToDevice, s));
+      k_aos_to_soa<<<blocks_for(n), kThreads, 0, s>>>(staging.p, stride / 8, P, ND, pd.p, cap, orig.p);
+      CKL();
+    }
+    sync();
+    step_built = false;
+    matrix_valid = false;
+  }
+  void get_particles(double* aos, int64_t n, int64_t stride) {
+    if (n != P) throw SimError(IMPM_ERR_CONFIG, "particle count mismatch");
+    if (stride % 8 != 0 || stride < ND * 8) throw SimError(IMPM_ERR_CONFIG, "bad particle stride");
+    if (n == 0) return;
+    DBuf<double> staging;
+    staging.ensure(n * (stride / 8));
+    if (stride != ND * 8) CK(cudaMemcpyAsync(staging.p, aos, n * stride, cudaMemcpyHostToDevice, s));
+    k_soa_to_aos<<<blocks_for(n), kThreads, 0, s>>>(pd.p, cap, P, ND, orig.p, staging.p, stride / 8);
+    CKL();
+    CK(cudaMemcpyAsync(aos, staging.p, n * stride, cudaMemcpyDeviceToHost, s));
+    sync();
+  }
+  void set_particle_field(int field, const double* vals_h) {
+    if (field < 0 || field >= ND) throw SimError(IMPM_ERR_CONFIG, "bad particle field");
+    DBuf<double> tmp;
+    tmp.ensure(std::max(P, 1));
+    CK(cudaMemcpyAsync(tmp.p, vals_h, sizeof(double) * P, cudaMemcpyHostToDevice, s));
+    k_set_field<<<blocks_for(P), kThreads, 0, s>>>(pd.p + field * cap, tmp.p, orig.p, P);
+    CKL();
+    sync();
+    step_built = false;
+  }
+
+  // ---------------------------------------------------------- scans
+  template <class T>
+  void scan(const int* in, int64_t n, T* out, DBuf<T>& sums_buf, T* total_slot) {
+    const int64_t nb = (n + 4095) / 4096;
+    sums_buf.ensure(nb + 1);
+    k_scan_block<T><<<static_cast<unsigned>(std::max<int64_t>(nb, 1)), 1024, 0, s>>>(in, n, out, sums_buf.p);
+    CKL();
+    k_scan_sums<T><<<1, 1024, 0, s>>>(sums_buf.p, static_cast<int>(nb), sums_buf.p + nb);
+    CKL();
+    k_scan_add<T><<<blocks_for(std::max<int64_t>(n, 1)), kThreads, 0, s>>>(out, n, sums_buf.p, sums_buf.p + nb,
+                                                                           total_slot);
+    CKL();
+  }
+
+  // ------------------------------------------------- begin_step (K1-K4)
+  std::string ood_message(int code) {
+    return "particle " + std::to_string(code / 4) + " has support outside the grid on axis " +
+           std::to_string(code % 4);
+  }
+
+  void begin_step() {
+    if (opt.total_lagrangian && step_built) return;  // mpm_solver.hpp:94
+    const int N = g.N;
+    reset_status();
+    bin_count.ensure(N + 1);
+    bin_start.ensure(N + 1);
+    mass.ensure(N);
+    act_flag.ensure(N);
+    act_scan.ensure(N + 1);
+    act_idx.ensure(N);
+    act_list.ensure(N);
+    free_flag.ensure(NF());
+    free_scan.ensure(NF() + 1);
+    freem.ensure(NF());
+    dof_of.ensure(NF());
+    node_of.ensure(NF());
+    field_of.ensure(NF());
+    for (auto* v : {&u, &r, &delta, &utry, &rtry, &prev, &tmp1, &tmp2, &kx, &kr, &kz, &kp, &kq, &kv, &ks, &kt, &khat})
+      v->ensure(NF());
+    {
+      Prof::Scope ps(&prof, kcSort);
+      dispatch([&](auto Dc, auto Sc) {
+        constexpr int DD = decltype(Dc)::value, SH = decltype(Sc)::value;
+        if (P > 0) {
+          k_support<DD, SH><<<blocks_for(P), kThreads, 0, s>>>(pd.p, cap, P, g, orig.p, key.p, sup.p, xs.p, st.p);
+          CKL();
+        }
+      });
+    }
+    read_status();
+    if (h_st->err_ood != INT_MAX) throw SimError(IMPM_ERR_OUT_OF_DOMAIN, ood_message(h_st->err_ood));
+    if (h_st->err_cfg != INT_MAX)
+      throw SimError(IMPM_ERR_CONFIG, "GIMP requires 0 < lp < h/2 (particle " + std::to_string(h_st->err_cfg) + ")");
+    {
+      Prof::Scope ps(&prof, kcSort);
+      // counting sort by first support node (K1)
+      CK(cudaMemsetAsync(bin_count.p, 0, sizeof(int) * (N + 1), s));
+      if (P > 0) {
+        k_bin_count<<<blocks_for(P), kThreads, 0, s>>>(key.p, P, bin_count.p, rank.p);
+        CKL();
+      }
+      scan<int>(bin_count.p, N, bin_start.p, scan_sums_i, bin_start.p + N);
+      if (P > 0) {
+        k_bin_scatter<<<blocks_for(P), kThreads, 0, s>>>(key.p, rank.p, bin_start.p, P, perm.p);
+        CKL();
+        k_bin_sort<<<blocks_for(N), kThreads, 0, s>>>(bin_start.p, N, perm.p);
+        CKL();
+        k_perm_check<<<blocks_for(P), kThreads, 0, s>>>(perm.p, P, st.p);
+        CKL();
+      }
+    }
+    read_status();
+    if (h_st->perm_moved) {
+      Prof::Scope ps(&prof, kcSort);
+      dim3 grid(blocks_for(P), ND);
+      k_gather_fields<<<grid, kThreads, 0, s>>>(pd.p, pd_tmp.p, cap, perm.p, P);
+      CKL();
+      k_gather_int<<<blocks_for(P), kThreads, 0, s>>>(orig.p, orig_tmp.p, perm.p, P);
+      CKL();
+      std::swap(pd.p, pd_tmp.p);
+      std::swap(pd.cap, pd_tmp.cap);
+      std::swap(orig.p, orig_tmp.p);
+      std::swap(orig.cap, orig_tmp.cap);
+      dispatch([&](auto Dc, auto Sc) {
+        constexpr int DD = decltype(Dc)::value, SH = decltype(Sc)::value;
+        k_support<DD, SH><<<blocks_for(P), kThreads, 0, s>>>(pd.p, cap, P, g, orig.p, key.p, sup.p, xs.p, st.p);
+        CKL();
+      });
+    }
+    {
+      Prof::Scope ps(&prof, kcMass);
+      dispatch([&](auto Dc, auto Sc) {
+        constexpr int DD = decltype(Dc)::value, SH = decltype(Sc)::value;
+        if (P > 0) {
+          k_bext<DD><<<blocks_for(P), kThreads, 0, s>>>(pd.p, cap, P, gravity[0], gravity[1], gravity[2], bext.p, st.p);
+          CKL();
+        }
+        k_node_mass<DD, DD, SH><<<blocks_for(N), kThreads, 0, s>>>(g, pd.p, cap, xs.p, bin_start.p, sup.p, fixed.p,
+                                                                    st.p, mass.p, act_flag.p, free_flag.p);
+        CKL();
+      });
+    }
+    {
+      Prof::Scope ps(&prof, kcDof);
+      scan<int>(free_flag.p, NF(), free_scan.p, scan_sums_i, free_scan.p + NF());
+      k_dof_finalize<<<blocks_for(NF()), kThreads, 0, s>>>(static_cast<int>(NF()), F, free_flag.p, free_scan.p,
+                                                             dof_of.p, node_of.p, field_of.p, freem.p);
+      CKL();
+      scan<int>(act_flag.p, N, act_scan.p, scan_sums_i, act_scan.p + N);
+      k_act_finalize<<<blocks_for(N), kThreads, 0, s>>>(N, act_flag.p, act_scan.p, act_idx.p, act_list.p);
+      CKL();
+    }
+    int counts[2];
+    CK(cudaMemcpyAsync(&counts[0], free_scan.p + NF(), sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&counts[1], act_scan.p + N, sizeof(int), cudaMemcpyDeviceToHost, s));
+    sync();
+    prof.flush();
+    n_dofs = counts[0];
+    n_act = counts[1];
+    const int S = ipow_c(5, D);
+    row_len = pad4(S * F * F);
+    vals.ensure(std::max<int64_t>(1, static_cast<int64_t>(n_act) * row_len));
+    dinv.ensure(std::max<int64_t>(1, static_cast<int64_t>(n_act) * F * F));
+    CK(cudaMemsetAsync(u.p, 0, sizeof(double) * NF(), s));
+    matrix_valid = false;
+    step_built = true;
+    sync();
+  }
+
+  // ------------------------------------------------------ residual (K5)
+  // r = r(u) in grid layout; returns ||r||; throws DomainError on det <= 0
+  double residual_dev(const double* ud, double load_scale, double* rd) {
+    clear_errors_only();
+    const MatParams mp = matp();
+    dispatch([&](auto Dc, auto Sc) {
+      constexpr int DD = decltype(Dc)::value, SH = decltype(Sc)::value;
+      if (P > 0) {
+        Prof::Scope ps(&prof, kcResP);
+        k_residual_particles<DD, SH><<<blocks_for(P), kThreads, 0, s>>>(g, pd.p, cap, P, xs.p, key.p, sup.p, orig.p,
+                                                                        ud, mp, opt.total_lagrangian, Pst.p, st.p);
+        CKL();
+      }
+      {
+        Prof::Scope ps(&prof, kcResN);
+        k_residual_nodes<DD, SH><<<kRedBlocks, kThreads, 0, s>>>(g, pd.p, cap, xs.p, bin_start.p, sup.p, Pst.p,
+                                                                 bext.p, act_flag.p, freem.p, load_scale, rd,
+                                                                 partials.p);
+        CKL();
+        k_finalize_sum<1><<<1, 1024, 0, s>>>(partials.p, kRedBlocks, &st.p->norm2);
+        CKL();
+      }
+    });
+    read_status();
+    prof.flush();
+    if (h_st->err_domain != INT_MAX)
+      throw SimError(IMPM_ERR_DOMAIN, "non-positive det(F) at particle " + std::to_string(h_st->err_domain));
+    return std::sqrt(h_st->norm2);
+  }
+
+  // ------------------------------------------------------ Jacobian (K6)
+  void jacobian_dev(const double* ud) {
+    const MatParams mp = matp();
+    dispatch([&](auto Dc, auto Sc) {
+      constexpr int DD = decltype(Dc)::value, SH = decltype(Sc)::value;
+      if (P > 0) {
+        Prof::Scope ps(&prof, kcTangent);
+        constexpr int K = DD == 3 ? 3 : DD * DD;
+        k_tangent<DD, SH, K><<<blocks_for(P, 128), 128, 0, s>>>(g, pd.p, cap, P, xs.p, key.p, sup.p, ud, mp,
+                                                                opt.total_lagrangian, Atan.p);
+        CKL();
+      }
+      if (n_act > 0) {
+        Prof::Scope ps(&prof, kcAssemble);
+        constexpr int W = DD == 3 ? 4 : 8;
+        constexpr int S = ipow_c(5, DD);
+        const size_t smem = sizeof(double) * W * (S * DD * DD + DD * DD * DD);
+        auto kern = k_assemble<DD, SH, W>;
+        if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<blocks_for(n_act, W), W * 32, smem, s>>>(g, pd.p, cap, xs.p, bin_start.p, sup.p, Atan.p, act_list.p,
+                                                        n_act, freem.p, vals.p, row_len, dinv.p);
+        CKL();
+      }
+    });
+    matrix_valid = true;
+  }
+
+  // ------------------------------------------------------- Krylov (K7)
+  void spmv(const double* x, double* y, const double* dotv, double* parts) {
+    Prof::Scope ps(&prof, kcSpmv);
+    auto launch = [&](auto Dc) {
+      constexpr int DD = decltype(Dc)::value;
+      constexpr int W = 8;
+      k_spmv<DD, DD, W><<<kRedBlocks, W * 32, 0, s>>>(g, act_list.p, n_act, vals.p, row_len, x, freem.p, y, dotv,
+                                                      parts, dflag.p);
+      CKL();
+    };
+    if (D == 1) launch(IC<1>{});
+    else if (D == 2) launch(IC<2>{});
+    else launch(IC<3>{});
+  }
+
+  template <int FF>
+  int cg_solve(const double* b, double* x) {
+    const int N = g.N;
+    const int max_it = opt.krylov_max_iter > 0 ? opt.krylov_max_iter : std::min(20000, std::max(100, 10 * n_dofs));
+    const double rtol2 = opt.krylov_rtol * opt.krylov_rtol;
+    CK(cudaMemsetAsync(dflag.p, 0, sizeof(int), s));
+    {
+      Prof::Scope ps(&prof, kcKrylov);
+      k_cg_init<FF><<<kRedBlocks, kThreads, 0, s>>>(N, act_idx.p, dinv.p, b, x, kr.p, kz.p, kp.p, partials.p);
+      CKL();
+      k_finalize_sum<2><<<1, 1024, 0, s>>>(partials.p, kRedBlocks, sums.p);
+      CKL();
+      k_cg_start<<<1, 1, 0, s>>>(sums.p, sc.p, rtol2);
+      CKL();
+    }
+    // b == 0 -> x = 0
+    CK(cudaMemcpyAsync(h_sc, sc.p, sizeof(double) * kNSlots, cudaMemcpyDeviceToHost, s));
+    sync();
+    if (h_sc[kDone] != 0.0) return 0;
+    const int batch = n_dofs < 20000 ? 16 : 4;
+    int done = 0;
+    while (true) {
+      for (int i = 0; i < batch; ++i) {
+        spmv(kp.p, kq.p, kp.p, partials.p);
+        Prof::Scope ps(&prof, kcKrylov);
+        k_finalize_sum<1><<<1, 1024, 0, s>>>(partials.p, kRedBlocks, sums.p);
+        k_cg_alpha<<<1, 1, 0, s>>>(sums.p, sc.p, dflag.p);
+        k_cg_update<FF><<<kRedBlocks, kThreads, 0, s>>>(N, act_idx.p, dinv.p, sc.p, dflag.p, x, kr.p, kz.p, kp.p,
+                                                        kq.p, partials.p);
+        k_finalize_sum<2><<<1, 1024, 0, s>>>(partials.p, kRedBlocks, sums.p);
+        k_cg_beta<<<1, 1, 0, s>>>(sums.p, sc.p, dflag.p, rtol2, max_it);
+        k_cg_p<FF><<<blocks_for(N), kThreads, 0, s>>>(N, act_idx.p, sc.p, dflag.p, kz.p, kp.p);
+        CKL();
+      }
+      CK(cudaMemcpyAsync(&done, dflag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(h_sc, sc.p, sizeof(double) * kNSlots, cudaMemcpyDeviceToHost, s));
+      sync();
+      prof.flush();
+      if (done) break;
+    }
+    const int iters = static_cast<int>(h_sc[kIters]);
+    if (done == 2) return -iters - 1;  // not SPD: caller falls back to BiCGStab
+    if (done == 3) throw SimError(IMPM_ERR_LINEAR_SOLVER, "Krylov breakdown: NaN residual");
+    if (done == 4) {
+      const double rel = std::sqrt(h_sc[kRr] / h_sc[kBb]);
+      if (!(rel <= 1e-6))
+        throw SimError(IMPM_ERR_LINEAR_SOLVER, "CG did not converge: relative residual " + std::to_string(rel));
+    }
+    return iters;
+  }
+
+  // host-scalar BiCGStab (right block-Jacobi preconditioning), nonsymmetric path
+  double dot(const double* a, const double* b) {
+    k_dot2<<<kRedBlocks, kThreads, 0, s>>>(NF(), a, b, nullptr, nullptr, partials.p);
+    k_finalize_sum<2><<<1, 1024, 0, s>>>(partials.p, kRedBlocks, sums.p);
+    CKL();
+    double h[2];
+    CK(cudaMemcpyAsync(h, sums.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+    sync();
+    return h[0];
+  }
+  void axpbypcz(double a, const double* x, double b, double* y, double c = 0.0, const double* z = nullptr) {
+    k_axpbypcz<<<kRedBlocks, kThreads, 0, s>>>(NF(), a, x, b, y, c, z);
+    CKL();
+  }
+  template <int FF>
+  void precond(const double* rin, double* z) {
+    k_precond<FF><<<blocks_for(g.N), kThreads, 0, s>>>(g.N, act_idx.p, dinv.p, rin, z);
+    CKL();
+  }
+  template <int FF>
+  int bicgstab_solve(const double* b, double* x) {
+    CK(cudaMemsetAsync(dflag.p, 0, sizeof(int), s));
+    const int max_it = opt.krylov_max_iter > 0 ? opt.krylov_max_iter : std::min(20000, std::max(100, 10 * n_dofs));
+    CK(cudaMemsetAsync(x, 0, sizeof(double) * NF(), s));
+    CK(cudaMemcpyAsync(kr.p, b, sizeof(double) * NF(), cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(khat.p, b, sizeof(double) * NF(), cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemsetAsync(kp.p, 0, sizeof(double) * NF(), s));
+    CK(cudaMemsetAsync(kv.p, 0, sizeof(double) * NF(), s));
+    const double bb = dot(b, b);
+    if (bb == 0.0) return 0;
+    const double tol2 = opt.krylov_rtol * opt.krylov_rtol * bb;
+    double rho = 1.0, alpha = 1.0, omega = 1.0;
+    for (int it = 1; it <= max_it; ++it) {
+      const double rho_new = dot(khat.p, kr.p);
+      if (rho_new == 0.0) throw SimError(IMPM_ERR_LINEAR_SOLVER, "BiCGStab breakdown (rho = 0)");
+      const double beta = (rho_new / rho) * (alpha / omega);
+      // p = r + beta (p - omega v)
+      axpbypcz(1.0, kr.p, beta, kp.p, -beta * omega, kv.p);
+      precond<FF>(kp.p, kz.p);  // phat in kz
+      spmv(kz.p, kv.p, nullptr, nullptr);
+      const double rv = dot(khat.p, kv.p);
+      alpha = rho_new / rv;
+      // s = r - alpha v
+      CK(cudaMemcpyAsync(ks.p, kr.p, sizeof(double) * NF(), cudaMemcpyDeviceToDevice, s));
+      axpbypcz(-alpha, kv.p, 1.0, ks.p);
+      axpbypcz(alpha, kz.p, 1.0, x);  // x += alpha phat
+      const double ss = dot(ks.p, ks.p);
+      if (ss <= tol2) return it;
+      precond<FF>(ks.p, tmp1.p);  // shat
+      spmv(tmp1.p, kt.p, nullptr, nullptr);
+      const double ts = dot(kt.p, ks.p), tt = dot(kt.p, kt.p);
+      omega = ts / tt;
+      axpbypcz(omega, tmp1.p, 1.0, x);
+      // r = s - omega t
+      CK(cudaMemcpyAsync(kr.p, ks.p, sizeof(double) * NF(), cudaMemcpyDeviceToDevice, s));
+      axpbypcz(-omega, kt.p, 1.0, kr.p);
+      const double rr = dot(kr.p, kr.p);
+      if (rr <= tol2) return it;
+      if (!(rr == rr)) throw SimError(IMPM_ERR_LINEAR_SOLVER, "BiCGStab breakdown: NaN residual");
+      rho = rho_new;
+    }
+    throw SimError(IMPM_ERR_LINEAR_SOLVER, "BiCGStab did not converge");
+  }
+
+  // delta = J^-1 rhs (grid layout); returns Krylov iterations
+  int solve_dev(const double* rhs, double* x) {
+    auto run = [&](auto Fc) -> int {
+      constexpr int FF = decltype(Fc)::value;
+      if (opt.krylov != IMPM_KRYLOV_BICGSTAB) {
+        const int it = cg_solve<FF>(rhs, x);
+        if (it >= 0) return it;
+        if (opt.krylov == IMPM_KRYLOV_CG) throw SimError(IMPM_ERR_LINEAR_SOLVER, "CG breakdown: J not SPD");
+        return -it - 1 + bicgstab_solve<FF>(rhs, x);
+      }
+      return bicgstab_solve<FF>(rhs, x);
+    };
+    if (F == 1) return run(IC<1>{});
+    if (F == 2) return run(IC<2>{});
+    return run(IC<3>{});
+  }
+
+  // ------------------------------------------------------ Newton (a16/a17)
+  impm_step_record* rec_ = nullptr;
+  std::vector<double> rels_;
+
+  void finish_record(impm_step_record* rec, const std::vector<double>& rels) {
+    if (!rec) return;
+    rec->n_rel = static_cast<int>(rels.size());
+    if (rec->rel_residuals)
+      for (int i = 0; i < std::min<int>(rec->n_rel, rec->rel_capacity); ++i) rec->rel_residuals[i] = rels[i];
+  }
+
+  int64_t ref_nnz_cache = -1;
+  int64_t ref_nnz() {
+    if (ref_nnz_cache >= 0) return ref_nnz_cache;
+    rowlen.ensure(std::max(n_dofs, 1) + 1);
+    rowptr.ensure(std::max(n_dofs, 1) + 1);
+    if (n_dofs == 0) return ref_nnz_cache = 0;
+    dispatch([&](auto Dc, auto) {
+      constexpr int DD = decltype(Dc)::value;
+      k_csr_count<DD, DD><<<blocks_for(n_dofs), kThreads, 0, s>>>(g, n_dofs, node_of.p, dof_of.p, rowlen.p);
+      CKL();
+    });
+    int64_t tot = 0;
+    // sum on host (small, once per step)
+    std::vector<int64_t> h(n_dofs);
+    CK(cudaMemcpyAsync(h.data(), rowlen.p, sizeof(int64_t) * n_dofs, cudaMemcpyDeviceToHost, s));
+    sync();
+    for (auto v : h) tot += v;
+    return ref_nnz_cache = tot;
+  }
+
+  // newton_attempt (mpm_solver.hpp:281-355); u already holds u_init
+  void newton_attempt(double load_scale, impm_step_record* rec) {
+    std::vector<double> rels;
+    const auto t0 = std::chrono::steady_clock::now();
+    double diff_s = 0.0, solve_s = 0.0, res_s = 0.0;
+    int kry = 0, iters = 0;
+    auto tres = std::chrono::steady_clock::now();
+    const double r0 = residual_dev(u.p, load_scale, r.p);
+    res_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - tres).count();
+    auto fill = [&]() {
+      if (!rec) return;
+      rec->step = step_counter;
+      rec->iterations = iters;
+      rec->r0_norm = r0;
+      rec->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      rec->diff_seconds = diff_s;
+      rec->solve_seconds = solve_s;
+      rec->residual_seconds = res_s;
+      rec->krylov_iterations = kry;
+      rec->backward_passes = iters * F * ipow_c(5, D);  // jacobian.hpp:117-125 equivalent
+      rec->nnz_assembled = iters * ref_nnz();
+      finish_record(rec, rels);
+    };
+    if (r0 < opt.abs_floor) {
+      fill();
+      return;
+    }
+    for (int it = 1; it <= opt.max_iterations; ++it) {
+      auto tj = std::chrono::steady_clock::now();
+      jacobian_dev(u.p);
+      sync();
+      diff_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - tj).count();
+      // rhs = -r
+      auto ts = std::chrono::steady_clock::now();
+      axpbypcz(-1.0, r.p, 0.0, tmp2.p);
+      kry += solve_dev(tmp2.p, delta.p);
+      solve_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - ts).count();
+      // full step; backtrack only while infeasible (mpm_solver.hpp:313-332)
+      double alpha = 1.0, rnorm = 0.0;
+      bool accepted = false;
+      for (int cut = 0; cut < 12 && !accepted; ++cut, alpha *= 0.5) {
+        CK(cudaMemcpyAsync(utry.p, u.p, sizeof(double) * NF(), cudaMemcpyDeviceToDevice, s));
+        axpbypcz(alpha, delta.p, 1.0, utry.p);
+        try {
+          tres = std::chrono::steady_clock::now();
+          rnorm = residual_dev(utry.p, load_scale, rtry.p);
+          res_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - tres).count();
+          std::swap(u.p, utry.p);
+          std::swap(r.p, rtry.p);
+          accepted = true;
+        } catch (const SimError& e) {
+          if (e.code != IMPM_ERR_DOMAIN) throw;
+        }
+      }
+      if (!accepted) {
+        fill();
+        throw SimError(IMPM_ERR_NONCONVERGENCE, "Newton stalled at step " + std::to_string(step_counter), rels);
+      }
+      const double rel = rnorm / r0;
+      rels.push_back(rel);
+      iters = it;
+      if (rel <= opt.tol) {
+        if (opt.total_lagrangian) {
+          have_uwarm = true;
+          CK(cudaMemcpyAsync(prev.p, u.p, sizeof(double) * NF(), cudaMemcpyDeviceToDevice, s));
+        } else {
+          have_prev = true;
+          CK(cudaMemcpyAsync(prev.p, u.p, sizeof(double) * NF(), cudaMemcpyDeviceToDevice, s));
+        }
+        sync();
+        fill();
+        return;
+      }
+    }
+    fill();
+    char buf[64];
+    std::snprintf(buf, sizeof buf, "%f", opt.tol);
+    throw SimError(IMPM_ERR_NONCONVERGENCE,
+                   std::string("Newton did not reach tol ") + buf + " in " + std::to_string(opt.max_iterations) +
+                       " iterations at step " + std::to_string(step_counter),
+                   rels);
+  }
+
+  // newton_solve (mpm_solver.hpp:248-279)
+  void newton_solve(double load_scale, impm_step_record* rec) {
+    if (!step_built) throw SimError(IMPM_ERR_CONFIG, "newton_solve before begin_step");
+    ref_nnz_cache = -1;
+    const bool have_warm = opt.total_lagrangian ? have_uwarm : have_prev;
+    ++step_counter;
+    if (have_warm) {
+      // warm = previous converged solution restricted to the current free DOFs
+      mask_copy(prev.p, tmp1.p);
+      bool warm_viable = true;
+      double r_warm = 0.0;
+      try {
+        r_warm = residual_dev(tmp1.p, load_scale, rtry.p);
+      } catch (const SimError& e) {
+        if (e.code != IMPM_ERR_DOMAIN) throw;
+        warm_viable = false;
+      }
+      if (warm_viable) {
+        CK(cudaMemsetAsync(utry.p, 0, sizeof(double) * NF(), s));
+        const double r_cold = residual_dev(utry.p, load_scale, rtry.p);
+        if (r_warm < r_cold) {
+          CK(cudaMemcpyAsync(u.p, tmp1.p, sizeof(double) * NF(), cudaMemcpyDeviceToDevice, s));
+          try {
+            newton_attempt(load_scale, rec);
+            return;
+          } catch (const SimError& e) {
+            if (e.code != IMPM_ERR_NONCONVERGENCE) throw;
+          }
+        }
+      }
+    }
+    CK(cudaMemsetAsync(u.p, 0, sizeof(double) * NF(), s));
+    newton_attempt(load_scale, rec);
+  }
+
+  // dst = src at free DOFs, 0 elsewhere (grid layout)
+  void mask_copy(const double* src, double* dst) {
+    // via dof vectors: dst = 0; dst[node_of,field_of] = src[...]
+    CK(cudaMemsetAsync(dst, 0, sizeof(double) * NF(), s));
+    if (n_dofs == 0) return;
+    tmp2.ensure(NF());
+    k_grid_to_dof<<<blocks_for(n_dofs), kThreads, 0, s>>>(n_dofs, src, node_of.p, field_of.p, F, kt.p);
+    k_dof_to_grid<<<blocks_for(n_dofs), kThreads, 0, s>>>(n_dofs, kt.p, node_of.p, field_of.p, F, dst);
+    CKL();
+  }
+
+  // ------------------------------------------------------- commit (K9)
+  void commit_step() {
+    if (!step_built) throw SimError(IMPM_ERR_CONFIG, "commit_step before begin_step");
+    clear_errors_only();
+    const int big = INT_MAX;
+    CK(cudaMemcpyAsync(&st.p->err_lp, &big, sizeof(int), cudaMemcpyHostToDevice, s));
+    const MatParams mp = matp();
+    dispatch([&](auto Dc, auto Sc) {
+      constexpr int DD = decltype(Dc)::value, SH = decltype(Sc)::value;
+      if (P > 0) {
+        Prof::Scope ps(&prof, kcCommit);
+        k_commit<DD, SH><<<blocks_for(P), kThreads, 0, s>>>(g, pd.p, cap, P, xs.p, key.p, sup.p, orig.p, u.p, mp,
+                                                            opt.total_lagrangian, st.p);
+        CKL();
+      }
+    });
+    read_status();
+    prof.flush();
+    if (h_st->err_domain != INT_MAX)
+      throw SimError(IMPM_ERR_DOMAIN, "inverted element at particle " + std::to_string(h_st->err_domain) +
+                                          ": det(I + grad du) <= 0");
+    if (h_st->err_lp != INT_MAX)
+      throw SimError(IMPM_ERR_DOMAIN, "particle domain half-width of particle " + std::to_string(h_st->err_lp) +
+                                          " reached half the grid spacing " + std::to_string(g.h) +
+                                          "; use finer particles or a capped domain update");
+    if (!opt.total_lagrangian) step_built = false;  // grid reset
+  }
+
+  // ------------------------------------------------------- parity taps
+  void upload_dof_vec(const double* h, double* gvec) {
+    CK(cudaMemsetAsync(gvec, 0, sizeof(double) * NF(), s));
+    if (n_dofs == 0) return;
+    CK(cudaMemcpyAsync(kt.p, h, sizeof(double) * n_dofs, cudaMemcpyHostToDevice, s));
+    k_dof_to_grid<<<blocks_for(n_dofs), kThreads, 0, s>>>(n_dofs, kt.p, node_of.p, field_of.p, F, gvec);
+    CKL();
+  }
+  void download_dof_vec(const double* gvec, double* h) {
+    if (n_dofs == 0) return;
+    k_grid_to_dof<<<blocks_for(n_dofs), kThreads, 0, s>>>(n_dofs, gvec, node_of.p, field_of.p, F, kt.p);
+    CKL();
+    CK(cudaMemcpyAsync(h, kt.p, sizeof(double) * n_dofs, cudaMemcpyDeviceToHost, s));
+    sync();
+  }
+
+  void export_csr(int64_t* nnz, int64_t* row_ptr_h, int32_t* cols_h, double* vals_h) {
+    const int64_t z = ref_nnz();
+    *nnz = z;
+    if (!row_ptr_h) return;
+    std::vector<int64_t> rl(n_dofs);
+    if (n_dofs) CK(cudaMemcpyAsync(rl.data(), rowlen.p, sizeof(int64_t) * n_dofs, cudaMemcpyDeviceToHost, s));
+    sync();
+    row_ptr_h[0] = 0;
+    for (int i = 0; i < n_dofs; ++i) row_ptr_h[i + 1] = row_ptr_h[i] + rl[i];
+    if (n_dofs == 0) return;
+    CK(cudaMemcpyAsync(rowptr.p, row_ptr_h, sizeof(int64_t) * (n_dofs + 1), cudaMemcpyHostToDevice, s));
+    DBuf<int> dcols;
+    DBuf<double> dvals;
+    dcols.ensure(z);
+    dvals.ensure(z);
+    dispatch([&](auto Dc, auto) {
+      constexpr int DD = decltype(Dc)::value;
+      k_csr_fill<DD, DD><<<blocks_for(n_dofs), kThreads, 0, s>>>(g, n_dofs, node_of.p, field_of.p, dof_of.p, act_idx.p,
+                                                                 vals.p, row_len, rowptr.p, dcols.p,
+                                                                 vals_h ? dvals.p : nullptr);
+      CKL();
+    });
+    if (cols_h) CK(cudaMemcpyAsync(cols_h, dcols.p, sizeof(int32_t) * z, cudaMemcpyDeviceToHost, s));
+    if (vals_h) CK(cudaMemcpyAsync(vals_h, dvals.p, sizeof(double) * z, cudaMemcpyDeviceToHost, s));
+    sync();
+  }
+};
+
+impm_status fail(Sim* sim, const SimError& e) {
+  if (sim) {
+    sim->err_msg = e.what();
+    sim->err_hist = e.history;
+  }
+  return e.code;
+}
+
+thread_local std::string g_create_error;
+
+}  // namespace
+
+// ================================================================ C ABI ===
+#define API_BEGIN(sim)        \
+  if (!(sim)) return IMPM_ERR_CONFIG; \
+  try {                       \
+    CK(cudaSetDevice((sim)->device));
+#define API_END(sim)                                            \
+  return IMPM_OK;                                               \
+  }                                                             \
+  catch (const SimError& e) {                                   \
+    return fail(sim, e);                                        \
+  }                                                             \
+  catch (const std::exception& e) {                             \
+    return fail(sim, SimError(IMPM_ERR_CUDA, e.what()));        \
+  }
+
+extern "C" {
+
+const char* impm_version(void) { return "impm-b200 0.1 (sm_100a, fp64)"; }
+int32_t impm_particle_doubles(int32_t dim) { return 6 * dim + 22 + dim * dim; }
+
+impm_status impm_sim_create(const impm_grid* grid, const impm_material* mat, const impm_options* opt, int32_t device,
+                            impm_sim** out) {
+  if (!grid || !mat || !opt || !out) return IMPM_ERR_CONFIG;
+  try {
+    *out = reinterpret_cast<impm_sim*>(new Sim(grid, mat, opt, device));
+    return IMPM_OK;
+  } catch (const SimError& e) {
+    g_create_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_create_error = e.what();
+    return IMPM_ERR_CUDA;
+  }
+}
+
+const char* impm_create_error(void) { return g_create_error.c_str(); }
+
+impm_status impm_sim_destroy(impm_sim* h) {
+  delete reinterpret_cast<Sim*>(h);
+  return IMPM_OK;
+}
+
+#define SIM Sim* sim = reinterpret_cast<Sim*>(h)
+
+impm_status impm_sim_set_stream(impm_sim* h, void* stream) {
+  SIM;
+  API_BEGIN(sim)
+  sim->s = stream ? static_cast<cudaStream_t>(stream) : sim->own_stream;
+  sim->prof.s = sim->s;
+  API_END(sim)
+}
+
+impm_status impm_sim_set_particles(impm_sim* h, const double* aos, int64_t n, int64_t stride) {
+  SIM;
+  API_BEGIN(sim)
+  sim->set_particles(aos, n, stride);
+  API_END(sim)
+}
+impm_status impm_sim_get_particles(impm_sim* h, double* aos, int64_t n, int64_t stride) {
+  SIM;
+  API_BEGIN(sim)
+  sim->get_particles(aos, n, stride);
+  API_END(sim)
+}
+impm_status impm_sim_set_particle_field(impm_sim* h, int32_t field, const double* vals) {
+  SIM;
+  API_BEGIN(sim)
+  sim->set_particle_field(field, vals);
+  API_END(sim)
+}
+impm_status impm_sim_n_particles(impm_sim* h, int64_t* n) {
+  SIM;
+  API_BEGIN(sim)
+  *n = sim->P;
+  API_END(sim)
+}
+impm_status impm_sim_set_fixed(impm_sim* h, const uint8_t* fixed) {
+  SIM;
+  API_BEGIN(sim)
+  CK(cudaMemcpyAsync(sim->fixed.p, fixed, sim->NF(), cudaMemcpyHostToDevice, sim->s));
+  sim->sync();
+  sim->step_built = sim->opt.total_lagrangian ? sim->step_built : false;
+  API_END(sim)
+}
+impm_status impm_sim_set_gravity(impm_sim* h, const double* gv) {
+  SIM;
+  API_BEGIN(sim)
+  for (int a = 0; a < 3; ++a) sim->gravity[a] = a < sim->D ? gv[a] : 0.0;
+  API_END(sim)
+}
+impm_status impm_sim_set_options(impm_sim* h, const impm_options* o) {
+  SIM;
+  API_BEGIN(sim)
+  sim->set_options(o);
+  API_END(sim)
+}
+impm_status impm_sim_begin_step(impm_sim* h) {
+  SIM;
+  API_BEGIN(sim)
+  sim->begin_step();
+  API_END(sim)
+}
+impm_status impm_sim_n_dofs(impm_sim* h, int32_t* n) {
+  SIM;
+  API_BEGIN(sim)
+  *n = sim->n_dofs;
+  API_END(sim)
+}
+impm_status impm_sim_dof_map(impm_sim* h, int32_t* dof_of, int32_t* node_of, int32_t* field_of) {
+  SIM;
+  API_BEGIN(sim)
+  if (dof_of) CK(cudaMemcpyAsync(dof_of, sim->dof_of.p, sizeof(int) * sim->NF(), cudaMemcpyDeviceToHost, sim->s));
+  if (node_of && sim->n_dofs)
+    CK(cudaMemcpyAsync(node_of, sim->node_of.p, sizeof(int) * sim->n_dofs, cudaMemcpyDeviceToHost, sim->s));
+  if (field_of && sim->n_dofs)
+    CK(cudaMemcpyAsync(field_of, sim->field_of.p, sizeof(int) * sim->n_dofs, cudaMemcpyDeviceToHost, sim->s));
+  sim->sync();
+  API_END(sim)
+}
+impm_status impm_sim_node_mass(impm_sim* h, double* m) {
+  SIM;
+  API_BEGIN(sim)
+  CK(cudaMemcpyAsync(m, sim->mass.p, sizeof(double) * sim->g.N, cudaMemcpyDeviceToHost, sim->s));
+  sim->sync();
+  API_END(sim)
+}
+impm_status impm_sim_colour_groups(impm_sim* h, int32_t* group_of_dof, int32_t* n_groups) {
+  SIM;
+  API_BEGIN(sim)
+  // group = field * 5^D + sum_a (idx_a mod 5) 5^(D-1-a)   (jacobian.hpp:101-110)
+  const int S = ipow_c(5, sim->D);
+  *n_groups = sim->F * S;
+  if (group_of_dof && sim->n_dofs) {
+    std::vector<int> node_of(sim->n_dofs), field_of(sim->n_dofs);
+    CK(cudaMemcpyAsync(node_of.data(), sim->node_of.p, sizeof(int) * sim->n_dofs, cudaMemcpyDeviceToHost, sim->s));
+    CK(cudaMemcpyAsync(field_of.data(), sim->field_of.p, sizeof(int) * sim->n_dofs, cudaMemcpyDeviceToHost, sim->s));
+    sim->sync();
+    for (int d = 0; d < sim->n_dofs; ++d) {
+      int off = 0;
+      for (int a = 0; a < sim->D; ++a) off = off * 5 + ((node_of[d] / sim->g.stride[a]) % sim->g.nodes[a]) % 5;
+      group_of_dof[d] = field_of[d] * S + off;
+    }
+  }
+  API_END(sim)
+}
+impm_status impm_sim_p2g_map(impm_sim* h, const double* per_particle, double* out) {
+  SIM;
+  API_BEGIN(sim)
+  if (!sim->step_built) throw SimError(IMPM_ERR_CONFIG, "p2g_map before begin_step");
+  DBuf<double> f, o;
+  f.ensure(std::max(sim->P, 1));
+  o.ensure(sim->g.N);
+  DBuf<double> fo;
+  fo.ensure(std::max(sim->P, 1));
+  CK(cudaMemcpyAsync(fo.p, per_particle, sizeof(double) * sim->P, cudaMemcpyHostToDevice, sim->s));
+  k_set_field<<<blocks_for(sim->P), kThreads, 0, sim->s>>>(f.p, fo.p, sim->orig.p, sim->P);
+  sim->dispatch([&](auto Dc, auto Sc) {
+    constexpr int DD = decltype(Dc)::value, SH = decltype(Sc)::value;
+    k_p2g_map<DD, SH><<<blocks_for(sim->g.N), kThreads, 0, sim->s>>>(sim->g, sim->pd.p, sim->cap, sim->xs.p,
+                                                                      sim->bin_start.p, sim->sup.p, sim->mass.p, f.p,
+                                                                      o.p);
+  });
+  CKL();
+  CK(cudaMemcpyAsync(out, o.p, sizeof(double) * sim->g.N, cudaMemcpyDeviceToHost, sim->s));
+  sim->sync();
+  API_END(sim)
+}
+impm_status impm_sim_residual(impm_sim* h, const double* uh, double load_scale, double* rh) {
+  SIM;
+  API_BEGIN(sim)
+  if (!sim->step_built) throw SimError(IMPM_ERR_CONFIG, "residual before begin_step");
+  sim->upload_dof_vec(uh, sim->tmp1.p);
+  sim->residual_dev(sim->tmp1.p, load_scale, sim->rtry.p);
+  sim->download_dof_vec(sim->rtry.p, rh);
+  API_END(sim)
+}
+impm_status impm_sim_jacobian_csr(impm_sim* h, const double* uh, double load_scale, int64_t* nnz, int64_t* row_ptr,
+                                  int32_t* cols, double* vals) {
+  SIM;
+  API_BEGIN(sim)
+  (void)load_scale;  // J does not depend on the load scale (external loads are constant in u)
+  if (!sim->step_built) throw SimError(IMPM_ERR_CONFIG, "jacobian before begin_step");
+  if (row_ptr && uh) {
+    sim->upload_dof_vec(uh, sim->tmp1.p);
+    sim->jacobian_dev(sim->tmp1.p);
+    sim->sync();
+    sim->prof.flush();
+  }
+  sim->export_csr(nnz, row_ptr, cols, vals);
+  API_END(sim)
+}
+impm_status impm_sim_linear_solve(impm_sim* h, const double* uh, double load_scale, const double* rhs, double* delta,
+                                  int32_t* kit) {
+  SIM;
+  API_BEGIN(sim)
+  (void)load_scale;
+  if (!sim->step_built) throw SimError(IMPM_ERR_CONFIG, "linear_solve before begin_step");
+  sim->upload_dof_vec(uh, sim->tmp1.p);
+  sim->jacobian_dev(sim->tmp1.p);
+  sim->upload_dof_vec(rhs, sim->tmp2.p);
+  const int it = sim->solve_dev(sim->tmp2.p, sim->delta.p);
+  if (kit) *kit = it;
+  sim->download_dof_vec(sim->delta.p, delta);
+  sim->prof.flush();
+  API_END(sim)
+}
+impm_status impm_sim_newton_solve(impm_sim* h, double load_scale, impm_step_record* rec) {
+  SIM;
+  API_BEGIN(sim)
+  sim->newton_solve(load_scale, rec);
+  API_END(sim)
+}
+impm_status impm_sim_commit_step(impm_sim* h) {
+  SIM;
+  API_BEGIN(sim)
+  sim->commit_step();
+  API_END(sim)
+}
+impm_status impm_sim_step(impm_sim* h, double load_scale, impm_step_record* rec) {
+  SIM;
+  API_BEGIN(sim)
+  sim->begin_step();
+  sim->newton_solve(load_scale, rec);
+  sim->commit_step();
+  API_END(sim)
+}
+impm_status impm_sim_nodal_solution(impm_sim* h, double* uh) {
+  SIM;
+  API_BEGIN(sim)
+  sim->download_dof_vec(sim->u.p, uh);
+  API_END(sim)
+}
+impm_status impm_sim_set_nodal_solution(impm_sim* h, const double* uh) {
+  SIM;
+  API_BEGIN(sim)
+  sim->upload_dof_vec(uh, sim->u.p);
+  sim->sync();
+  API_END(sim)
+}
+impm_status impm_sim_last_error(impm_sim* h, char* msg, size_t cap, double* history, int32_t* hist_len) {
+  SIM;
+  if (!sim) {
+    if (msg && cap) std::snprintf(msg, cap, "%s", g_create_error.c_str());
+    return IMPM_OK;
+  }
+  if (msg && cap) std::snprintf(msg, cap, "%s", sim->err_msg.c_str());
+  if (hist_len) {
+    const int n = static_cast<int>(sim->err_hist.size());
+    if (history)
+      for (int i = 0; i < std::min(n, *hist_len); ++i) history[i] = sim->err_hist[i];
+    *hist_len = n;
+  }
+  return IMPM_OK;
+}
+impm_status impm_sim_kernel_times(impm_sim* h, const char** names, double* ms, int64_t* launches, int32_t* n,
+                                  int32_t reset) {
+  SIM;
+  API_BEGIN(sim)
+  sim->sync();
+  sim->prof.flush();
+  *n = kcCount;
+  for (int i = 0; i < kcCount; ++i) {
+    if (names) names[i] = kClassNames[i];
+    if (ms) ms[i] = sim->prof.ms[i];
+    if (launches) launches[i] = sim->prof.launches[i];
+  }
+  if (reset) {
+    for (int i = 0; i < kcCount; ++i) {
+      sim->prof.ms[i] = 0;
+      sim->prof.launches[i] = 0;
+    }
+  }
+  API_END(sim)
+}
+impm_status impm_sim_matrix_info(impm_sim* h, int64_t* n_rows, int64_t* row_values, int64_t* ref_nnz) {
+  SIM;
+  API_BEGIN(sim)
+  if (n_rows) *n_rows = sim->n_act;
+  if (row_values) *row_values = sim->row_len;
+  if (ref_nnz) *ref_nnz = sim->step_built ? sim->ref_nnz() : 0;
+  API_END(sim)
+}
+
+}  // extern "C"
