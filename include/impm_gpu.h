@@ -105,6 +105,10 @@ typedef struct impm_sim impm_sim; /* opaque: one MpmSim<D> on one device */
 /* version / capability */
 const char* impm_version(void);
 int32_t impm_particle_doubles(int32_t dim); /* 6D+22+D*D */
+/* kernel launches this library has issued since load (all sims, all devices) */
+int64_t impm_launch_count(void);
+/* message of the last failed impm_sim_create on this thread */
+const char* impm_create_error(void);
 
 /* MpmSim(Grid, particles, MaterialSpec, SolverOptions) (mpm_solver.hpp:63-68) */
 impm_status impm_sim_create(const impm_grid* grid, const impm_material* mat, const impm_options* opt,

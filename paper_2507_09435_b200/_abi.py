@@ -68,6 +68,7 @@ _SIGNATURES = {
     "impm_version": (ctypes.c_char_p, []),
     "impm_particle_doubles": (c_int32, [c_int32]),
     "impm_create_error": (ctypes.c_char_p, []),
+    "impm_launch_count": (c_int64, []),
     "impm_sim_create": (c_int32, [_P(Grid), _P(Material), _P(Options), c_int32, _P(c_void_p)]),
     "impm_sim_destroy": (c_int32, [c_void_p]),
     "impm_sim_set_stream": (c_int32, [c_void_p, c_void_p]),

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <climits>
 #include <cmath>
@@ -23,6 +24,9 @@
 using namespace impm_gpu;
 
 namespace {
+
+// kernel launches issued by this library (every <<<>>> is followed by ++g_launches)
+std::atomic<long long> g_launches{0};
 
 // ----------------------------------------------------------- errors -----
 struct SimError : std::runtime_error {
@@ -308,7 +312,7 @@ struct Sim {
     staging.ensure(std::max<int64_t>(1, n * (stride / 8)));
     if (n > 0) {
       CK(cudaMemcpyAsync(staging.p, aos, n * stride, cudaMemcpyHostToDevice, s));
-      k_aos_to_soa<<<blocks_for(n), kThreads, 0, s>>>(staging.p, stride / 8, P, ND, pd.p, cap, orig.p);
+      k_aos_to_soa<<<blocks_for(n), kThreads, 0, s>>>(staging.p, stride / 8, P, ND, pd.p, cap, orig.p); ++g_launches;
       CKL();
     }
     sync();
@@ -322,7 +326,7 @@ struct Sim {
     DBuf<double> staging;
     staging.ensure(n * (stride / 8));
     if (stride != ND * 8) CK(cudaMemcpyAsync(staging.p, aos, n * stride, cudaMemcpyHostToDevice, s));
-    k_soa_to_aos<<<blocks_for(n), kThreads, 0, s>>>(pd.p, cap, P, ND, orig.p, staging.p, stride / 8);
+    k_soa_to_aos<<<blocks_for(n), kThreads, 0, s>>>(pd.p, cap, P, ND, orig.p, staging.p, stride / 8); ++g_launches;
     CKL();
     CK(cudaMemcpyAsync(aos, staging.p, n * stride, cudaMemcpyDeviceToHost, s));
     sync();
@@ -332,7 +336,7 @@ struct Sim {
     DBuf<double> tmp;
     tmp.ensure(std::max(P, 1));
     CK(cudaMemcpyAsync(tmp.p, vals_h, sizeof(double) * P, cudaMemcpyHostToDevice, s));
-    k_set_field<<<blocks_for(P), kThreads, 0, s>>>(pd.p + field * cap, tmp.p, orig.p, P);
+    k_set_field<<<blocks_for(P), kThreads, 0, s>>>(pd.p + field * cap, tmp.p, orig.p, P); ++g_launches;
     CKL();
     sync();
     step_built = false;
@@ -343,12 +347,12 @@ struct Sim {
   void scan(const int* in, int64_t n, T* out, DBuf<T>& sums_buf, T* total_slot) {
     const int64_t nb = (n + 4095) / 4096;
     sums_buf.ensure(nb + 1);
-    k_scan_block<T><<<static_cast<unsigned>(std::max<int64_t>(nb, 1)), 1024, 0, s>>>(in, n, out, sums_buf.p);
+    k_scan_block<T><<<static_cast<unsigned>(std::max<int64_t>(nb, 1)), 1024, 0, s>>>(in, n, out, sums_buf.p); ++g_launches;
     CKL();
-    k_scan_sums<T><<<1, 1024, 0, s>>>(sums_buf.p, static_cast<int>(nb), sums_buf.p + nb);
+    k_scan_sums<T><<<1, 1024, 0, s>>>(sums_buf.p, static_cast<int>(nb), sums_buf.p + nb); ++g_launches;
     CKL();
     k_scan_add<T><<<blocks_for(std::max<int64_t>(n, 1)), kThreads, 0, s>>>(out, n, sums_buf.p, sums_buf.p + nb,
-                                                                           total_slot);
+                                                                           total_slot); ++g_launches;
     CKL();
   }
 
@@ -382,7 +386,7 @@ struct Sim {
       dispatch([&](auto Dc, auto Sc) {
         constexpr int DD = decltype(Dc)::value, SH = decltype(Sc)::value;
         if (P > 0) {
-          k_support<DD, SH><<<blocks_for(P), kThreads, 0, s>>>(pd.p, cap, P, g, orig.p, key.p, sup.p, xs.p, st.p);
+          k_support<DD, SH><<<blocks_for(P), kThreads, 0, s>>>(pd.p, cap, P, g, orig.p, key.p, sup.p, xs.p, st.p); ++g_launches;
           CKL();
         }
       });
@@ -396,16 +400,16 @@ struct Sim {
       // counting sort by first support node (K1)
       CK(cudaMemsetAsync(bin_count.p, 0, sizeof(int) * (N + 1), s));
       if (P > 0) {
-        k_bin_count<<<blocks_for(P), kThreads, 0, s>>>(key.p, P, bin_count.p, rank.p);
+        k_bin_count<<<blocks_for(P), kThreads, 0, s>>>(key.p, P, bin_count.p, rank.p); ++g_launches;
         CKL();
       }
       scan<int>(bin_count.p, N, bin_start.p, scan_sums_i, bin_start.p + N);
       if (P > 0) {
-        k_bin_scatter<<<blocks_for(P), kThreads, 0, s>>>(key.p, rank.p, bin_start.p, P, perm.p);
+        k_bin_scatter<<<blocks_for(P), kThreads, 0, s>>>(key.p, rank.p, bin_start.p, P, perm.p); ++g_launches;
         CKL();
-        k_bin_sort<<<blocks_for(N), kThreads, 0, s>>>(bin_start.p, N, perm.p);
+        k_bin_sort<<<blocks_for(N), kThreads, 0, s>>>(bin_start.p, N, perm.p); ++g_launches;
         CKL();
-        k_perm_check<<<blocks_for(P), kThreads, 0, s>>>(perm.p, P, st.p);
+        k_perm_check<<<blocks_for(P), kThreads, 0, s>>>(perm.p, P, st.p); ++g_launches;
         CKL();
       }
     }
@@ -413,9 +417,9 @@ struct Sim {
     if (h_st->perm_moved) {
       Prof::Scope ps(&prof, kcSort);
       dim3 grid(blocks_for(P), ND);
-      k_gather_fields<<<grid, kThreads, 0, s>>>(pd.p, pd_tmp.p, cap, perm.p, P);
+      k_gather_fields<<<grid, kThreads, 0, s>>>(pd.p, pd_tmp.p, cap, perm.p, P); ++g_launches;
       CKL();
-      k_gather_int<<<blocks_for(P), kThreads, 0, s>>>(orig.p, orig_tmp.p, perm.p, P);
+      k_gather_int<<<blocks_for(P), kThreads, 0, s>>>(orig.p, orig_tmp.p, perm.p, P); ++g_launches;
       CKL();
       std::swap(pd.p, pd_tmp.p);
       std::swap(pd.cap, pd_tmp.cap);
@@ -423,7 +427,7 @@ struct Sim {
       std::swap(orig.cap, orig_tmp.cap);
       dispatch([&](auto Dc, auto Sc) {
         constexpr int DD = decltype(Dc)::value, SH = decltype(Sc)::value;
-        k_support<DD, SH><<<blocks_for(P), kThreads, 0, s>>>(pd.p, cap, P, g, orig.p, key.p, sup.p, xs.p, st.p);
+        k_support<DD, SH><<<blocks_for(P), kThreads, 0, s>>>(pd.p, cap, P, g, orig.p, key.p, sup.p, xs.p, st.p); ++g_launches;
         CKL();
       });
     }
@@ -432,11 +436,11 @@ struct Sim {
       dispatch([&](auto Dc, auto Sc) {
         constexpr int DD = decltype(Dc)::value, SH = decltype(Sc)::value;
         if (P > 0) {
-          k_bext<DD><<<blocks_for(P), kThreads, 0, s>>>(pd.p, cap, P, gravity[0], gravity[1], gravity[2], bext.p, st.p);
+          k_bext<DD><<<blocks_for(P), kThreads, 0, s>>>(pd.p, cap, P, gravity[0], gravity[1], gravity[2], bext.p, st.p); ++g_launches;
           CKL();
         }
         k_node_mass<DD, DD, SH><<<blocks_for(N), kThreads, 0, s>>>(g, pd.p, cap, xs.p, bin_start.p, sup.p, fixed.p,
-                                                                    st.p, mass.p, act_flag.p, free_flag.p);
+                                                                    st.p, mass.p, act_flag.p, free_flag.p); ++g_launches;
         CKL();
       });
     }
@@ -444,10 +448,10 @@ struct Sim {
       Prof::Scope ps(&prof, kcDof);
       scan<int>(free_flag.p, NF(), free_scan.p, scan_sums_i, free_scan.p + NF());
       k_dof_finalize<<<blocks_for(NF()), kThreads, 0, s>>>(static_cast<int>(NF()), F, free_flag.p, free_scan.p,
-                                                             dof_of.p, node_of.p, field_of.p, freem.p);
+                                                             dof_of.p, node_of.p, field_of.p, freem.p); ++g_launches;
       CKL();
       scan<int>(act_flag.p, N, act_scan.p, scan_sums_i, act_scan.p + N);
-      k_act_finalize<<<blocks_for(N), kThreads, 0, s>>>(N, act_flag.p, act_scan.p, act_idx.p, act_list.p);
+      k_act_finalize<<<blocks_for(N), kThreads, 0, s>>>(N, act_flag.p, act_scan.p, act_idx.p, act_list.p); ++g_launches;
       CKL();
     }
     int counts[2];
@@ -477,16 +481,16 @@ struct Sim {
       if (P > 0) {
         Prof::Scope ps(&prof, kcResP);
         k_residual_particles<DD, SH><<<blocks_for(P), kThreads, 0, s>>>(g, pd.p, cap, P, xs.p, key.p, sup.p, orig.p,
-                                                                        ud, mp, opt.total_lagrangian, Pst.p, st.p);
+                                                                        ud, mp, opt.total_lagrangian, Pst.p, st.p); ++g_launches;
         CKL();
       }
       {
         Prof::Scope ps(&prof, kcResN);
         k_residual_nodes<DD, SH><<<kRedBlocks, kThreads, 0, s>>>(g, pd.p, cap, xs.p, bin_start.p, sup.p, Pst.p,
                                                                  bext.p, act_flag.p, freem.p, load_scale, rd,
-                                                                 partials.p);
+                                                                 partials.p); ++g_launches;
         CKL();
-        k_finalize_sum<1><<<1, 1024, 0, s>>>(partials.p, kRedBlocks, &st.p->norm2);
+        k_finalize_sum<1><<<1, 1024, 0, s>>>(partials.p, kRedBlocks, &st.p->norm2); ++g_launches;
         CKL();
       }
     });
@@ -506,7 +510,7 @@ struct Sim {
         Prof::Scope ps(&prof, kcTangent);
         constexpr int K = DD == 3 ? 3 : DD * DD;
         k_tangent<DD, SH, K><<<blocks_for(P, 128), 128, 0, s>>>(g, pd.p, cap, P, xs.p, key.p, sup.p, ud, mp,
-                                                                opt.total_lagrangian, Atan.p);
+                                                                opt.total_lagrangian, Atan.p); ++g_launches;
         CKL();
       }
       if (n_act > 0) {
@@ -517,7 +521,7 @@ struct Sim {
         auto kern = k_assemble<DD, SH, W>;
         if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         kern<<<blocks_for(n_act, W), W * 32, smem, s>>>(g, pd.p, cap, xs.p, bin_start.p, sup.p, Atan.p, act_list.p,
-                                                        n_act, freem.p, vals.p, row_len, dinv.p);
+                                                        n_act, freem.p, vals.p, row_len, dinv.p); ++g_launches;
         CKL();
       }
     });
@@ -531,7 +535,7 @@ struct Sim {
       constexpr int DD = decltype(Dc)::value;
       constexpr int W = 8;
       k_spmv<DD, DD, W><<<kRedBlocks, W * 32, 0, s>>>(g, act_list.p, n_act, vals.p, row_len, x, freem.p, y, dotv,
-                                                      parts, dflag.p);
+                                                      parts, dflag.p); ++g_launches;
       CKL();
     };
     if (D == 1) launch(IC<1>{});
@@ -547,11 +551,11 @@ struct Sim {
     CK(cudaMemsetAsync(dflag.p, 0, sizeof(int), s));
     {
       Prof::Scope ps(&prof, kcKrylov);
-      k_cg_init<FF><<<kRedBlocks, kThreads, 0, s>>>(N, act_idx.p, dinv.p, b, x, kr.p, kz.p, kp.p, partials.p);
+      k_cg_init<FF><<<kRedBlocks, kThreads, 0, s>>>(N, act_idx.p, dinv.p, b, x, kr.p, kz.p, kp.p, partials.p); ++g_launches;
       CKL();
-      k_finalize_sum<2><<<1, 1024, 0, s>>>(partials.p, kRedBlocks, sums.p);
+      k_finalize_sum<2><<<1, 1024, 0, s>>>(partials.p, kRedBlocks, sums.p); ++g_launches;
       CKL();
-      k_cg_start<<<1, 1, 0, s>>>(sums.p, sc.p, rtol2);
+      k_cg_start<<<1, 1, 0, s>>>(sums.p, sc.p, rtol2); ++g_launches;
       CKL();
     }
     // b == 0 -> x = 0
@@ -564,13 +568,13 @@ struct Sim {
       for (int i = 0; i < batch; ++i) {
         spmv(kp.p, kq.p, kp.p, partials.p);
         Prof::Scope ps(&prof, kcKrylov);
-        k_finalize_sum<1><<<1, 1024, 0, s>>>(partials.p, kRedBlocks, sums.p);
-        k_cg_alpha<<<1, 1, 0, s>>>(sums.p, sc.p, dflag.p);
+        k_finalize_sum<1><<<1, 1024, 0, s>>>(partials.p, kRedBlocks, sums.p); ++g_launches;
+        k_cg_alpha<<<1, 1, 0, s>>>(sums.p, sc.p, dflag.p); ++g_launches;
         k_cg_update<FF><<<kRedBlocks, kThreads, 0, s>>>(N, act_idx.p, dinv.p, sc.p, dflag.p, x, kr.p, kz.p, kp.p,
-                                                        kq.p, partials.p);
-        k_finalize_sum<2><<<1, 1024, 0, s>>>(partials.p, kRedBlocks, sums.p);
-        k_cg_beta<<<1, 1, 0, s>>>(sums.p, sc.p, dflag.p, rtol2, max_it);
-        k_cg_p<FF><<<blocks_for(N), kThreads, 0, s>>>(N, act_idx.p, sc.p, dflag.p, kz.p, kp.p);
+                                                        kq.p, partials.p); ++g_launches;
+        k_finalize_sum<2><<<1, 1024, 0, s>>>(partials.p, kRedBlocks, sums.p); ++g_launches;
+        k_cg_beta<<<1, 1, 0, s>>>(sums.p, sc.p, dflag.p, rtol2, max_it); ++g_launches;
+        k_cg_p<FF><<<blocks_for(N), kThreads, 0, s>>>(N, act_idx.p, sc.p, dflag.p, kz.p, kp.p); ++g_launches;
         CKL();
       }
       CK(cudaMemcpyAsync(&done, dflag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -592,8 +596,8 @@ struct Sim {
 
   // host-scalar BiCGStab (right block-Jacobi preconditioning), nonsymmetric path
   double dot(const double* a, const double* b) {
-    k_dot2<<<kRedBlocks, kThreads, 0, s>>>(NF(), a, b, nullptr, nullptr, partials.p);
-    k_finalize_sum<2><<<1, 1024, 0, s>>>(partials.p, kRedBlocks, sums.p);
+    k_dot2<<<kRedBlocks, kThreads, 0, s>>>(NF(), a, b, nullptr, nullptr, partials.p); ++g_launches;
+    k_finalize_sum<2><<<1, 1024, 0, s>>>(partials.p, kRedBlocks, sums.p); ++g_launches;
     CKL();
     double h[2];
     CK(cudaMemcpyAsync(h, sums.p, sizeof(h), cudaMemcpyDeviceToHost, s));
@@ -601,12 +605,12 @@ struct Sim {
     return h[0];
   }
   void axpbypcz(double a, const double* x, double b, double* y, double c = 0.0, const double* z = nullptr) {
-    k_axpbypcz<<<kRedBlocks, kThreads, 0, s>>>(NF(), a, x, b, y, c, z);
+    k_axpbypcz<<<kRedBlocks, kThreads, 0, s>>>(NF(), a, x, b, y, c, z); ++g_launches;
     CKL();
   }
   template <int FF>
   void precond(const double* rin, double* z) {
-    k_precond<FF><<<blocks_for(g.N), kThreads, 0, s>>>(g.N, act_idx.p, dinv.p, rin, z);
+    k_precond<FF><<<blocks_for(g.N), kThreads, 0, s>>>(g.N, act_idx.p, dinv.p, rin, z); ++g_launches;
     CKL();
   }
   template <int FF>
@@ -690,7 +694,7 @@ struct Sim {
     if (n_dofs == 0) return ref_nnz_cache = 0;
     dispatch([&](auto Dc, auto) {
       constexpr int DD = decltype(Dc)::value;
-      k_csr_count<DD, DD><<<blocks_for(n_dofs), kThreads, 0, s>>>(g, n_dofs, node_of.p, dof_of.p, rowlen.p);
+      k_csr_count<DD, DD><<<blocks_for(n_dofs), kThreads, 0, s>>>(g, n_dofs, node_of.p, dof_of.p, rowlen.p); ++g_launches;
       CKL();
     });
     int64_t tot = 0;
@@ -826,8 +830,8 @@ struct Sim {
     CK(cudaMemsetAsync(dst, 0, sizeof(double) * NF(), s));
     if (n_dofs == 0) return;
     tmp2.ensure(NF());
-    k_grid_to_dof<<<blocks_for(n_dofs), kThreads, 0, s>>>(n_dofs, src, node_of.p, field_of.p, F, kt.p);
-    k_dof_to_grid<<<blocks_for(n_dofs), kThreads, 0, s>>>(n_dofs, kt.p, node_of.p, field_of.p, F, dst);
+    k_grid_to_dof<<<blocks_for(n_dofs), kThreads, 0, s>>>(n_dofs, src, node_of.p, field_of.p, F, kt.p); ++g_launches;
+    k_dof_to_grid<<<blocks_for(n_dofs), kThreads, 0, s>>>(n_dofs, kt.p, node_of.p, field_of.p, F, dst); ++g_launches;
     CKL();
   }
 
@@ -843,7 +847,7 @@ struct Sim {
       if (P > 0) {
         Prof::Scope ps(&prof, kcCommit);
         k_commit<DD, SH><<<blocks_for(P), kThreads, 0, s>>>(g, pd.p, cap, P, xs.p, key.p, sup.p, orig.p, u.p, mp,
-                                                            opt.total_lagrangian, st.p);
+                                                            opt.total_lagrangian, st.p); ++g_launches;
         CKL();
       }
     });
@@ -864,12 +868,12 @@ struct Sim {
     CK(cudaMemsetAsync(gvec, 0, sizeof(double) * NF(), s));
     if (n_dofs == 0) return;
     CK(cudaMemcpyAsync(kt.p, h, sizeof(double) * n_dofs, cudaMemcpyHostToDevice, s));
-    k_dof_to_grid<<<blocks_for(n_dofs), kThreads, 0, s>>>(n_dofs, kt.p, node_of.p, field_of.p, F, gvec);
+    k_dof_to_grid<<<blocks_for(n_dofs), kThreads, 0, s>>>(n_dofs, kt.p, node_of.p, field_of.p, F, gvec); ++g_launches;
     CKL();
   }
   void download_dof_vec(const double* gvec, double* h) {
     if (n_dofs == 0) return;
-    k_grid_to_dof<<<blocks_for(n_dofs), kThreads, 0, s>>>(n_dofs, gvec, node_of.p, field_of.p, F, kt.p);
+    k_grid_to_dof<<<blocks_for(n_dofs), kThreads, 0, s>>>(n_dofs, gvec, node_of.p, field_of.p, F, kt.p); ++g_launches;
     CKL();
     CK(cudaMemcpyAsync(h, kt.p, sizeof(double) * n_dofs, cudaMemcpyDeviceToHost, s));
     sync();
@@ -894,7 +898,7 @@ struct Sim {
       constexpr int DD = decltype(Dc)::value;
       k_csr_fill<DD, DD><<<blocks_for(n_dofs), kThreads, 0, s>>>(g, n_dofs, node_of.p, field_of.p, dof_of.p, act_idx.p,
                                                                  vals.p, row_len, rowptr.p, dcols.p,
-                                                                 vals_h ? dvals.p : nullptr);
+                                                                 vals_h ? dvals.p : nullptr); ++g_launches;
       CKL();
     });
     if (cols_h) CK(cudaMemcpyAsync(cols_h, dcols.p, sizeof(int32_t) * z, cudaMemcpyDeviceToHost, s));
@@ -933,6 +937,7 @@ thread_local std::string g_create_error;
 extern "C" {
 
 const char* impm_version(void) { return "impm-b200 0.1 (sm_100a, fp64)"; }
+int64_t impm_launch_count(void) { return g_launches.load(); }
 int32_t impm_particle_doubles(int32_t dim) { return 6 * dim + 22 + dim * dim; }
 
 impm_status impm_sim_create(const impm_grid* grid, const impm_material* mat, const impm_options* opt, int32_t device,
@@ -1070,12 +1075,12 @@ impm_status impm_sim_p2g_map(impm_sim* h, const double* per_particle, double* ou
   DBuf<double> fo;
   fo.ensure(std::max(sim->P, 1));
   CK(cudaMemcpyAsync(fo.p, per_particle, sizeof(double) * sim->P, cudaMemcpyHostToDevice, sim->s));
-  k_set_field<<<blocks_for(sim->P), kThreads, 0, sim->s>>>(f.p, fo.p, sim->orig.p, sim->P);
+  k_set_field<<<blocks_for(sim->P), kThreads, 0, sim->s>>>(f.p, fo.p, sim->orig.p, sim->P); ++g_launches;
   sim->dispatch([&](auto Dc, auto Sc) {
     constexpr int DD = decltype(Dc)::value, SH = decltype(Sc)::value;
     k_p2g_map<DD, SH><<<blocks_for(sim->g.N), kThreads, 0, sim->s>>>(sim->g, sim->pd.p, sim->cap, sim->xs.p,
                                                                       sim->bin_start.p, sim->sup.p, sim->mass.p, f.p,
-                                                                      o.p);
+                                                                      o.p); ++g_launches;
   });
   CKL();
   CK(cudaMemcpyAsync(out, o.p, sizeof(double) * sim->g.N, cudaMemcpyDeviceToHost, sim->s));

@@ -1,0 +1,93 @@
+"""Synthetic problems of BASELINE.json's configs.
+
+All use seed_box (particle.hpp:33-69) on the scenario grid convention of the
+reference (origin -h, cells+3 nodes per axis, src/scenarios.cpp:96-98),
+fp64, fixed seeds. Where a config names a model the reference does not have
+(Drucker-Prager, modified Cam-Clay) the pinned substitute of SURVEY.md §8(d)
+is used and the substitution is named in `Problem.note`.
+"""
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .particles import GridSpec, ParticleArray, seed_box
+from .sim import ElasticParams, MaterialSpec, SolverOptions
+
+
+@dataclass
+class Problem:
+    name: str
+    grid: GridSpec
+    particles: np.ndarray
+    material: MaterialSpec
+    options: SolverOptions
+    fixed: np.ndarray
+    gravity: np.ndarray
+    load_steps: int
+    note: str = ""
+    meta: dict = field(default_factory=dict)
+
+
+def _column_fixed(grid: GridSpec, extent):
+    """base fixed, lateral rollers (src/inverse.cpp:33-36 pattern, D-dimensional)."""
+    D = grid.dim
+    pos = grid.node_positions()
+    fixed = np.zeros((pos.shape[0], D), dtype=np.uint8)
+    fixed[pos[:, D - 1] <= 1e-12, :] = 1
+    for a in range(D - 1):
+        side = (pos[:, a] <= 1e-12) | (pos[:, a] >= extent[a] - 1e-12)
+        fixed[side, a] = 1
+    return fixed.reshape(-1)
+
+
+def _strip_traction(parts, D, extent, frac, t_hat, axes=None):
+    """traction on the top particle layer under a centred strip/patch
+    (src/inverse.cpp:45-61 pattern); axes = lateral axes the strip is narrow in."""
+    pa = ParticleArray(parts, D)
+    X = pa.X
+    top = X[:, D - 1].max()
+    sel = X[:, D - 1] >= top - 1e-9
+    axes = list(range(D - 1)) if axes is None else axes
+    area = 1.0
+    for a in range(D - 1):
+        if a in axes:
+            lo, hi = 0.5 * extent[a] * (1 - frac), 0.5 * extent[a] * (1 + frac)
+            sel &= (X[:, a] >= lo) & (X[:, a] <= hi)
+            area *= extent[a] * frac
+        else:
+            area *= extent[a]
+    n = int(sel.sum())
+    pa.traction_force[sel, D - 1] = -t_hat * area / max(n, 1)
+    return n
+
+
+def column2d_nh(cells=64, ppc=2, h=1.0, steps=10):
+    """cfg 1: 2D neo-Hookean column under self-weight, 64x64 cells, ~16K particles."""
+    grid = GridSpec(2, (-h, -h), h, (cells + 3, cells + 3))
+    W = cells * h
+    parts = seed_box(grid, (0.0, 0.0), (W, W), ppc, 2000.0)
+    mat = MaterialSpec("neo_hookean", ElasticParams(10e6, 0.3))
+    return Problem("cfg1_column2d_nh", grid, parts, mat, SolverOptions(tol=1e-10), _column_fixed(grid, (W, W)),
+                   np.array([0.0, -9.81]), steps, note="GIMP transfer (pinned); B-spline variant unpinned")
+
+
+def footing3d(cells=(128, 128, 64), ppc=2, h=0.5, steps=20, t_hat=100e3, frac=0.125, E=10e6, nu=0.3):
+    """cfg 4 / cfg 5 slab: 3D strip footing, 128x128x64 cells, ppc 2 (8,388,608
+    particles). Modified Cam-Clay is absent from the reference: the pinned
+    substitute is neo-Hookean; the rigid footing is a strip
+    traction on the top layer (the reference has no contact)."""
+    D = 3
+    grid = GridSpec(3, (-h, -h, -h), h, tuple(c + 3 for c in cells))
+    ext = tuple(c * h for c in cells)
+    parts = seed_box(grid, (0.0, 0.0, 0.0), ext, ppc, 2000.0)
+    n_strip = _strip_traction(parts, D, ext, frac, t_hat, axes=[0])
+    mat = MaterialSpec("neo_hookean", ElasticParams(E, nu))
+    return Problem("cfg4_footing3d_nh", grid, parts, mat, SolverOptions(tol=1e-10), _column_fixed(grid, ext),
+                   np.array([0.0, 0.0, -9.81]), steps,
+                   note="neo-Hookean substitute for modified Cam-Clay (unpinned); strip traction footing",
+                   meta={"strip_particles": n_strip})
+
+
+def by_name(name, **kw):
+    table = {"cfg1": column2d_nh, "cfg4": footing3d, "cfg5": footing3d}
+    return table[name](**kw)
