@@ -69,6 +69,9 @@ typedef enum impm_shape_kind { IMPM_SHAPE_GIMP = 1, IMPM_SHAPE_BSPLINE2 = 2 } im
 /* Linear solver behind the sparse_lu_solve seam (src/linear_solver.cpp:11-88). */
 typedef enum impm_krylov_kind { IMPM_KRYLOV_AUTO = 0, IMPM_KRYLOV_CG = 1, IMPM_KRYLOV_BICGSTAB = 2 } impm_krylov_kind;
 
+/* Preconditioner of the Krylov solve. */
+typedef enum impm_precond_kind { IMPM_PRECOND_MG = 0, IMPM_PRECOND_BLOCK_JACOBI = 1 } impm_precond_kind;
+
 /* impm::SolverOptions (mpm_solver.hpp:27-36) + GPU linear-solver knobs. */
 typedef struct impm_options {
   double tol;                 /* relative residual (1e-11) */
@@ -80,6 +83,8 @@ typedef struct impm_options {
   double krylov_rtol;         /* relative true-residual target (1e-12) */
   int32_t krylov_max_iter;    /* 0 => 10*n_dofs capped at 20000 */
   int32_t profile;            /* 1: per-kernel-class CUDA-event timing */
+  int32_t precond;            /* impm_precond_kind */
+  int32_t mg_smooth;          /* multigrid pre/post block-Jacobi sweeps (0 => 2) */
 } impm_options;
 
 /* impm::StepRecord (mpm_solver.hpp:38-46) + GPU counters. rel_residuals is

@@ -38,6 +38,8 @@ class Options(ctypes.Structure):
         ("krylov_rtol", c_double),
         ("krylov_max_iter", c_int32),
         ("profile", c_int32),
+        ("precond", c_int32),
+        ("mg_smooth", c_int32),
     ]
 
 

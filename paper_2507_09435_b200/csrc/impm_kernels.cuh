@@ -24,6 +24,10 @@ namespace impm_gpu {
 
 __host__ __device__ constexpr int ipow_c(int b, int e) { return e == 0 ? 1 : b * ipow_c(b, e - 1); }
 __host__ __device__ constexpr int pad4(int x) { return (x + 3) / 4 * 4; }
+// Compacted rows are stored component-major: [c][block pos][d], each
+// component chunk padded to an even length (16-byte aligned double2 loads).
+__host__ __device__ constexpr int cpad(int nzb, int F) { return (nzb * F + 1) & ~1; }
+__host__ __device__ constexpr int row_len_for(int S, int F) { return pad4(F * cpad(S, F)); }
 
 // Particle<D> field offsets (particle.hpp:10-29)
 template <int D>
@@ -641,21 +645,27 @@ __global__ void __launch_bounds__(WARPS * 32) k_assemble(GridC g, const double* 
                                                          const int* __restrict__ sup, const double* __restrict__ A,
                                                          const int* __restrict__ act_list, int n_act,
                                                          const uint8_t* __restrict__ freem, double* __restrict__ vals,
-                                                         int64_t row_len, double* __restrict__ dinv) {
+                                                         int64_t row_len, double* __restrict__ dinv,
+                                                         uint8_t* __restrict__ row_slots, int* __restrict__ row_nzb,
+                                                         unsigned long long* __restrict__ nzb_total) {
   constexpr int DD = D * D;
   constexpr int S = ipow_c(5, D);
   constexpr int ACC = S * DD;
   constexpr int NH = D * D * D;
+  constexpr int WS = ACC + NH + (2 * S + 7) / 8;  // doubles per warp: acc, H, touched + slot list bytes
   extern __shared__ double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* acc = smem + warp * (ACC + NH);
+  double* acc = smem + warp * WS;
   double* H = acc + ACC;
+  uint8_t* touched = reinterpret_cast<uint8_t*>(H + NH);
+  uint8_t* clist = touched + S;
   const int row = blockIdx.x * WARPS + warp;
   if (row >= n_act) return;
   const int k = act_list[row];
   int kidx[3];
   unflat<D>(g, k, kidx);
   for (int j = lane; j < ACC; j += 32) acc[j] = 0.0;
+  for (int j = lane; j < S; j += 32) touched[j] = 0;
   __syncwarp();
   for_each_particle_of_node<D>(g, kidx, bin_start, sup, [&](int p, const int* off) {
     // lanes a*3+i evaluate the 1D weights of axis a at support node i
@@ -729,6 +739,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_assemble(GridC g, const double* 
         slot = slot * 5 + (li[a] - off[a] + 2);
       }
       tensor_weight<D>(w, dw, W, gl);
+      touched[slot] = 1;
       double* blk = acc + slot * DD;
 #pragma unroll
       for (int c = 0; c < D; ++c)
@@ -742,9 +753,31 @@ __global__ void __launch_bounds__(WARPS * 32) k_assemble(GridC g, const double* 
     }
     __syncwarp();
   });
+  // compact the structurally nonzero blocks (touched by a particle pair) in
+  // ascending slot order; the SpMV streams only these
+  int base = 0;
+  for (int s0 = 0; s0 < S; s0 += 32) {
+    const int sl = s0 + lane;
+    const bool f = sl < S && touched[sl];
+    const unsigned m = __ballot_sync(0xffffffffu, f);
+    if (f) {
+      const int pos = base + __popc(m & ((1u << lane) - 1u));
+      clist[pos] = static_cast<uint8_t>(sl);
+      row_slots[static_cast<int64_t>(row) * S + pos] = static_cast<uint8_t>(sl);
+    }
+    base += __popc(m);
+  }
+  __syncwarp();
+  const int nzb = base;
   double* dst = vals + static_cast<int64_t>(row) * row_len;
-  for (int j = lane; j < row_len; j += 32) dst[j] = j < ACC ? acc[j] : 0.0;
+  const int cp = cpad(nzb, D);
+  for (int j = lane; j < D * cp; j += 32) {
+    const int c = j / cp, rem = j - c * cp, pos = rem / D, d = rem - pos * D;
+    dst[j] = rem < nzb * D ? acc[clist[pos] * DD + c * D + d] : 0.0;
+  }
   if (lane == 0) {
+    row_nzb[row] = nzb;
+    atomicAdd(nzb_total, static_cast<unsigned long long>(nzb));
     // masked diagonal block inverse: [D_ff 0; 0 I]^-1
     const double* blk = acc + (S - 1) / 2 * DD;
     bool fr[3];
@@ -762,57 +795,111 @@ __global__ void __launch_bounds__(WARPS * 32) k_assemble(GridC g, const double* 
 }
 
 // -------------------------------------------------------------- K7 SpMV --
-// y = J x on the box BSR (warp per row, coalesced row streaming, x gathered
-// from L1/L2), masked to free DOFs, fused partial of dotv . y.
-template <int D, int F, int WARPS>
+// y = J x on the box BSR: one warp per active row. The row's 5^D neighbour
+// x-records are staged once in shared memory, then the row (S*F*F fp64,
+// 16-byte aligned) is streamed with coalesced 16-byte loads; a per-block
+// table maps value j -> (x slot, output component). Masked to free DOFs;
+// fused partial of dotv . y for the CG step.
+template <int D, int F>
+struct SpmvTab {
+  static constexpr int S = ipow_c(5, D);
+  static constexpr int NV = S * F * F;
+};
+
+// MODE 0: y = A x (+ partial dotv.y); MODE 1: damped block-Jacobi sweep
+// y = x + omega Dinv (b - A x); MODE 2: residual y = b - A x.
+enum SpmvMode { kSpmvY = 0, kSpmvJacobi = 1, kSpmvResid = 2 };
+
+template <int D, int F, int WARPS, int MODE = kSpmvY>
 __global__ void __launch_bounds__(WARPS * 32) k_spmv(GridC g, const int* __restrict__ act_list, int n_act,
                                                      const double* __restrict__ vals, int64_t row_len,
+                                                     const uint8_t* __restrict__ row_slots,
+                                                     const int* __restrict__ row_nzb,
                                                      const double* __restrict__ x, const uint8_t* __restrict__ freem,
                                                      double* __restrict__ y, const double* __restrict__ dotv,
-                                                     double* __restrict__ partials, const int* __restrict__ done) {
+                                                     double* __restrict__ partials, const int* __restrict__ done,
+                                                     const double* __restrict__ b = nullptr,
+                                                     const double* __restrict__ dinv = nullptr, double omega = 0.0) {
   constexpr int S = ipow_c(5, D);
   constexpr int FF = F * F;
+  constexpr int XS = cpad(S, F);
+  __shared__ int offt[S];
+  __shared__ __align__(16) double xs_all[WARPS][XS];
+  for (int sl = threadIdx.x; sl < S; sl += blockDim.x) {
+    int rs = sl, off = 0;
+#pragma unroll
+    for (int a = D - 1; a >= 0; --a) {
+      off += (rs % 5 - 2) * g.stride[a];
+      rs /= 5;
+    }
+    offt[sl] = off;  // stored blocks always couple in-grid nodes
+  }
+  __syncthreads();
   double part[1] = {0.0};
   if (done == nullptr || *done == 0) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* xs = xs_all[warp];
     for (int row = blockIdx.x * WARPS + warp; row < n_act; row += gridDim.x * WARPS) {
       const int k = act_list[row];
-      int kidx[3];
-      unflat<D>(g, k, kidx);
-      double acc[F];
+      const int nzb = row_nzb[row];
+      const int cp = cpad(nzb, F);
+      const uint8_t* rsl = row_slots + static_cast<int64_t>(row) * S;
+      for (int pos = lane; pos < nzb; pos += 32) {
+        const int64_t nb = static_cast<int64_t>(k + offt[rsl[pos]]) * F;
 #pragma unroll
-      for (int c = 0; c < F; ++c) acc[c] = 0.0;
-      const double* rv = vals + static_cast<int64_t>(row) * row_len;
-      for (int j = lane; j < S * FF; j += 32) {
-        const int s = j / FF, rem = j - s * FF, c = rem / F, d = rem - c * F;
-        int rs = s, nb = k;
-        bool ok = true;
+        for (int d = 0; d < F; ++d) xs[pos * F + d] = __ldg(x + nb + d);
+      }
+      if (lane == 0 && cp != nzb * F) xs[nzb * F] = 0.0;
+      __syncwarp();
+      double acc[3] = {0.0, 0.0, 0.0};
+      const double* rbase = vals + static_cast<int64_t>(row) * row_len;
+      const int h = cp >> 1;
 #pragma unroll
-        for (int a = D - 1; a >= 0; --a) {
-          const int rel = rs % 5 - 2;
-          rs /= 5;
-          const int ia = kidx[a] + rel;
-          ok = ok && ia >= 0 && ia < g.nodes[a];
-          nb += rel * g.stride[a];
+      for (int c = 0; c < F; ++c) {
+        const double2* rv = reinterpret_cast<const double2*>(rbase + c * cp);
+        const double2* xv = reinterpret_cast<const double2*>(xs);
+        double a = 0.0;
+#pragma unroll 4
+        for (int j2 = lane; j2 < h; j2 += 32) {
+          const double2 v = __ldcs(rv + j2);  // streamed once: evict-first
+          const double2 xx = xv[j2];
+          a = fma(v.x, xx.x, a);
+          a = fma(v.y, xx.y, a);
         }
-        if (ok) {
-          const double v = rv[j] * x[static_cast<int64_t>(nb) * F + d];
-#pragma unroll
-          for (int cc = 0; cc < F; ++cc)
-            if (cc == c) acc[cc] += v;
-        }
+        acc[c] = a;
       }
 #pragma unroll
       for (int c = 0; c < F; ++c)
         for (int o = 16; o > 0; o >>= 1) acc[c] += __shfl_down_sync(0xffffffffu, acc[c], o);
       if (lane == 0) {
+        const int64_t base = static_cast<int64_t>(k) * F;
+        if constexpr (MODE == kSpmvY) {
 #pragma unroll
-        for (int c = 0; c < F; ++c) {
-          const double v = freem[k * F + c] ? acc[c] : 0.0;
-          y[static_cast<int64_t>(k) * F + c] = v;
-          if (dotv) part[0] += v * dotv[static_cast<int64_t>(k) * F + c];
+          for (int c = 0; c < F; ++c) {
+            const double v = freem[base + c] ? acc[c] : 0.0;
+            y[base + c] = v;
+            if (dotv) part[0] += v * dotv[base + c];
+          }
+        } else {
+          double rr[F];
+#pragma unroll
+          for (int c = 0; c < F; ++c) rr[c] = freem[base + c] ? b[base + c] - acc[c] : 0.0;
+          if constexpr (MODE == kSpmvResid) {
+#pragma unroll
+            for (int c = 0; c < F; ++c) y[base + c] = rr[c];
+          } else {
+            const double* Di = dinv + static_cast<int64_t>(row) * FF;
+#pragma unroll
+            for (int c = 0; c < F; ++c) {
+              double sacc = 0.0;
+#pragma unroll
+              for (int d = 0; d < F; ++d) sacc += Di[c * F + d] * rr[d];
+              y[base + c] = freem[base + c] ? x[base + c] + omega * sacc : 0.0;
+            }
+          }
         }
       }
+      __syncwarp();
     }
   }
   if (partials) block_sum_store<1>(part, partials);
@@ -947,6 +1034,117 @@ __global__ void k_cg_p(int N, const int* __restrict__ act_idx, const double* __r
   for (int c = 0; c < F; ++c) p[n * F + c] = z[n * F + c] + beta * p[n * F + c];
 }
 
+// Sum of `nb` partials (row k of NV rows) by one block, fixed order: every
+// block of the consumer kernel computes the same value (deterministic, no
+// separate finalize launch).
+template <int NV>
+__device__ __forceinline__ void block_reduce_partials(const double* __restrict__ partials, int nb, double (&out)[NV]) {
+  __shared__ double red[NV][32];
+  __shared__ double res[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    double s = 0.0;
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) s += partials[k * nb + i];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[k][threadIdx.x >> 5] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int nw = blockDim.x >> 5;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      double s = threadIdx.x < nw ? red[k][threadIdx.x] : 0.0;
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+      if (threadIdx.x == 0) res[k] = s;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < NV; ++k) out[k] = res[k];
+}
+
+// CG step part 1: alpha = rz / p.q (from the SpMV partials); x += a p;
+// r -= a q; z = Minv r; partials of r.z and r.r.  rz lives in sc[kRz + par].
+template <int F>
+__global__ void k_cg_update2(int N, const int* __restrict__ act_idx, const double* __restrict__ dinv,
+                             double* __restrict__ sc, int* __restrict__ done, int par, const double* __restrict__ pq_part,
+                             int nb, double* __restrict__ x, double* __restrict__ r, double* __restrict__ z,
+                             const double* __restrict__ p, const double* __restrict__ q,
+                             double* __restrict__ partials) {
+  double v[2] = {0.0, 0.0};
+  const int was_done = *done;
+  double pq[1];
+  block_reduce_partials<1>(pq_part, nb, pq);
+  if (!was_done) {
+    const double rz = sc[par ? kBeta : kRz];  // ping-pong slot holding the current r.z
+    if (!(pq[0] > 0.0)) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        sc[kDone] = 2.0;
+        *done = 2;
+      }
+    } else {
+      const double alpha = rz / pq[0];
+      for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
+        const int row = act_idx[n];
+        if (row < 0) continue;
+        double rl[F];
+#pragma unroll
+        for (int c = 0; c < F; ++c) {
+          x[n * F + c] += alpha * p[n * F + c];
+          rl[c] = r[n * F + c] - alpha * q[n * F + c];
+          r[n * F + c] = rl[c];
+        }
+#pragma unroll
+        for (int c = 0; c < F; ++c) {
+          double s = 0.0;
+#pragma unroll
+          for (int d = 0; d < F; ++d) s += dinv[static_cast<int64_t>(row) * F * F + c * F + d] * rl[d];
+          z[n * F + c] = s;
+          v[0] += rl[c] * s;
+          v[1] += rl[c] * rl[c];
+        }
+      }
+    }
+  }
+  block_sum_store<2>(v, partials);
+}
+
+// CG step part 2: convergence test on r.r, beta = rz_new / rz, p = z + beta p.
+// Block 0 records rz_new in the other ping-pong slot and the iteration count.
+template <int F>
+__global__ void k_cg_p2(int N, const int* __restrict__ act_idx, double* __restrict__ sc, int* __restrict__ done,
+                        int par, int it, const double* __restrict__ part, int nb, double rtol2, int max_iter,
+                        const double* __restrict__ z, double* __restrict__ p) {
+  if (*done) return;
+  double v[2];
+  block_reduce_partials<2>(part, nb, v);
+  const double rz_new = v[0], rr = v[1];
+  const double rz = sc[par ? kBeta : kRz];
+  const double iters = it + 1.0;
+  int stop = 0;
+  if (!(rr == rr)) stop = 3;
+  else if (rr <= rtol2 * sc[kBb]) stop = 1;
+  else if (iters >= max_iter) stop = 4;
+  // every block takes the same decision from the same sums
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    sc[kIters] = iters;
+    sc[kRr] = rr;
+    sc[par ? kRz : kBeta] = rz_new;
+    if (stop) {
+      sc[kDone] = stop;
+      *done = stop;
+    }
+  }
+  if (stop) return;
+  const double beta = rz_new / rz;
+  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
+    if (act_idx[n] < 0) continue;
+#pragma unroll
+    for (int c = 0; c < F; ++c) p[n * F + c] = z[n * F + c] + beta * p[n * F + c];
+  }
+}
+
 // generic BLAS-1 on grid vectors (nonsymmetric Krylov path)
 __global__ void k_dot2(int64_t n, const double* __restrict__ a, const double* __restrict__ b,
                        const double* __restrict__ c, const double* __restrict__ d, double* __restrict__ partials) {
@@ -982,6 +1180,417 @@ __global__ void k_precond(int N, const int* __restrict__ act_idx, const double* 
       for (int d = 0; d < F; ++d) s += dinv[static_cast<int64_t>(row) * F * F + c * F + d] * r[n * F + d];
     z[n * F + c] = s;
   }
+}
+
+// ------------------------------------------------- K7 multigrid (Galerkin) --
+// Vertex-centred factor-2 coarsening of the structured grid: coarse node I
+// sits on fine node 2I; trilinear prolongation P (weights 1 / 0.5 per axis).
+// The coarse operator A_c = P^T M A M P (M = free-DOF mask) is again a 5^D
+// box-BSR (|2I-2J| <= 1+2+1), stored compacted like the fine Jacobian, so the
+// same SpMV / smoother kernel serves every level.
+__device__ __forceinline__ double p1w(int e) { return e == 0 ? 1.0 : 0.5; }
+
+// coarse node active iff an active fine row lies in supp(P_I)
+template <int D>
+__global__ void k_coarse_active(GridC gf, GridC gc, const int* __restrict__ fine_act_idx, int* __restrict__ cflag) {
+  const int I = blockIdx.x * blockDim.x + threadIdx.x;
+  if (I >= gc.N) return;
+  int ci[3];
+  unflat<D>(gc, I, ci);
+  int act = 0;
+  constexpr int NE = ipow_c(3, D);
+  for (int e = 0; e < NE && !act; ++e) {
+    int r = e, fi = 0;
+    bool ok = true;
+#pragma unroll
+    for (int a = D - 1; a >= 0; --a) {
+      const int ia = 2 * ci[a] + (r % 3) - 1;
+      r /= 3;
+      ok = ok && ia >= 0 && ia < gf.nodes[a];
+      fi += ia * gf.stride[a];
+    }
+    if (ok && fine_act_idx[fi] >= 0) act = 1;
+  }
+  cflag[I] = act;
+}
+
+// Galerkin step 1 (one warp per fine row i): T[i][J] = sum_j A_ij M_j P_jJ
+// for the <= 4^D coarse nodes J whose support meets the +-2 box of i
+// (J_a in [(i_a-2)>>1, +4)); lanes own the coarse slots (deterministic).
+template <int D, int F, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_galerkin_ap(GridC gf, GridC gc, int f_n_act,
+                                                            const int* __restrict__ f_act_list,
+                                                            const double* __restrict__ fvals, int64_t f_row_len,
+                                                            const uint8_t* __restrict__ f_slots,
+                                                            const int* __restrict__ f_nzb,
+                                                            const uint8_t* __restrict__ f_freem,
+                                                            double* __restrict__ T) {
+  constexpr int S = ipow_c(5, D);
+  constexpr int FF = F * F;
+  constexpr int NT = ipow_c(4, D);
+  constexpr int NTL = (NT + 31) / 32;
+  __shared__ short inv_all[WARPS][S];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  short* inv = inv_all[warp];
+  for (int row = blockIdx.x * WARPS + warp; row < f_n_act; row += gridDim.x * WARPS) {
+    const int i = f_act_list[row];
+    int fi[3];
+    unflat<D>(gf, i, fi);
+    const int nzb = f_nzb[row];
+    const uint8_t* fs = f_slots + static_cast<int64_t>(row) * S;
+    for (int sl = lane; sl < S; sl += 32) inv[sl] = -1;
+    __syncwarp();
+    for (int pos = lane; pos < nzb; pos += 32) inv[fs[pos]] = static_cast<short>(pos);
+    __syncwarp();
+    const double* fv = fvals + static_cast<int64_t>(row) * f_row_len;
+    const int cpf = cpad(nzb, F);
+    double* Ti = T + static_cast<int64_t>(row) * NT * FF;
+#pragma unroll
+    for (int u = 0; u < NTL; ++u) {
+      const int tl = lane + 32 * u;
+      if (tl >= NT) continue;
+      double acc[FF];
+#pragma unroll
+      for (int e = 0; e < FF; ++e) acc[e] = 0.0;
+      // per axis: coarse J_a = ((fi_a - 2) >> 1) + t_a; fine j_a = 2 J_a + f, |j_a - fi_a| <= 2
+      int Ja[3], lo[3], hi[3];
+      bool ok = true;
+      int r = tl;
+#pragma unroll
+      for (int a = D - 1; a >= 0; --a) {
+        const int t = r % 4;
+        r /= 4;
+        Ja[a] = ((fi[a] - 2) >> 1) + t;
+        ok = ok && Ja[a] >= 0 && Ja[a] < gc.nodes[a];
+        lo[a] = max(-1, fi[a] - 2 - 2 * Ja[a]);
+        hi[a] = min(1, fi[a] + 2 - 2 * Ja[a]);
+        ok = ok && lo[a] <= hi[a];
+      }
+      if (ok) {
+        const int f1lo = D > 1 ? lo[1] : 0, f1hi = D > 1 ? hi[1] : 0;
+        const int f2lo = D > 2 ? lo[2] : 0, f2hi = D > 2 ? hi[2] : 0;
+        for (int f0 = lo[0]; f0 <= hi[0]; ++f0)
+          for (int f1 = f1lo; f1 <= f1hi; ++f1)
+            for (int f2 = f2lo; f2 <= f2hi; ++f2) {
+              const int fo[3] = {f0, f1, f2};
+              int sl = 0, j = 0;
+              double w = 1.0;
+              bool in = true;
+#pragma unroll
+              for (int a = 0; a < D; ++a) {
+                const int ja = 2 * Ja[a] + fo[a];
+                in = in && ja >= 0 && ja < gf.nodes[a];
+                sl = sl * 5 + (ja - fi[a] + 2);
+                j += ja * gf.stride[a];
+                w *= p1w(fo[a]);
+              }
+              if (!in) continue;
+              const int pos = inv[sl];
+              if (pos < 0) continue;
+              const double* blk = fv + pos * F;
+#pragma unroll
+              for (int d = 0; d < F; ++d) {
+                if (!f_freem[static_cast<int64_t>(j) * F + d]) continue;
+#pragma unroll
+                for (int c = 0; c < F; ++c) acc[c * F + d] += w * blk[c * cpf + d];
+              }
+            }
+      }
+#pragma unroll
+      for (int e = 0; e < FF; ++e) Ti[tl * FF + e] = acc[e];
+    }
+    __syncwarp();
+  }
+}
+
+// Galerkin step 2 (one warp per coarse row I): A_c[I][J] = sum_i w_i M_i T[i][J]
+// over the 3^D fine rows i in supp(P_I); lanes own coarse box slots J.
+// Compacts nonzero blocks, sets the coarse free mask from the diagonal and
+// the masked block inverse.
+template <int D, int F, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_galerkin_ptap(GridC gf, GridC gc, const int* __restrict__ f_act_idx,
+                                                              const uint8_t* __restrict__ f_freem,
+                                                              const double* __restrict__ T,
+                                                              const int* __restrict__ c_act_list, int c_n_act,
+                                                              double* __restrict__ cvals, int64_t c_row_len,
+                                                              uint8_t* __restrict__ c_slots, int* __restrict__ c_nzb,
+                                                              uint8_t* __restrict__ c_freem, double* __restrict__ c_dinv,
+                                                              unsigned long long* __restrict__ nzb_total) {
+  constexpr int S = ipow_c(5, D);
+  constexpr int FF = F * F;
+  constexpr int NE = ipow_c(3, D);
+  constexpr int NT = ipow_c(4, D);
+  constexpr int NJ = (S + 31) / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int row = blockIdx.x * WARPS + warp; row < c_n_act; row += gridDim.x * WARPS) {
+    const int I = c_act_list[row];
+    int ci[3];
+    unflat<D>(gc, I, ci);
+    double acc[NJ][FF];
+#pragma unroll
+    for (int t = 0; t < NJ; ++t)
+#pragma unroll
+      for (int e = 0; e < FF; ++e) acc[t][e] = 0.0;
+    for (int e = 0; e < NE; ++e) {
+      int r = e, fi[3], eo[3], i = 0;
+      bool ok = true;
+      double wi = 1.0;
+#pragma unroll
+      for (int a = D - 1; a >= 0; --a) {
+        eo[a] = (r % 3) - 1;
+        r /= 3;
+        fi[a] = 2 * ci[a] + eo[a];
+        ok = ok && fi[a] >= 0 && fi[a] < gf.nodes[a];
+        i += fi[a] * gf.stride[a];
+      }
+      if (!ok) continue;
+      const int frow = f_act_idx[i];
+      if (frow < 0) continue;
+#pragma unroll
+      for (int a = 0; a < D; ++a) wi *= p1w(eo[a]);
+      bool mi[3];
+#pragma unroll
+      for (int c = 0; c < F; ++c) mi[c] = f_freem[static_cast<int64_t>(i) * F + c] != 0;
+      const double* Ti = T + static_cast<int64_t>(frow) * NT * FF;
+#pragma unroll
+      for (int t = 0; t < NJ; ++t) {
+        const int js = lane + 32 * t;
+        if (js >= S) continue;
+        int rs = js, tl = 0;
+        bool in = true;
+#pragma unroll
+        for (int a = D - 1; a >= 0; --a) {
+          const int Ja = ci[a] + rs % 5 - 2;
+          rs /= 5;
+          const int ta = Ja - ((fi[a] - 2) >> 1);
+          in = in && ta >= 0 && ta < 4;
+          tl += ta * (a == D - 1 ? 1 : (a == D - 2 ? 4 : 16));
+        }
+        if (!in) continue;
+        const double* tb = Ti + tl * FF;
+#pragma unroll
+        for (int c = 0; c < F; ++c) {
+          if (!mi[c]) continue;
+#pragma unroll
+          for (int d = 0; d < F; ++d) acc[t][c * F + d] += wi * tb[c * F + d];
+        }
+      }
+    }
+    int base = 0;
+    int posv[NJ];
+    bool flag[NJ];
+#pragma unroll
+    for (int t = 0; t < NJ; ++t) {
+      const int js = lane + 32 * t;
+      bool f = false;
+      if (js < S)
+#pragma unroll
+        for (int e = 0; e < FF; ++e) f = f || acc[t][e] != 0.0;
+      const unsigned m = __ballot_sync(0xffffffffu, f);
+      posv[t] = base + __popc(m & ((1u << lane) - 1u));
+      flag[t] = f;
+      base += __popc(m);
+    }
+    const int cpc = cpad(base, F);
+    double* rowv = cvals + static_cast<int64_t>(row) * c_row_len;
+    if (lane < F && (base * F) % 2) rowv[lane * cpc + base * F] = 0.0;  // chunk pad
+#pragma unroll
+    for (int t = 0; t < NJ; ++t) {
+      const int js = lane + 32 * t;
+      if (flag[t]) {
+        const int pos = posv[t];
+        c_slots[static_cast<int64_t>(row) * S + pos] = static_cast<uint8_t>(js);
+#pragma unroll
+        for (int c = 0; c < F; ++c)
+#pragma unroll
+          for (int d = 0; d < F; ++d) rowv[c * cpc + pos * F + d] = acc[t][c * F + d];
+      }
+      if (js == (S - 1) / 2) {
+        bool fr[3];
+#pragma unroll
+        for (int c = 0; c < F; ++c) {
+          fr[c] = acc[t][c * F + c] > 0.0;
+          c_freem[static_cast<int64_t>(I) * F + c] = fr[c] ? 1 : 0;
+        }
+        Mat<double, F> Mb;
+#pragma unroll
+        for (int c = 0; c < F; ++c)
+#pragma unroll
+          for (int d = 0; d < F; ++d) Mb(c, d) = (fr[c] && fr[d]) ? acc[t][c * F + d] : (c == d ? 1.0 : 0.0);
+        const Mat<double, F> Mi = inverse(Mb);
+#pragma unroll
+        for (int e2 = 0; e2 < FF; ++e2) c_dinv[static_cast<int64_t>(row) * FF + e2] = Mi.e[e2];
+      }
+    }
+    if (lane == 0) {
+      c_nzb[row] = base;
+      atomicAdd(nzb_total, static_cast<unsigned long long>(base));
+    }
+  }
+}
+
+// b_c = P^T r (masked to coarse free components)
+template <int D, int F>
+__global__ void k_restrict(GridC gf, GridC gc, const int* __restrict__ done, const double* __restrict__ rf,
+                           const uint8_t* __restrict__ c_freem, double* __restrict__ bc) {
+  if (done && *done) return;
+  const int I = blockIdx.x * blockDim.x + threadIdx.x;
+  if (I >= gc.N) return;
+  int ci[3];
+  unflat<D>(gc, I, ci);
+  double acc[F];
+#pragma unroll
+  for (int c = 0; c < F; ++c) acc[c] = 0.0;
+  constexpr int NE = ipow_c(3, D);
+  for (int e = 0; e < NE; ++e) {
+    int r = e, fi = 0;
+    bool ok = true;
+    double w = 1.0;
+#pragma unroll
+    for (int a = D - 1; a >= 0; --a) {
+      const int eo = (r % 3) - 1;
+      r /= 3;
+      const int ia = 2 * ci[a] + eo;
+      ok = ok && ia >= 0 && ia < gf.nodes[a];
+      fi += ia * gf.stride[a];
+      w *= p1w(eo);
+    }
+    if (!ok) continue;
+#pragma unroll
+    for (int c = 0; c < F; ++c) acc[c] += w * rf[static_cast<int64_t>(fi) * F + c];
+  }
+#pragma unroll
+  for (int c = 0; c < F; ++c) bc[static_cast<int64_t>(I) * F + c] = c_freem[static_cast<int64_t>(I) * F + c] ? acc[c] : 0.0;
+}
+
+// x_f += P x_c (masked to fine free components)
+template <int D, int F>
+__global__ void k_prolong_add(GridC gf, GridC gc, const int* __restrict__ done, const double* __restrict__ xc,
+                              const uint8_t* __restrict__ f_freem, double* __restrict__ xf) {
+  if (done && *done) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= gf.N) return;
+  int fi[3];
+  unflat<D>(gf, i, fi);
+  double acc[F];
+#pragma unroll
+  for (int c = 0; c < F; ++c) acc[c] = 0.0;
+  constexpr int NC = ipow_c(2, D);
+  for (int e = 0; e < NC; ++e) {
+    int I = 0;
+    double w = 1.0;
+    bool ok = true;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      const int bit = (e >> a) & 1;
+      int Ia;
+      if (fi[a] % 2 == 0) {
+        if (bit) { ok = false; Ia = 0; } else { Ia = fi[a] / 2; }
+      } else {
+        Ia = (fi[a] - 1) / 2 + bit;
+        w *= 0.5;
+      }
+      ok = ok && Ia >= 0 && Ia < gc.nodes[a];
+      I += Ia * gc.stride[a];
+    }
+    if (!ok) continue;
+#pragma unroll
+    for (int c = 0; c < F; ++c) acc[c] += w * xc[static_cast<int64_t>(I) * F + c];
+  }
+#pragma unroll
+  for (int c = 0; c < F; ++c)
+    if (f_freem[static_cast<int64_t>(i) * F + c]) xf[static_cast<int64_t>(i) * F + c] += acc[c];
+}
+
+__global__ void k_fill_free(int64_t n, const uint8_t* __restrict__ freem, double* __restrict__ v) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) v[i] = freem[i] ? 1.0 : 0.0;
+}
+
+// power-iteration step: lam = |t| / |v|, v = t / |t|  (sums = {t.t, v.v})
+__global__ void k_power_step(int64_t n, const double* __restrict__ sums, const double* __restrict__ t,
+                             double* __restrict__ v, double* __restrict__ lam) {
+  const double tt = sums[0], vv = sums[1];
+  const double inv = tt > 0.0 ? rsqrt(tt) : 0.0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    v[i] = t[i] * inv;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *lam = vv > 0.0 ? sqrt(tt / vv) : 1.0;
+}
+
+// first smoothing sweep from x = 0: x = omega Dinv b (masked)
+template <int F>
+__global__ void k_jacobi0(int n_act, const int* __restrict__ done, const int* __restrict__ act_list,
+                          const double* __restrict__ dinv, const uint8_t* __restrict__ freem, double omega,
+                          const double* __restrict__ b, double* __restrict__ x) {
+  if (done && *done) return;
+  for (int row = blockIdx.x * blockDim.x + threadIdx.x; row < n_act; row += gridDim.x * blockDim.x) {
+    const int64_t base = static_cast<int64_t>(act_list[row]) * F;
+#pragma unroll
+    for (int c = 0; c < F; ++c) {
+      double s = 0.0;
+#pragma unroll
+      for (int d = 0; d < F; ++d) s += dinv[static_cast<int64_t>(row) * F * F + c * F + d] * b[base + d];
+      x[base + c] = freem[base + c] ? omega * s : 0.0;
+    }
+  }
+}
+
+// coarsest level: x = Ainv b with a dense inverse over (active row, component)
+__global__ void k_dense_apply(int n, int F, const int* __restrict__ done, const int* __restrict__ act_list,
+                              const double* __restrict__ Ainv, const double* __restrict__ b, double* __restrict__ x) {
+  if (done && *done) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j < n; ++j) s += Ainv[static_cast<int64_t>(i) * n + j] * b[static_cast<int64_t>(act_list[j / F]) * F + j % F];
+    x[static_cast<int64_t>(act_list[i / F]) * F + i % F] = s;
+  }
+}
+
+// CG (MG-preconditioned) step part 1: alpha from p.q; x += a p; r -= a q;
+// partial r.r into row 1 of `partials`.
+template <int F>
+__global__ void k_cg_update_mg(int N, const int* __restrict__ act_idx, double* __restrict__ sc, int* __restrict__ done,
+                               int par, const double* __restrict__ pq_part, int nb, double* __restrict__ x,
+                               double* __restrict__ r, const double* __restrict__ p, const double* __restrict__ q,
+                               double* __restrict__ partials_rr) {
+  double v[1] = {0.0};
+  const int was_done = *done;
+  double pq[1];
+  block_reduce_partials<1>(pq_part, nb, pq);
+  if (!was_done) {
+    const double rz = sc[par ? kBeta : kRz];
+    if (!(pq[0] > 0.0)) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        sc[kDone] = 2.0;
+        *done = 2;
+      }
+    } else {
+      const double alpha = rz / pq[0];
+      for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
+        if (act_idx[n] < 0) continue;
+#pragma unroll
+        for (int c = 0; c < F; ++c) {
+          x[n * F + c] += alpha * p[n * F + c];
+          const double rl = r[n * F + c] - alpha * q[n * F + c];
+          r[n * F + c] = rl;
+          v[0] += rl * rl;
+        }
+      }
+    }
+  }
+  block_sum_store<1>(v, partials_rr);
+}
+
+// partial a.b over grid vectors (row 0 of `partials`)
+__global__ void k_dot1(int64_t n, const int* __restrict__ done, const double* __restrict__ a,
+                       const double* __restrict__ b, double* __restrict__ partials) {
+  double v[1] = {0.0};
+  if (!(done && *done))
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+      v[0] += a[i] * b[i];
+  block_sum_store<1>(v, partials);
 }
 
 // --------------------------------------------------------------- K9 G2P --
@@ -1107,7 +1716,8 @@ __global__ void k_csr_count(GridC g, int n, const int* __restrict__ node_of, con
 template <int D, int F>
 __global__ void k_csr_fill(GridC g, int n, const int* __restrict__ node_of, const int* __restrict__ field_of,
                            const int* __restrict__ dof_of, const int* __restrict__ act_idx,
-                           const double* __restrict__ vals, int64_t row_len, const int64_t* __restrict__ row_ptr,
+                           const double* __restrict__ vals, int64_t row_len, const uint8_t* __restrict__ row_slots,
+                           const int* __restrict__ row_nzb, const int64_t* __restrict__ row_ptr,
                            int* __restrict__ cols, double* __restrict__ out) {
   const int d = blockIdx.x * blockDim.x + threadIdx.x;
   if (d >= n) return;
@@ -1117,14 +1727,18 @@ __global__ void k_csr_fill(GridC g, int n, const int* __restrict__ node_of, cons
   unflat<D>(g, k, kidx);
   const int64_t row = act_idx[k];
   int64_t o = row_ptr[d];
+  const int nzb = row_nzb[row];
+  int pos = 0;
   for (int s = 0; s < S; ++s) {
     int nb;
+    while (pos < nzb && row_slots[row * S + pos] < s) ++pos;
+    const bool stored = pos < nzb && row_slots[row * S + pos] == s;
     if (!box_slot_node<D>(g, kidx, s, nb)) continue;
     for (int f = 0; f < F; ++f) {
       const int col = dof_of[nb * F + f];
       if (col < 0) continue;
       cols[o] = col;
-      if (out) out[o] = vals[row * row_len + s * F * F + c * F + f];
+      if (out) out[o] = stored ? vals[row * row_len + c * cpad(nzb, F) + pos * F + f] : 0.0;
       ++o;
     }
   }

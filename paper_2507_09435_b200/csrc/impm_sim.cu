@@ -75,9 +75,13 @@ template <int V>
 using IC = std::integral_constant<int, V>;
 
 // ---------------------------------------------------------- profiling ---
-enum KClass { kcSort = 0, kcMass, kcDof, kcResP, kcResN, kcTangent, kcAssemble, kcSpmv, kcKrylov, kcCommit, kcCount };
-const char* kClassNames[kcCount] = {"support_sort", "node_mass", "dof_map",  "residual_particles", "residual_nodes",
-                                    "tangent",      "assemble",  "spmv",     "krylov_vector",      "commit"};
+enum KClass {
+  kcSort = 0, kcMass, kcDof, kcResP, kcResN, kcTangent, kcAssemble, kcSpmv, kcKrylov, kcCommit, kcMgSetup, kcVcycle,
+  kcGalerkin, kcMgPower, kcMgCoarsest, kcCount
+};
+const char* kClassNames[kcCount] = {"support_sort", "node_mass", "dof_map", "residual_particles", "residual_nodes",
+                                    "tangent",      "assemble",  "spmv",    "krylov_vector",      "commit",
+                                    "mg_setup",     "vcycle",    "galerkin", "mg_power",           "mg_coarsest"};
 
 struct Prof {
   bool on = false;
@@ -129,6 +133,29 @@ struct Prof {
   }
 };
 
+// ---------------------------------------------------------- multigrid ---
+struct MgLevel {
+  GridC g{};
+  int n_act = 0;
+  int64_t row_len = 0;
+  // owned storage (coarse levels; level 0 views the fine Jacobian)
+  DBuf<int> act_flag_b, act_scan_b, act_idx_b, act_list_b, row_nzb_b;
+  DBuf<uint8_t> freem_b, row_slots_b;
+  DBuf<double> vals_b, dinv_b;
+  DBuf<double> xa, xb, r, bvec;  // level vectors (grid layout)
+  // views
+  const int* act_idx = nullptr;
+  const int* act_list = nullptr;
+  const int* row_nzb = nullptr;
+  const uint8_t* freem = nullptr;
+  const uint8_t* row_slots = nullptr;
+  const double* vals = nullptr;
+  const double* dinv = nullptr;
+  double* x = nullptr;  // current iterate (ping-pong between xa / xb)
+  double* t = nullptr;
+  double omega = 0.5;
+};
+
 // ------------------------------------------------------------ the sim ---
 struct Sim {
   // configuration
@@ -158,8 +185,18 @@ struct Sim {
   DBuf<double> kx, kr, kz, kp, kq, kv, ks, kt, khat;
   // matrix
   DBuf<double> vals, dinv;
+  DBuf<uint8_t> row_slots;
+  DBuf<int> row_nzb;
+  DBuf<unsigned long long> nzb_total;
+  unsigned long long h_nzb_total = 0;
   int64_t row_len = 0;
   bool matrix_valid = false;
+  // multigrid hierarchy (rebuilt with every Jacobian)
+  std::vector<std::unique_ptr<MgLevel>> mg;
+  DBuf<double> mg_dense, mg_lam, mg_T;
+  DBuf<unsigned long long> mg_nzb;
+  int mg_dense_n = 0;
+  unsigned long long mg_stored_blocks = 0;
   // reductions / status
   DBuf<double> partials, sums, sc;
   DBuf<DevStatus> st;
@@ -462,9 +499,12 @@ struct Sim {
     n_dofs = counts[0];
     n_act = counts[1];
     const int S = ipow_c(5, D);
-    row_len = pad4(S * F * F);
+    row_len = row_len_for(S, F);
     vals.ensure(std::max<int64_t>(1, static_cast<int64_t>(n_act) * row_len));
     dinv.ensure(std::max<int64_t>(1, static_cast<int64_t>(n_act) * F * F));
+    row_slots.ensure(std::max<int64_t>(1, static_cast<int64_t>(n_act) * S));
+    row_nzb.ensure(std::max(1, n_act));
+    nzb_total.ensure(1);
     CK(cudaMemsetAsync(u.p, 0, sizeof(double) * NF(), s));
     matrix_valid = false;
     step_built = true;
@@ -517,11 +557,14 @@ struct Sim {
         Prof::Scope ps(&prof, kcAssemble);
         constexpr int W = DD == 3 ? 4 : 8;
         constexpr int S = ipow_c(5, DD);
-        const size_t smem = sizeof(double) * W * (S * DD * DD + DD * DD * DD);
+        const size_t smem = sizeof(double) * W * (S * DD * DD + DD * DD * DD + (2 * S + 7) / 8);
         auto kern = k_assemble<DD, SH, W>;
         if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaMemsetAsync(nzb_total.p, 0, sizeof(unsigned long long), s));
         kern<<<blocks_for(n_act, W), W * 32, smem, s>>>(g, pd.p, cap, xs.p, bin_start.p, sup.p, Atan.p, act_list.p,
-                                                        n_act, freem.p, vals.p, row_len, dinv.p); ++g_launches;
+                                                        n_act, freem.p, vals.p, row_len, dinv.p, row_slots.p,
+                                                        row_nzb.p, nzb_total.p);
+        CK(cudaMemcpyAsync(&h_nzb_total, nzb_total.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s)); ++g_launches;
         CKL();
       }
     });
@@ -534,8 +577,8 @@ struct Sim {
     auto launch = [&](auto Dc) {
       constexpr int DD = decltype(Dc)::value;
       constexpr int W = 8;
-      k_spmv<DD, DD, W><<<kRedBlocks, W * 32, 0, s>>>(g, act_list.p, n_act, vals.p, row_len, x, freem.p, y, dotv,
-                                                      parts, dflag.p); ++g_launches;
+      k_spmv<DD, DD, W><<<kRedBlocks, W * 32, 0, s>>>(g, act_list.p, n_act, vals.p, row_len, row_slots.p,
+                                                      row_nzb.p, x, freem.p, y, dotv, parts, dflag.p); ++g_launches;
       CKL();
     };
     if (D == 1) launch(IC<1>{});
@@ -564,24 +607,23 @@ struct Sim {
     if (h_sc[kDone] != 0.0) return 0;
     const int batch = n_dofs < 20000 ? 16 : 4;
     int done = 0;
-    while (true) {
-      for (int i = 0; i < batch; ++i) {
-        spmv(kp.p, kq.p, kp.p, partials.p);
+    double* partA = partials.p;
+    double* partB = partials.p + 2 * kRedBlocks;
+    for (int it = 0; !done;) {
+      for (int i = 0; i < batch; ++i, ++it) {
+        const int par = it & 1;
+        spmv(kp.p, kq.p, kp.p, partA);
         Prof::Scope ps(&prof, kcKrylov);
-        k_finalize_sum<1><<<1, 1024, 0, s>>>(partials.p, kRedBlocks, sums.p); ++g_launches;
-        k_cg_alpha<<<1, 1, 0, s>>>(sums.p, sc.p, dflag.p); ++g_launches;
-        k_cg_update<FF><<<kRedBlocks, kThreads, 0, s>>>(N, act_idx.p, dinv.p, sc.p, dflag.p, x, kr.p, kz.p, kp.p,
-                                                        kq.p, partials.p); ++g_launches;
-        k_finalize_sum<2><<<1, 1024, 0, s>>>(partials.p, kRedBlocks, sums.p); ++g_launches;
-        k_cg_beta<<<1, 1, 0, s>>>(sums.p, sc.p, dflag.p, rtol2, max_it); ++g_launches;
-        k_cg_p<FF><<<blocks_for(N), kThreads, 0, s>>>(N, act_idx.p, sc.p, dflag.p, kz.p, kp.p); ++g_launches;
+        k_cg_update2<FF><<<kRedBlocks, kThreads, 0, s>>>(N, act_idx.p, dinv.p, sc.p, dflag.p, par, partA, kRedBlocks,
+                                                         x, kr.p, kz.p, kp.p, kq.p, partB); ++g_launches;
+        k_cg_p2<FF><<<kRedBlocks, kThreads, 0, s>>>(N, act_idx.p, sc.p, dflag.p, par, it, partB, kRedBlocks, rtol2,
+                                                    max_it, kz.p, kp.p); ++g_launches;
         CKL();
       }
       CK(cudaMemcpyAsync(&done, dflag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
       CK(cudaMemcpyAsync(h_sc, sc.p, sizeof(double) * kNSlots, cudaMemcpyDeviceToHost, s));
       sync();
       prof.flush();
-      if (done) break;
     }
     const int iters = static_cast<int>(h_sc[kIters]);
     if (done == 2) return -iters - 1;  // not SPD: caller falls back to BiCGStab
@@ -658,12 +700,357 @@ struct Sim {
     throw SimError(IMPM_ERR_LINEAR_SOLVER, "BiCGStab did not converge");
   }
 
+
+  // ------------------------------------------------ multigrid (K7 precond)
+  template <int DD, int MODE>
+  void level_spmv(MgLevel& L, const double* x, double* y, const double* b, double omega, const double* dotv,
+                  double* parts) {
+    constexpr int W = 8;
+    k_spmv<DD, DD, W, MODE><<<kRedBlocks, W * 32, 0, s>>>(L.g, L.act_list, L.n_act, L.vals, L.row_len, L.row_slots,
+                                                          L.row_nzb, x, L.freem, y, dotv, parts, dflag.p, b, L.dinv,
+                                                          omega); ++g_launches;
+    CKL();
+  }
+
+  template <int DD>
+  void mg_setup() {
+    constexpr int S = ipow_c(5, DD);
+    constexpr int FF = DD * DD;
+    // level objects (and their device buffers) persist across setups; only
+    // growth reallocates
+    std::vector<std::unique_ptr<MgLevel>> pool;
+    pool.swap(mg);
+    auto take = [&pool]() {
+      if (pool.empty()) return std::make_unique<MgLevel>();
+      auto p = std::move(pool.front());
+      pool.erase(pool.begin());
+      return p;
+    };
+    auto L0 = take();
+    L0->g = g;
+    L0->n_act = n_act;
+    L0->row_len = row_len;
+    L0->act_idx = act_idx.p;
+    L0->act_list = act_list.p;
+    L0->row_nzb = row_nzb.p;
+    L0->freem = freem.p;
+    L0->row_slots = row_slots.p;
+    L0->vals = vals.p;
+    L0->dinv = dinv.p;
+    mg.push_back(std::move(L0));
+    mg_stored_blocks = 0;
+    const int coarsest_max = 200;  // unknowns solved densely at the bottom
+    mg_nzb.ensure(1);
+    while (static_cast<int64_t>(mg.back()->n_act) * DD > coarsest_max && mg.size() < 16) {
+      MgLevel& F0 = *mg.back();
+      auto C = take();
+      GridC gc{};
+      int N = 1;
+      for (int a = 0; a < 3; ++a) {
+        gc.nodes[a] = a < DD ? F0.g.nodes[a] / 2 + 1 : 1;
+        gc.origin[a] = F0.g.origin[a];
+        N *= gc.nodes[a];
+      }
+      gc.stride[DD - 1] = 1;
+      for (int a = DD - 2; a >= 0; --a) gc.stride[a] = gc.stride[a + 1] * gc.nodes[a + 1];
+      for (int a = DD; a < 3; ++a) gc.stride[a] = 0;
+      gc.h = F0.g.h * 2.0;
+      gc.N = N;
+      if (N >= F0.g.N) break;  // no further coarsening possible
+      C->g = gc;
+      C->act_flag_b.ensure(N);
+      C->act_scan_b.ensure(N + 1);
+      C->act_idx_b.ensure(N);
+      C->act_list_b.ensure(N);
+      k_coarse_active<DD><<<blocks_for(N), kThreads, 0, s>>>(F0.g, gc, F0.act_idx, C->act_flag_b.p); ++g_launches;
+      CKL();
+      scan<int>(C->act_flag_b.p, N, C->act_scan_b.p, scan_sums_i, C->act_scan_b.p + N);
+      k_act_finalize<<<blocks_for(N), kThreads, 0, s>>>(N, C->act_flag_b.p, C->act_scan_b.p, C->act_idx_b.p,
+                                                          C->act_list_b.p); ++g_launches;
+      CKL();
+      int na = 0;
+      CK(cudaMemcpyAsync(&na, C->act_scan_b.p + N, sizeof(int), cudaMemcpyDeviceToHost, s));
+      sync();
+      C->n_act = na;
+      C->row_len = row_len_for(S, DD);
+      C->vals_b.ensure(std::max<int64_t>(1, static_cast<int64_t>(na) * C->row_len));
+      C->row_slots_b.ensure(std::max<int64_t>(1, static_cast<int64_t>(na) * S));
+      C->row_nzb_b.ensure(std::max(1, na));
+      C->dinv_b.ensure(std::max<int64_t>(1, static_cast<int64_t>(na) * FF));
+      C->freem_b.ensure(static_cast<int64_t>(N) * DD);
+      CK(cudaMemsetAsync(C->freem_b.p, 0, static_cast<int64_t>(N) * DD, s));
+      C->act_idx = C->act_idx_b.p;
+      C->act_list = C->act_list_b.p;
+      C->row_nzb = C->row_nzb_b.p;
+      C->freem = C->freem_b.p;
+      C->row_slots = C->row_slots_b.p;
+      C->vals = C->vals_b.p;
+      C->dinv = C->dinv_b.p;
+      CK(cudaMemsetAsync(mg_nzb.p, 0, sizeof(unsigned long long), s));
+      {
+        Prof::Scope psg(&prof, kcGalerkin);
+        constexpr int NT = ipow_c(4, DD);
+        mg_T.ensure(std::max<int64_t>(1, static_cast<int64_t>(F0.n_act) * NT * FF));
+        constexpr int W = 8;
+        if (F0.n_act > 0) {
+          k_galerkin_ap<DD, DD, W><<<std::min<unsigned>(blocks_for(F0.n_act, W), 148 * 8), W * 32, 0, s>>>(
+              F0.g, gc, F0.n_act, F0.act_list, F0.vals, F0.row_len, F0.row_slots, F0.row_nzb, F0.freem, mg_T.p);
+          ++g_launches;
+          CKL();
+        }
+        if (na > 0) {
+          k_galerkin_ptap<DD, DD, W><<<std::min<unsigned>(blocks_for(na, W), 148 * 8), W * 32, 0, s>>>(
+              F0.g, gc, F0.act_idx, F0.freem, mg_T.p, C->act_list, na, C->vals_b.p, C->row_len, C->row_slots_b.p,
+              C->row_nzb_b.p, C->freem_b.p, C->dinv_b.p, mg_nzb.p);
+          ++g_launches;
+          CKL();
+        }
+      }
+      mg.push_back(std::move(C));
+    }
+    // level vectors (zero outside active rows / free components)
+    for (auto& Lp : mg) {
+      MgLevel& L = *Lp;
+      const int64_t n = static_cast<int64_t>(L.g.N) * DD;
+      L.xa.ensure(n);
+      L.xb.ensure(n);
+      L.r.ensure(n);
+      L.bvec.ensure(n);
+      for (auto* v : {&L.xa, &L.xb, &L.r, &L.bvec}) CK(cudaMemsetAsync(v->p, 0, sizeof(double) * n, s));
+      L.x = L.xa.p;
+      L.t = L.xb.p;
+    }
+    // damping of the block-Jacobi smoother from a power estimate of
+    // lambda_max(Dinv A): omega = 4 / (3 lambda) (Chebyshev-optimal
+    // smoothing); device-resident, one host read for all levels
+    CK(cudaMemsetAsync(dflag.p, 0, sizeof(int), s));
+    mg_lam.ensure(std::max<size_t>(mg.size(), 1));
+    {
+      Prof::Scope psp(&prof, kcMgPower);
+      for (size_t l = 0; l + 1 < mg.size(); ++l) {
+        MgLevel& L = *mg[l];
+        const int64_t n = static_cast<int64_t>(L.g.N) * DD;
+        k_fill_free<<<blocks_for(n), kThreads, 0, s>>>(n, L.freem, L.bvec.p); ++g_launches;
+        CKL();
+        for (int it = 0; it < 8; ++it) {
+          level_spmv<DD, kSpmvY>(L, L.bvec.p, L.r.p, nullptr, 0.0, nullptr, nullptr);
+          k_precond<DD><<<blocks_for(L.g.N), kThreads, 0, s>>>(L.g.N, L.act_idx, L.dinv, L.r.p, L.t); ++g_launches;
+          k_dot2<<<kRedBlocks, kThreads, 0, s>>>(n, L.t, L.t, L.bvec.p, L.bvec.p, partials.p); ++g_launches;
+          k_finalize_sum<2><<<1, 1024, 0, s>>>(partials.p, kRedBlocks, sums.p); ++g_launches;
+          k_power_step<<<kRedBlocks, kThreads, 0, s>>>(n, sums.p, L.t, L.bvec.p, mg_lam.p + l); ++g_launches;
+          CKL();
+        }
+      }
+    }
+    {
+      std::vector<double> lam(mg.size(), 1.0);
+      if (mg.size() > 1)
+        CK(cudaMemcpyAsync(lam.data(), mg_lam.p, sizeof(double) * (mg.size() - 1), cudaMemcpyDeviceToHost, s));
+      sync();
+      for (size_t l = 0; l + 1 < mg.size(); ++l) {
+        MgLevel& L = *mg[l];
+        const int64_t n = static_cast<int64_t>(L.g.N) * DD;
+        L.omega = 4.0 / (3.0 * 1.1 * (lam[l] > 0 ? lam[l] : 1.0));
+        CK(cudaMemsetAsync(L.t, 0, sizeof(double) * n, s));
+        CK(cudaMemsetAsync(L.bvec.p, 0, sizeof(double) * n, s));
+        CK(cudaMemsetAsync(L.r.p, 0, sizeof(double) * n, s));
+      }
+    }
+    Prof::Scope psc(&prof, kcMgCoarsest);
+    // coarsest: dense inverse over (active row, component), identity on non-free
+    MgLevel& B = *mg.back();
+    const int nb = B.n_act, n = nb * DD;
+    mg_dense_n = n;
+    if (n > 0) {
+      std::vector<int> slots_nzb(nb);
+      std::vector<uint8_t> slots(static_cast<size_t>(nb) * S), fm(static_cast<size_t>(B.g.N) * DD);
+      std::vector<int> alist(nb), aidx(B.g.N);
+      std::vector<double> vals_h(static_cast<size_t>(nb) * B.row_len), dense(static_cast<size_t>(n) * n, 0.0);
+      CK(cudaMemcpyAsync(slots_nzb.data(), B.row_nzb, sizeof(int) * nb, cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(slots.data(), B.row_slots, slots.size(), cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(fm.data(), B.freem, fm.size(), cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(alist.data(), B.act_list, sizeof(int) * nb, cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(aidx.data(), B.act_idx, sizeof(int) * B.g.N, cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(vals_h.data(), B.vals, sizeof(double) * vals_h.size(), cudaMemcpyDeviceToHost, s));
+      sync();
+      for (int rrow = 0; rrow < nb; ++rrow) {
+        const int k = alist[rrow];
+        int kidx[3] = {0, 0, 0};
+        for (int a = 0; a < DD; ++a) kidx[a] = (k / B.g.stride[a]) % B.g.nodes[a];
+        for (int pos = 0; pos < slots_nzb[rrow]; ++pos) {
+          int sl = slots[static_cast<size_t>(rrow) * S + pos], nbn = 0;
+          int rel[3];
+          for (int a = DD - 1; a >= 0; --a) {
+            rel[a] = sl % 5 - 2;
+            sl /= 5;
+          }
+          bool ok = true;
+          for (int a = 0; a < DD; ++a) {
+            const int ia = kidx[a] + rel[a];
+            ok = ok && ia >= 0 && ia < B.g.nodes[a];
+            nbn += ia * B.g.stride[a];
+          }
+          if (!ok) continue;
+          const int crow = aidx[nbn];
+          if (crow < 0) continue;
+          for (int c = 0; c < DD; ++c)
+            for (int d = 0; d < DD; ++d)
+              if (fm[static_cast<size_t>(k) * DD + c] && fm[static_cast<size_t>(nbn) * DD + d])
+                dense[static_cast<size_t>(rrow * DD + c) * n + crow * DD + d] =
+                    vals_h[static_cast<size_t>(rrow) * B.row_len + c * cpad(slots_nzb[rrow], DD) + pos * DD + d];
+        }
+        for (int c = 0; c < DD; ++c)
+          if (!fm[static_cast<size_t>(k) * DD + c]) dense[static_cast<size_t>(rrow * DD + c) * n + rrow * DD + c] = 1.0;
+      }
+      std::vector<double> inv = invert_dense(dense, n);
+      mg_dense.ensure(static_cast<size_t>(n) * n);
+      CK(cudaMemcpyAsync(mg_dense.p, inv.data(), sizeof(double) * inv.size(), cudaMemcpyHostToDevice, s));
+      sync();
+    }
+  }
+
+  // Gauss-Jordan with partial pivoting (coarsest level, n <= ~600)
+  static std::vector<double> invert_dense(std::vector<double> a, int n) {
+    std::vector<double> inv(static_cast<size_t>(n) * n, 0.0);
+    for (int i = 0; i < n; ++i) inv[static_cast<size_t>(i) * n + i] = 1.0;
+    for (int c = 0; c < n; ++c) {
+      int p = c;
+      for (int r2 = c + 1; r2 < n; ++r2)
+        if (std::abs(a[static_cast<size_t>(r2) * n + c]) > std::abs(a[static_cast<size_t>(p) * n + c])) p = r2;
+      if (a[static_cast<size_t>(p) * n + c] == 0.0) continue;  // singular direction: leave it
+      if (p != c)
+        for (int j = 0; j < n; ++j) {
+          std::swap(a[static_cast<size_t>(p) * n + j], a[static_cast<size_t>(c) * n + j]);
+          std::swap(inv[static_cast<size_t>(p) * n + j], inv[static_cast<size_t>(c) * n + j]);
+        }
+      const double d = 1.0 / a[static_cast<size_t>(c) * n + c];
+      for (int j = 0; j < n; ++j) {
+        a[static_cast<size_t>(c) * n + j] *= d;
+        inv[static_cast<size_t>(c) * n + j] *= d;
+      }
+      for (int r2 = 0; r2 < n; ++r2) {
+        if (r2 == c) continue;
+        const double f = a[static_cast<size_t>(r2) * n + c];
+        if (f == 0.0) continue;
+        for (int j = 0; j < n; ++j) {
+          a[static_cast<size_t>(r2) * n + j] -= f * a[static_cast<size_t>(c) * n + j];
+          inv[static_cast<size_t>(r2) * n + j] -= f * inv[static_cast<size_t>(c) * n + j];
+        }
+      }
+    }
+    return inv;
+  }
+
+  // z = V-cycle(b) at level l; result in mg[l]->x
+  template <int DD>
+  void vcycle(size_t l, const double* b) {
+    MgLevel& L = *mg[l];
+    if (l + 1 == mg.size()) {
+      if (mg_dense_n > 0) {
+        k_dense_apply<<<std::min<unsigned>(blocks_for(mg_dense_n, 128), 148), 128, 0, s>>>(
+            mg_dense_n, DD, dflag.p, L.act_list, mg_dense.p, b, L.x); ++g_launches;
+        CKL();
+      }
+      return;
+    }
+    const int nu = opt.mg_smooth > 0 ? opt.mg_smooth : 2;
+    // pre-smoothing from x = 0
+    k_jacobi0<DD><<<kRedBlocks, kThreads, 0, s>>>(L.n_act, dflag.p, L.act_list, L.dinv, L.freem, L.omega, b, L.x);
+    ++g_launches;
+    CKL();
+    for (int i = 1; i < nu; ++i) {
+      level_spmv<DD, kSpmvJacobi>(L, L.x, L.t, b, L.omega, nullptr, nullptr);
+      std::swap(L.x, L.t);
+    }
+    level_spmv<DD, kSpmvResid>(L, L.x, L.r.p, b, 0.0, nullptr, nullptr);
+    MgLevel& C = *mg[l + 1];
+    k_restrict<DD, DD><<<blocks_for(C.g.N), kThreads, 0, s>>>(L.g, C.g, dflag.p, L.r.p, C.freem, C.bvec.p);
+    ++g_launches;
+    CKL();
+    vcycle<DD>(l + 1, C.bvec.p);
+    k_prolong_add<DD, DD><<<blocks_for(L.g.N), kThreads, 0, s>>>(L.g, C.g, dflag.p, C.x, L.freem, L.x);
+    ++g_launches;
+    CKL();
+    for (int i = 0; i < nu; ++i) {
+      level_spmv<DD, kSpmvJacobi>(L, L.x, L.t, b, L.omega, nullptr, nullptr);
+      std::swap(L.x, L.t);
+    }
+  }
+
+  // MG-preconditioned CG (device-resident scalars, batched host checks)
+  template <int DD>
+  int cg_mg_solve(const double* b, double* x) {
+    const int N = g.N;
+    const int64_t n = NF();
+    const int max_it = opt.krylov_max_iter > 0 ? opt.krylov_max_iter : std::min(20000, std::max(100, 10 * n_dofs));
+    const double rtol2 = opt.krylov_rtol * opt.krylov_rtol;
+    {
+      Prof::Scope ps(&prof, kcMgSetup);
+      mg_setup<DD>();
+    }
+    CK(cudaMemsetAsync(dflag.p, 0, sizeof(int), s));
+    double* partA = partials.p;
+    double* partB = partials.p + 2 * kRedBlocks;
+    CK(cudaMemsetAsync(x, 0, sizeof(double) * n, s));
+    CK(cudaMemcpyAsync(kr.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    {
+      Prof::Scope ps(&prof, kcVcycle);
+      vcycle<DD>(0, kr.p);
+    }
+    const double* z = mg[0]->x;
+    CK(cudaMemcpyAsync(kp.p, z, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    k_dot2<<<kRedBlocks, kThreads, 0, s>>>(n, kr.p, z, b, b, partials.p); ++g_launches;
+    k_finalize_sum<2><<<1, 1024, 0, s>>>(partials.p, kRedBlocks, sums.p); ++g_launches;
+    k_cg_start<<<1, 1, 0, s>>>(sums.p, sc.p, rtol2); ++g_launches;
+    CKL();
+    CK(cudaMemcpyAsync(h_sc, sc.p, sizeof(double) * kNSlots, cudaMemcpyDeviceToHost, s));
+    sync();
+    if (h_sc[kDone] != 0.0) return 0;
+    const int batch = n_dofs < 20000 ? 8 : 4;
+    int done = 0;
+    for (int it = 0; !done;) {
+      for (int i = 0; i < batch; ++i, ++it) {
+        const int par = it & 1;
+        spmv(kp.p, kq.p, kp.p, partA);
+        {
+          Prof::Scope ps(&prof, kcKrylov);
+          k_cg_update_mg<DD><<<kRedBlocks, kThreads, 0, s>>>(N, act_idx.p, sc.p, dflag.p, par, partA, kRedBlocks, x,
+                                                             kr.p, kp.p, kq.p, partB + kRedBlocks); ++g_launches;
+          CKL();
+        }
+        {
+          Prof::Scope ps(&prof, kcVcycle);
+          vcycle<DD>(0, kr.p);
+        }
+        z = mg[0]->x;
+        Prof::Scope ps(&prof, kcKrylov);
+        k_dot1<<<kRedBlocks, kThreads, 0, s>>>(n, dflag.p, kr.p, z, partB); ++g_launches;
+        k_cg_p2<DD><<<kRedBlocks, kThreads, 0, s>>>(N, act_idx.p, sc.p, dflag.p, par, it, partB, kRedBlocks, rtol2,
+                                                    max_it, z, kp.p); ++g_launches;
+        CKL();
+      }
+      CK(cudaMemcpyAsync(&done, dflag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(h_sc, sc.p, sizeof(double) * kNSlots, cudaMemcpyDeviceToHost, s));
+      sync();
+      prof.flush();
+    }
+    const int iters = static_cast<int>(h_sc[kIters]);
+    if (done == 2) return -iters - 1;
+    if (done == 3) throw SimError(IMPM_ERR_LINEAR_SOLVER, "Krylov breakdown: NaN residual");
+    if (done == 4) {
+      const double rel = std::sqrt(h_sc[kRr] / h_sc[kBb]);
+      if (!(rel <= 1e-6))
+        throw SimError(IMPM_ERR_LINEAR_SOLVER, "MG-CG did not converge: relative residual " + std::to_string(rel));
+    }
+    return iters;
+  }
+
   // delta = J^-1 rhs (grid layout); returns Krylov iterations
   int solve_dev(const double* rhs, double* x) {
     auto run = [&](auto Fc) -> int {
       constexpr int FF = decltype(Fc)::value;
       if (opt.krylov != IMPM_KRYLOV_BICGSTAB) {
-        const int it = cg_solve<FF>(rhs, x);
+        const int it = opt.precond == IMPM_PRECOND_MG ? cg_mg_solve<FF>(rhs, x) : cg_solve<FF>(rhs, x);
         if (it >= 0) return it;
         if (opt.krylov == IMPM_KRYLOV_CG) throw SimError(IMPM_ERR_LINEAR_SOLVER, "CG breakdown: J not SPD");
         return -it - 1 + bicgstab_solve<FF>(rhs, x);
@@ -897,7 +1284,8 @@ struct Sim {
     dispatch([&](auto Dc, auto) {
       constexpr int DD = decltype(Dc)::value;
       k_csr_fill<DD, DD><<<blocks_for(n_dofs), kThreads, 0, s>>>(g, n_dofs, node_of.p, field_of.p, dof_of.p, act_idx.p,
-                                                                 vals.p, row_len, rowptr.p, dcols.p,
+                                                                 vals.p, row_len, row_slots.p, row_nzb.p, rowptr.p,
+                                                                 dcols.p,
                                                                  vals_h ? dvals.p : nullptr); ++g_launches;
       CKL();
     });
@@ -1198,7 +1586,10 @@ impm_status impm_sim_matrix_info(impm_sim* h, int64_t* n_rows, int64_t* row_valu
   SIM;
   API_BEGIN(sim)
   if (n_rows) *n_rows = sim->n_act;
-  if (row_values) *row_values = sim->row_len;
+  if (row_values) {
+    sim->sync();
+    *row_values = static_cast<int64_t>(sim->h_nzb_total) * sim->F * sim->F;  // stored block values (all rows)
+  }
   if (ref_nnz) *ref_nnz = sim->step_built ? sim->ref_nnz() : 0;
   API_END(sim)
 }

@@ -18,6 +18,7 @@ from .particles import GridSpec, ParticleArray, particle_doubles
 MATERIAL_KINDS = {"hencky": 0, "hencky_j2": 1, "neo_hookean": 2}
 SHAPES = {"gimp": 1, "quadratic-bspline": 2, "quadratic_bspline": 2}
 KRYLOV = {"auto": 0, "cg": 1, "bicgstab": 2}
+PRECOND = {"mg": 0, "multigrid": 0, "block_jacobi": 1, "jacobi": 1}
 
 
 @dataclass
@@ -53,11 +54,13 @@ class SolverOptions:
     krylov_rtol: float = 1e-12
     krylov_max_iter: int = 0
     profile: bool = False
+    precond: str = "mg"
+    mg_smooth: int = 2
 
     def to_c(self):
         return _abi.Options(self.tol, self.abs_floor, int(self.max_iterations), int(bool(self.total_lagrangian)),
                             SHAPES[self.shape], KRYLOV[self.krylov], self.krylov_rtol, int(self.krylov_max_iter),
-                            int(bool(self.profile)))
+                            int(bool(self.profile)), PRECOND[self.precond], int(self.mg_smooth))
 
 
 @dataclass
