@@ -84,7 +84,7 @@ typedef struct impm_options {
   int32_t krylov_max_iter;    /* 0 => 10*n_dofs capped at 20000 */
   int32_t profile;            /* 1: per-kernel-class CUDA-event timing */
   int32_t precond;            /* impm_precond_kind */
-  int32_t mg_smooth;          /* multigrid pre/post block-Jacobi sweeps (0 => 2) */
+  int32_t mg_smooth;          /* multigrid pre/post block-Jacobi sweeps (0 => 1) */
 } impm_options;
 
 /* impm::StepRecord (mpm_solver.hpp:38-46) + GPU counters. rel_residuals is

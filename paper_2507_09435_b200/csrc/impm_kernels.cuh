@@ -633,165 +633,277 @@ __global__ void k_tangent(GridC g, const double* __restrict__ pd, int64_t cap, i
   }
 }
 
-// Jacobian assembly (K6 phase B): one warp per active node row k. For every
-// particle p whose support contains k (fixed order), lane t < |supp(p)|
-// adds the block (k, l_t) = sum_f H_k[c][d][f] grad_{l_t, f}, with
-// H_k[c][d][f] = sum_b grad_{k,b} A_p[c b][d f], into a shared-memory row
-// accumulator. Rows are written once, coalesced; no atomics. The row's
-// diagonal block inverse (block-Jacobi, masked to free components) is fused.
-template <int D, int SHAPE, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32) k_assemble(GridC g, const double* __restrict__ pd, int64_t cap,
-                                                         const double* __restrict__ xs, const int* __restrict__ bin_start,
-                                                         const int* __restrict__ sup, const double* __restrict__ A,
-                                                         const int* __restrict__ act_list, int n_act,
-                                                         const uint8_t* __restrict__ freem, double* __restrict__ vals,
-                                                         int64_t row_len, double* __restrict__ dinv,
-                                                         uint8_t* __restrict__ row_slots, int* __restrict__ row_nzb,
-                                                         unsigned long long* __restrict__ nzb_total) {
-  constexpr int DD = D * D;
-  constexpr int S = ipow_c(5, D);
-  constexpr int ACC = S * DD;
-  constexpr int NH = D * D * D;
-  constexpr int WS = ACC + NH + (2 * S + 7) / 8;  // doubles per warp: acc, H, touched + slot list bytes
-  extern __shared__ double smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* acc = smem + warp * WS;
-  double* H = acc + ACC;
-  uint8_t* touched = reinterpret_cast<uint8_t*>(H + NH);
-  uint8_t* clist = touched + S;
-  const int row = blockIdx.x * WARPS + warp;
-  if (row >= n_act) return;
-  const int k = act_list[row];
-  int kidx[3];
-  unflat<D>(g, k, kidx);
-  for (int j = lane; j < ACC; j += 32) acc[j] = 0.0;
-  for (int j = lane; j < S; j += 32) touched[j] = 0;
-  __syncwarp();
-  for_each_particle_of_node<D>(g, kidx, bin_start, sup, [&](int p, const int* off) {
-    // lanes a*3+i evaluate the 1D weights of axis a at support node i
-    int cnt[3], bfirst[3];
-    const int sp = sup[p];
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      cnt[a] = sup_cnt(sp, a);
-      bfirst[a] = kidx[a] - off[a];
-    }
-    double w1 = 0.0, dw1 = 0.0;
-    if (lane < 3 * D) {
-      const int a = lane / 3, i = lane % 3;
-      int ca = cnt[0], fa = bfirst[0];
-#pragma unroll
-      for (int b = 1; b < D; ++b)
-        if (a == b) {
-          ca = cnt[b];
-          fa = bfirst[b];
-        }
-      if (i < ca) {
-        const WeightValue wv = weight_1d<SHAPE>(xs[a * cap + p] - node_coord(g, a, fa + i),
-                                                pd[(PF<D>::lp + a) * cap + p], g.h);
-        w1 = wv.w;
-        dw1 = wv.dw;
-      }
-    }
-    double wa[3][3], dwa[3][3];
-#pragma unroll
+// ------------------------------------------- K6 Jacobian: structure ------
+// Per bin (= first support node): bit a set when some particle of the bin
+// has a 3-node support on axis a; bit 7 = bin non-empty.
+__global__ void k_bin_flags(int N, int D, const int* __restrict__ bin_start, const int* __restrict__ sup,
+                            uint8_t* __restrict__ bflag) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= N) return;
+  const int s0 = bin_start[b], e0 = bin_start[b + 1];
+  int f = 0;
+  for (int p = s0; p < e0; ++p)
     for (int a = 0; a < D; ++a)
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        wa[a][i] = __shfl_sync(0xffffffffu, w1, a * 3 + i);
-        dwa[a][i] = __shfl_sync(0xffffffffu, dw1, a * 3 + i);
-      }
-    // gradient of node k
-    double gk[3];
-    {
-      double w[3], dw[3], W;
-#pragma unroll
-      for (int a = 0; a < D; ++a) {
-        w[a] = wa[a][off[a]];
-        dw[a] = dwa[a][off[a]];
-      }
-      tensor_weight<D>(w, dw, W, gk);
-    }
-    const double* Ap = A + static_cast<int64_t>(p) * DD * DD;
-    if (lane < NH) {
-      const int c = lane / DD, df = lane % DD;
-      double s = 0.0;
-#pragma unroll
-      for (int b = 0; b < D; ++b) s += gk[b] * Ap[(c * D + b) * DD + df];
-      H[lane] = s;
-    }
-    __syncwarp();
-    const int nsup = cnt[0] * (D > 1 ? cnt[1] : 1) * (D > 2 ? cnt[2] : 1);
-    if (lane < nsup) {
-      int li[3] = {0, 0, 0};
-      int rem = lane;
+      if (sup_cnt(sup[p], a) == 3) f |= 1 << a;
+  bflag[b] = static_cast<uint8_t>(e0 > s0 ? (0x80 | f) : 0);
+}
+
+// Row structure (once per load step: it does not depend on u): the stored
+// block columns of row k are the box offsets l - k of every bin support box
+// containing k (a superset of the particle-pair couplings; the reference
+// pattern, jacobian.hpp:36-65, is the full +-2 box). Ascending slot list,
+// count and a 128-bit slot mask (position = popcount below the slot).
+template <int D>
+__global__ void k_row_structure(GridC g, const int* __restrict__ act_list, int n_act,
+                                const uint8_t* __restrict__ bflag, uint8_t* __restrict__ row_slots,
+                                int* __restrict__ row_nzb, unsigned* __restrict__ row_mask,
+                                unsigned long long* __restrict__ nzb_total) {
+  constexpr int S = ipow_c(5, D);
+  constexpr int NB = ipow_c(3, D);
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long cnt = 0;
+  if (row < n_act) {
+    const int k = act_list[row];
+    int kidx[3];
+    unflat<D>(g, k, kidx);
+    unsigned m[4] = {0u, 0u, 0u, 0u};
+    for (int ob = 0; ob < NB; ++ob) {
+      int off[3] = {0, 0, 0}, r = ob, b = 0;
+      bool ok = true;
 #pragma unroll
       for (int a = D - 1; a >= 0; --a) {
-        li[a] = rem % cnt[a];
-        rem /= cnt[a];
+        off[a] = r % 3;
+        r /= 3;
+        ok = ok && kidx[a] - off[a] >= 0;
+        b += (kidx[a] - off[a]) * g.stride[a];
       }
-      double w[3], dw[3], W, gl[3];
-      int slot = 0;
+      if (!ok) continue;
+      const int fl = bflag[b];
+      if (!(fl & 0x80)) continue;
+      int cn[3] = {1, 1, 1};
 #pragma unroll
       for (int a = 0; a < D; ++a) {
-        w[a] = wa[a][li[a]];
-        dw[a] = dwa[a][li[a]];
-        slot = slot * 5 + (li[a] - off[a] + 2);
+        cn[a] = 2 + ((fl >> a) & 1);
+        ok = ok && off[a] < cn[a];
       }
-      tensor_weight<D>(w, dw, W, gl);
-      touched[slot] = 1;
-      double* blk = acc + slot * DD;
+      if (!ok) continue;
+      for (int i0 = 0; i0 < cn[0]; ++i0)
+        for (int i1 = 0; i1 < (D > 1 ? cn[1] : 1); ++i1)
+          for (int i2 = 0; i2 < (D > 2 ? cn[2] : 1); ++i2) {
+            const int li[3] = {i0, i1, i2};
+            int sl = 0;
 #pragma unroll
-      for (int c = 0; c < D; ++c)
+            for (int a = 0; a < D; ++a) sl = sl * 5 + (li[a] - off[a] + 2);
+            m[sl >> 5] |= 1u << (sl & 31);
+          }
+    }
+    int pos = 0;
+    uint8_t* out = row_slots + static_cast<int64_t>(row) * S;
+    for (int w = 0; w < 4; ++w) {
+      unsigned bits = m[w];
+      row_mask[static_cast<int64_t>(row) * 4 + w] = bits;
+      while (bits) {
+        const int bt = __ffs(bits) - 1;
+        bits &= bits - 1;
+        out[pos++] = static_cast<uint8_t>(w * 32 + bt);
+      }
+    }
+    row_nzb[row] = pos;
+    cnt = pos;
+  }
+  // one atomic per warp (integer: order-independent)
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_down_sync(0xffffffffu, cnt, o);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(nzb_total, cnt);
+}
+
+__device__ __forceinline__ int mask_pos(const unsigned* m, int sl) {
+  int pos = 0;
+  const int w = sl >> 5;
 #pragma unroll
-        for (int d = 0; d < D; ++d) {
-          double s = 0.0;
+  for (int i = 0; i < 4; ++i)
+    if (i < w) pos += __popc(m[i]);
+  return pos + __popc(m[w] & ((1u << (sl & 31)) - 1u));
+}
+
+// zero the stored part of every row (component chunks incl. padding)
+__global__ void k_zero_rows(int n_act, int F, const int* __restrict__ row_nzb, double* __restrict__ vals,
+                            int64_t row_len) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= n_act) return;
+  const int n = F * cpad(row_nzb[warp], F);
+  double* r = vals + static_cast<int64_t>(warp) * row_len;
+  for (int j = lane; j < n; j += 32) r[j] = 0.0;
+}
+
+// ------------------------------------------- K6 Jacobian: numeric ---------
+// Colour-batched, bin-centric assembly. Bins of colour (c_a = idx_a mod 3)
+// are >= 3 nodes apart per axis, so their support boxes (<= 3 nodes/axis)
+// and hence their (k, l) blocks are disjoint: one warp owns a bin and adds
+// its element blocks straight into the BSR rows, no atomics, fixed order.
+// Per particle: 1D weights (lanes < 3D), node gradients g^k (lane per box
+// node), H_k[c][d][f] = sum_b g^k_b A_p[cb][df] (lanes over (k, cdf)); then
+// every lane accumulates its PPL block pairs (k, l) += H_k . g^l over the
+// bin's particles in registers before one read-modify-write.
+template <int D, int SHAPE, int PPL, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_assemble_bins(
+    GridC g, const double* __restrict__ pd, int64_t cap, const double* __restrict__ xs,
+    const int* __restrict__ bin_start, const uint8_t* __restrict__ bflag, const double* __restrict__ A,
+    const int* __restrict__ act_idx, const unsigned* __restrict__ row_mask, const int* __restrict__ row_nzb,
+    double* __restrict__ vals, int64_t row_len, int c0, int c1, int c2, int nb0, int nb1, int nb2) {
+  constexpr int DD = D * D;
+  constexpr int D3 = D * D * D;
+  constexpr int NK = ipow_c(3, D);
+  __shared__ double W1s[WARPS][3][3], DW1s[WARPS][3][3];
+  __shared__ double Gs[WARPS][NK][3];
+  __shared__ double Hs[WARPS][NK * D3];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nbins = nb0 * nb1 * nb2;
+  const int col[3] = {c0, c1, c2};
+  const int nbv[3] = {nb0, nb1, nb2};
+  for (int bi = blockIdx.x * WARPS + warp; bi < nbins; bi += gridDim.x * WARPS) {
+    int bidx[3] = {0, 0, 0}, r = bi, b = 0;
 #pragma unroll
-          for (int f = 0; f < D; ++f) s += H[(c * D + d) * D + f] * gl[f];
-          blk[c * D + d] += s;
+    for (int a = D - 1; a >= 0; --a) {
+      bidx[a] = 3 * (r % nbv[a]) + col[a];
+      r /= nbv[a];
+      b += bidx[a] * g.stride[a];
+    }
+    const int fl = bflag[b];
+    if (!(fl & 0x80)) continue;
+    int cn[3] = {1, 1, 1};
+#pragma unroll
+    for (int a = 0; a < D; ++a) cn[a] = 2 + ((fl >> a) & 1);
+    const int nk = cn[0] * cn[1] * cn[2];
+    const int npairs = nk * nk;
+    const int p0 = bin_start[b], p1 = bin_start[b + 1];
+    for (int q0 = 0; q0 < npairs; q0 += 32 * PPL) {
+      double acc[PPL][DD];
+#pragma unroll
+      for (int t = 0; t < PPL; ++t)
+#pragma unroll
+        for (int e = 0; e < DD; ++e) acc[t][e] = 0.0;
+      for (int p = p0; p < p1; ++p) {
+        if (lane < 3 * D) {
+          const int a = lane / 3, i = lane % 3;
+          double w = 0.0, dw = 0.0;
+          if (i < cn[a]) {
+            const WeightValue wv = weight_1d<SHAPE>(xs[a * cap + p] - node_coord(g, a, bidx[a] + i),
+                                                    pd[(PF<D>::lp + a) * cap + p], g.h);
+            w = wv.w;
+            dw = wv.dw;
+          }
+          W1s[warp][a][i] = w;
+          DW1s[warp][a][i] = dw;
         }
+        __syncwarp();
+        for (int k = lane; k < nk; k += 32) {
+          int li[3] = {0, 0, 0}, rr = k;
+#pragma unroll
+          for (int a = D - 1; a >= 0; --a) {
+            li[a] = rr % cn[a];
+            rr /= cn[a];
+          }
+          double w[3], dw[3], W, gk[3];
+#pragma unroll
+          for (int a = 0; a < D; ++a) {
+            w[a] = W1s[warp][a][li[a]];
+            dw[a] = DW1s[warp][a][li[a]];
+          }
+          tensor_weight<D>(w, dw, W, gk);
+#pragma unroll
+          for (int a = 0; a < D; ++a) Gs[warp][k][a] = gk[a];
+        }
+        __syncwarp();
+        const double* Ap = A + static_cast<int64_t>(p) * DD * DD;
+        for (int e = lane; e < nk * D3; e += 32) {
+          const int k = e / D3, cdf = e - k * D3, c = cdf / DD, df = cdf - c * DD;
+          double sacc = 0.0;
+#pragma unroll
+          for (int bb = 0; bb < D; ++bb) sacc += Gs[warp][k][bb] * __ldg(Ap + (c * D + bb) * DD + df);
+          Hs[warp][e] = sacc;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int t = 0; t < PPL; ++t) {
+          const int q = q0 + lane + 32 * t;
+          if (q < npairs) {
+            const int k = q / nk, l = q - k * nk;
+            const double* Hk = &Hs[warp][k * D3];
+            double gl[3];
+#pragma unroll
+            for (int f = 0; f < D; ++f) gl[f] = Gs[warp][l][f];
+#pragma unroll
+            for (int cd = 0; cd < DD; ++cd) {
+              double sacc = 0.0;
+#pragma unroll
+              for (int f = 0; f < D; ++f) sacc += Hk[cd * D + f] * gl[f];
+              acc[t][cd] += sacc;
+            }
+          }
+        }
+        __syncwarp();
+      }
+      // read-modify-write of the owned blocks (exclusive within this colour)
+#pragma unroll
+      for (int t = 0; t < PPL; ++t) {
+        const int q = q0 + lane + 32 * t;
+        if (q >= npairs) continue;
+        const int k = q / nk, l = q - k * nk;
+        int lk[3] = {0, 0, 0}, ll[3] = {0, 0, 0}, rk = k, rl = l, node = 0, sl = 0;
+#pragma unroll
+        for (int a = D - 1; a >= 0; --a) {
+          lk[a] = rk % cn[a];
+          rk /= cn[a];
+          ll[a] = rl % cn[a];
+          rl /= cn[a];
+        }
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          node += (bidx[a] + lk[a]) * g.stride[a];
+          sl = sl * 5 + (ll[a] - lk[a] + 2);
+        }
+        const int row = act_idx[node];
+        if (row < 0) continue;
+        const unsigned* m = row_mask + static_cast<int64_t>(row) * 4;
+        const int pos = mask_pos(m, sl);
+        const int cp = cpad(row_nzb[row], D);
+        double* rv = vals + static_cast<int64_t>(row) * row_len + pos * D;
+#pragma unroll
+        for (int c = 0; c < D; ++c)
+#pragma unroll
+          for (int d = 0; d < D; ++d) rv[c * cp + d] += acc[t][c * D + d];
+      }
     }
-    __syncwarp();
-  });
-  // compact the structurally nonzero blocks (touched by a particle pair) in
-  // ascending slot order; the SpMV streams only these
-  int base = 0;
-  for (int s0 = 0; s0 < S; s0 += 32) {
-    const int sl = s0 + lane;
-    const bool f = sl < S && touched[sl];
-    const unsigned m = __ballot_sync(0xffffffffu, f);
-    if (f) {
-      const int pos = base + __popc(m & ((1u << lane) - 1u));
-      clist[pos] = static_cast<uint8_t>(sl);
-      row_slots[static_cast<int64_t>(row) * S + pos] = static_cast<uint8_t>(sl);
+  }
+}
+
+// masked diagonal block inverse per row (block-Jacobi / MG smoother)
+template <int D>
+__global__ void k_diag_inverse(int n_act, const int* __restrict__ act_list, const uint8_t* __restrict__ freem,
+                               const unsigned* __restrict__ row_mask, const int* __restrict__ row_nzb,
+                               const double* __restrict__ vals, int64_t row_len, double* __restrict__ dinv) {
+  constexpr int S = ipow_c(5, D);
+  constexpr int DD = D * D;
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= n_act) return;
+  const int k = act_list[row];
+  const unsigned* m = row_mask + static_cast<int64_t>(row) * 4;
+  const int sc = (S - 1) / 2;
+  const bool has = (m[sc >> 5] >> (sc & 31)) & 1u;
+  const int pos = mask_pos(m, sc);
+  const int cp = cpad(row_nzb[row], D);
+  const double* rv = vals + static_cast<int64_t>(row) * row_len + pos * D;
+  Mat<double, D> Mb;
+#pragma unroll
+  for (int c = 0; c < D; ++c)
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const bool fr = freem[static_cast<int64_t>(k) * D + c] && freem[static_cast<int64_t>(k) * D + d];
+      Mb(c, d) = (has && fr) ? rv[c * cp + d] : (c == d ? 1.0 : 0.0);
     }
-    base += __popc(m);
-  }
-  __syncwarp();
-  const int nzb = base;
-  double* dst = vals + static_cast<int64_t>(row) * row_len;
-  const int cp = cpad(nzb, D);
-  for (int j = lane; j < D * cp; j += 32) {
-    const int c = j / cp, rem = j - c * cp, pos = rem / D, d = rem - pos * D;
-    dst[j] = rem < nzb * D ? acc[clist[pos] * DD + c * D + d] : 0.0;
-  }
-  if (lane == 0) {
-    row_nzb[row] = nzb;
-    atomicAdd(nzb_total, static_cast<unsigned long long>(nzb));
-    // masked diagonal block inverse: [D_ff 0; 0 I]^-1
-    const double* blk = acc + (S - 1) / 2 * DD;
-    bool fr[3];
+  const Mat<double, D> Mi = inverse(Mb);
 #pragma unroll
-    for (int c = 0; c < D; ++c) fr[c] = freem[k * D + c] != 0;
-    Mat<double, D> Mb;
-#pragma unroll
-    for (int c = 0; c < D; ++c)
-#pragma unroll
-      for (int d = 0; d < D; ++d) Mb(c, d) = (fr[c] && fr[d]) ? blk[c * D + d] : (c == d ? 1.0 : 0.0);
-    const Mat<double, D> Mi = inverse(Mb);
-#pragma unroll
-    for (int i = 0; i < DD; ++i) dinv[static_cast<int64_t>(row) * DD + i] = Mi.e[i];
-  }
+  for (int i = 0; i < DD; ++i) dinv[static_cast<int64_t>(row) * DD + i] = Mi.e[i];
 }
 
 // -------------------------------------------------------------- K7 SpMV --

@@ -185,8 +185,9 @@ struct Sim {
   DBuf<double> kx, kr, kz, kp, kq, kv, ks, kt, khat;
   // matrix
   DBuf<double> vals, dinv;
-  DBuf<uint8_t> row_slots;
+  DBuf<uint8_t> row_slots, bflag;
   DBuf<int> row_nzb;
+  DBuf<unsigned> row_mask;
   DBuf<unsigned long long> nzb_total;
   unsigned long long h_nzb_total = 0;
   int64_t row_len = 0;
@@ -504,7 +505,25 @@ struct Sim {
     dinv.ensure(std::max<int64_t>(1, static_cast<int64_t>(n_act) * F * F));
     row_slots.ensure(std::max<int64_t>(1, static_cast<int64_t>(n_act) * S));
     row_nzb.ensure(std::max(1, n_act));
+    row_mask.ensure(std::max<int64_t>(1, static_cast<int64_t>(n_act) * 4));
+    bflag.ensure(N);
     nzb_total.ensure(1);
+    {
+      // Jacobian sparsity structure of this step (independent of u)
+      Prof::Scope ps(&prof, kcDof);
+      k_bin_flags<<<blocks_for(N), kThreads, 0, s>>>(N, D, bin_start.p, sup.p, bflag.p); ++g_launches;
+      CK(cudaMemsetAsync(nzb_total.p, 0, sizeof(unsigned long long), s));
+      if (n_act > 0) {
+        dispatch([&](auto Dc, auto) {
+          constexpr int DD = decltype(Dc)::value;
+          k_row_structure<DD><<<blocks_for(n_act), kThreads, 0, s>>>(g, act_list.p, n_act, bflag.p, row_slots.p,
+                                                                      row_nzb.p, row_mask.p, nzb_total.p);
+          ++g_launches;
+        });
+      }
+      CKL();
+      CK(cudaMemcpyAsync(&h_nzb_total, nzb_total.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    }
     CK(cudaMemsetAsync(u.p, 0, sizeof(double) * NF(), s));
     matrix_valid = false;
     step_built = true;
@@ -555,16 +574,26 @@ struct Sim {
       }
       if (n_act > 0) {
         Prof::Scope ps(&prof, kcAssemble);
-        constexpr int W = DD == 3 ? 4 : 8;
-        constexpr int S = ipow_c(5, DD);
-        const size_t smem = sizeof(double) * W * (S * DD * DD + DD * DD * DD + (2 * S + 7) / 8);
-        auto kern = k_assemble<DD, SH, W>;
-        if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        CK(cudaMemsetAsync(nzb_total.p, 0, sizeof(unsigned long long), s));
-        kern<<<blocks_for(n_act, W), W * 32, smem, s>>>(g, pd.p, cap, xs.p, bin_start.p, sup.p, Atan.p, act_list.p,
-                                                        n_act, freem.p, vals.p, row_len, dinv.p, row_slots.p,
-                                                        row_nzb.p, nzb_total.p);
-        CK(cudaMemcpyAsync(&h_nzb_total, nzb_total.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s)); ++g_launches;
+        k_zero_rows<<<blocks_for(static_cast<int64_t>(n_act) * 32), kThreads, 0, s>>>(n_act, DD, row_nzb.p, vals.p,
+                                                                                    row_len); ++g_launches;
+        constexpr int W = 4;
+        constexpr int PPL = DD == 3 ? 5 : (DD == 2 ? 3 : 1);
+        const int nc = ipow_c(3, DD);
+        for (int col = 0; col < nc; ++col) {
+          int cc[3] = {0, 0, 0}, nb[3] = {1, 1, 1}, r = col;
+          for (int a = DD - 1; a >= 0; --a) {
+            cc[a] = r % 3;
+            r /= 3;
+            nb[a] = std::max(0, (g.nodes[a] - cc[a] + 2) / 3);
+          }
+          const int nbins = nb[0] * nb[1] * nb[2];
+          if (nbins == 0) continue;
+          k_assemble_bins<DD, SH, PPL, W><<<std::min<unsigned>(blocks_for(nbins, W), 148 * 16), W * 32, 0, s>>>(
+              g, pd.p, cap, xs.p, bin_start.p, bflag.p, Atan.p, act_idx.p, row_mask.p, row_nzb.p, vals.p, row_len,
+              cc[0], cc[1], cc[2], nb[0], nb[1], nb[2]); ++g_launches;
+        }
+        k_diag_inverse<DD><<<blocks_for(n_act), kThreads, 0, s>>>(n_act, act_list.p, freem.p, row_mask.p, row_nzb.p,
+                                                                   vals.p, row_len, dinv.p); ++g_launches;
         CKL();
       }
     });
@@ -953,7 +982,7 @@ struct Sim {
       }
       return;
     }
-    const int nu = opt.mg_smooth > 0 ? opt.mg_smooth : 2;
+    const int nu = opt.mg_smooth > 0 ? opt.mg_smooth : 1;
     // pre-smoothing from x = 0
     k_jacobi0<DD><<<kRedBlocks, kThreads, 0, s>>>(L.n_act, dflag.p, L.act_list, L.dinv, L.freem, L.omega, b, L.x);
     ++g_launches;

@@ -55,7 +55,7 @@ class SolverOptions:
     krylov_max_iter: int = 0
     profile: bool = False
     precond: str = "mg"
-    mg_smooth: int = 2
+    mg_smooth: int = 1
 
     def to_c(self):
         return _abi.Options(self.tol, self.abs_floor, int(self.max_iterations), int(bool(self.total_lagrangian)),
