@@ -67,7 +67,9 @@ typedef struct impm_material {
 typedef enum impm_shape_kind { IMPM_SHAPE_GIMP = 1, IMPM_SHAPE_BSPLINE2 = 2 } impm_shape_kind;
 
 /* Linear solver behind the sparse_lu_solve seam (src/linear_solver.cpp:11-88). */
-typedef enum impm_krylov_kind { IMPM_KRYLOV_AUTO = 0, IMPM_KRYLOV_CG = 1, IMPM_KRYLOV_BICGSTAB = 2 } impm_krylov_kind;
+typedef enum impm_krylov_kind {
+  IMPM_KRYLOV_AUTO = 0, IMPM_KRYLOV_CG = 1, IMPM_KRYLOV_BICGSTAB = 2, IMPM_KRYLOV_GMRES = 3
+} impm_krylov_kind;
 
 /* Preconditioner of the Krylov solve. */
 typedef enum impm_precond_kind { IMPM_PRECOND_MG = 0, IMPM_PRECOND_BLOCK_JACOBI = 1 } impm_precond_kind;
@@ -105,7 +107,15 @@ typedef struct impm_step_record {
   int64_t nnz_assembled;        /* reference-pattern scalar nnz x iterations */
 } impm_step_record;
 
-typedef struct impm_sim impm_sim; /* opaque: one MpmSim<D> on one device */
+/* impm::PoroParams (porous.hpp:22-38) */
+typedef struct impm_poro {
+  double lambda, mu;  /* Lame constants [Pa] */
+  double k;           /* intrinsic permeability [m^2] */
+  double mu_f;        /* fluid viscosity [Pa s] */
+  double rho_f;       /* fluid density [kg/m^3] */
+} impm_poro;
+
+typedef struct impm_sim impm_sim; /* opaque: one MpmSim<D> (or CoupledSim) on one device */
 
 /* version / capability */
 const char* impm_version(void);
@@ -165,6 +175,20 @@ impm_status impm_sim_step(impm_sim* sim, double load_scale, impm_step_record* re
 /* nodal_solution / set_nodal_solution (mpm_solver.hpp:409-410) */
 impm_status impm_sim_nodal_solution(impm_sim* sim, double* u /*[n]*/);
 impm_status impm_sim_set_nodal_solution(impm_sim* sim, const double* u /*[n]*/);
+
+/* impm::CoupledSim (porous.hpp:48-125): 2D u-p, fields (ux, uy, p) per node,
+ * set_fixed takes [node*3 + field] (fixed_u merged with fixed_p). The shared
+ * impm_sim_residual / _jacobian_csr / _linear_solve take dt as load_scale. */
+impm_status impm_coupled_create(const impm_grid* grid, const impm_poro* poro, const impm_options* opt,
+                                int32_t device, impm_sim** out);
+/* CoupledSim::initialize (src/porous.cpp:25-72): weights at the reference configuration */
+impm_status impm_coupled_initialize(impm_sim* sim);
+/* CoupledSim::step (src/porous.cpp:91-168) */
+impm_status impm_coupled_step(impm_sim* sim, double dt, impm_step_record* rec);
+/* CoupledSim::nodal_pressure (porous.hpp:81) */
+impm_status impm_coupled_nodal_pressure(impm_sim* sim, double* p /*[N]*/);
+/* accumulated vertical displacement per particle (u_total_y_, porous.hpp:118) and time() */
+impm_status impm_coupled_settlement(impm_sim* sim, double* u_total_y /*[P]*/, double* time);
 
 /* Last error of this sim: message, and for NONCONVERGENCE the residual history. */
 impm_status impm_sim_last_error(impm_sim* sim, char* msg, size_t cap, double* history, int32_t* hist_len);

@@ -11,13 +11,13 @@ include/impm_gpu.h.
 from .errors import (ConfigError, CudaError, DomainError, Error, LinearSolverError, NonConvergenceError,
                      OutOfDomainError, SeedingFault, UnsupportedOperation)
 from .particles import GridSpec, ParticleArray, particle_doubles, particle_fields, seed_box
-from .sim import DofMap, ElasticParams, MaterialSpec, MpmSim, SolverOptions, StepRecord
+from .sim import CoupledSim, DofMap, ElasticParams, MaterialSpec, MpmSim, PoroParams, SolverOptions, StepRecord
 
 __all__ = [
     "ConfigError", "CudaError", "DomainError", "Error", "LinearSolverError", "NonConvergenceError",
     "OutOfDomainError", "SeedingFault", "UnsupportedOperation", "GridSpec", "ParticleArray", "particle_doubles",
     "particle_fields", "seed_box", "DofMap", "ElasticParams", "MaterialSpec", "MpmSim", "SolverOptions",
-    "StepRecord", "gimp_weight_1d", "block_size",
+    "StepRecord", "gimp_weight_1d", "block_size", "CoupledSim", "PoroParams",
 ]
 
 

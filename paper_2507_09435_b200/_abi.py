@@ -43,6 +43,10 @@ class Options(ctypes.Structure):
     ]
 
 
+class Poro(ctypes.Structure):
+    _fields_ = [("lambda_", c_double), ("mu", c_double), ("k", c_double), ("mu_f", c_double), ("rho_f", c_double)]
+
+
 class StepRecordC(ctypes.Structure):
     _fields_ = [
         ("step", c_int32),
@@ -73,6 +77,11 @@ _SIGNATURES = {
     "impm_launch_count": (c_int64, []),
     "impm_sim_create": (c_int32, [_P(Grid), _P(Material), _P(Options), c_int32, _P(c_void_p)]),
     "impm_sim_destroy": (c_int32, [c_void_p]),
+    "impm_coupled_create": (c_int32, [_P(Grid), _P(Poro), _P(Options), c_int32, _P(c_void_p)]),
+    "impm_coupled_initialize": (c_int32, [c_void_p]),
+    "impm_coupled_step": (c_int32, [c_void_p, c_double, _P(StepRecordC)]),
+    "impm_coupled_nodal_pressure": (c_int32, [c_void_p, c_void_p]),
+    "impm_coupled_settlement": (c_int32, [c_void_p, c_void_p, _P(c_double)]),
     "impm_sim_set_stream": (c_int32, [c_void_p, c_void_p]),
     "impm_sim_set_particles": (c_int32, [c_void_p, c_void_p, c_int64, c_int64]),
     "impm_sim_get_particles": (c_int32, [c_void_p, c_void_p, c_int64, c_int64]),

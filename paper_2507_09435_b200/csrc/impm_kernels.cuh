@@ -127,14 +127,14 @@ struct DevStatus {
 template <int D, int SHAPE>
 __global__ void k_support(const double* __restrict__ pd, int64_t cap, int P, GridC g,
                           const int* __restrict__ orig, int* __restrict__ key, int* __restrict__ sup,
-                          double* __restrict__ xs, DevStatus* st) {
+                          double* __restrict__ xs, DevStatus* st, int use_X = 0) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P) return;
   int k = 0, packed = 0;
   bool ok = true;
 #pragma unroll
   for (int a = 0; a < D; ++a) {
-    const double x = pd[(PF<D>::x + a) * cap + i];
+    const double x = pd[((use_X ? PF<D>::X : PF<D>::x) + a) * cap + i];
     const double lp = pd[(PF<D>::lp + a) * cap + i];
     xs[a * cap + i] = x;
     int first, count;
@@ -878,12 +878,12 @@ __global__ void __launch_bounds__(WARPS * 32) k_assemble_bins(
 }
 
 // masked diagonal block inverse per row (block-Jacobi / MG smoother)
-template <int D>
+template <int D, int F = D>
 __global__ void k_diag_inverse(int n_act, const int* __restrict__ act_list, const uint8_t* __restrict__ freem,
                                const unsigned* __restrict__ row_mask, const int* __restrict__ row_nzb,
                                const double* __restrict__ vals, int64_t row_len, double* __restrict__ dinv) {
   constexpr int S = ipow_c(5, D);
-  constexpr int DD = D * D;
+  constexpr int DD = F * F;
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= n_act) return;
   const int k = act_list[row];
@@ -891,17 +891,17 @@ __global__ void k_diag_inverse(int n_act, const int* __restrict__ act_list, cons
   const int sc = (S - 1) / 2;
   const bool has = (m[sc >> 5] >> (sc & 31)) & 1u;
   const int pos = mask_pos(m, sc);
-  const int cp = cpad(row_nzb[row], D);
-  const double* rv = vals + static_cast<int64_t>(row) * row_len + pos * D;
-  Mat<double, D> Mb;
+  const int cp = cpad(row_nzb[row], F);
+  const double* rv = vals + static_cast<int64_t>(row) * row_len + pos * F;
+  Mat<double, F> Mb;
 #pragma unroll
-  for (int c = 0; c < D; ++c)
+  for (int c = 0; c < F; ++c)
 #pragma unroll
-    for (int d = 0; d < D; ++d) {
-      const bool fr = freem[static_cast<int64_t>(k) * D + c] && freem[static_cast<int64_t>(k) * D + d];
+    for (int d = 0; d < F; ++d) {
+      const bool fr = freem[static_cast<int64_t>(k) * F + c] && freem[static_cast<int64_t>(k) * F + d];
       Mb(c, d) = (has && fr) ? rv[c * cp + d] : (c == d ? 1.0 : 0.0);
     }
-  const Mat<double, D> Mi = inverse(Mb);
+  const Mat<double, F> Mi = inverse(Mb);
 #pragma unroll
   for (int i = 0; i < DD; ++i) dinv[static_cast<int64_t>(row) * DD + i] = Mi.e[i];
 }
@@ -1772,6 +1772,323 @@ __global__ void k_commit(GridC g, double* __restrict__ pd, int64_t cap, int P, c
       pd[(PF<D>::lp + a) * cap + p] = lp;
     }
   }
+}
+
+
+// ======================================================= coupled u-p (2D) ==
+// CoupledSim (porous.hpp:48-186, src/porous.cpp:25-168): small-strain u-p on
+// weights frozen at the reference configuration, 3 fields per node (ux, uy,
+// p), F = 3 blocks. Grid vectors are [node][3].
+struct PoroC {
+  double lam, mu, mob, rho_f, g0, g1;
+};
+
+// residual phase A: per particle Q = {V0 s'(c,b) (4), V0 p_w, V0 dEv, V0 mob gp (2)}
+template <int SHAPE>
+__global__ void k_up_particles(GridC g, const double* __restrict__ pd, int64_t cap, int P,
+                               const double* __restrict__ xs, const int* __restrict__ key,
+                               const int* __restrict__ sup, const int* __restrict__ orig,
+                               const double* __restrict__ x, PoroC pc, double* __restrict__ Q,
+                               DevStatus* st) {
+  constexpr int D = 2;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  int first[3], cnt[3];
+  AxisW aw[3];
+  particle_weights<D, SHAPE>(g, pd, cap, xs, p, key[p], sup[p], first, cnt, aw);
+  Mat<double, 2> G = Mat<double, 2>::zero();
+  double pw = 0.0, gp[2] = {0.0, 0.0};
+  for_each_support<D>(g, first, cnt, aw, [&](int node, double W, const double* grad) {
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const double uc = x[node * 3 + c];
+#pragma unroll
+      for (int a = 0; a < 2; ++a) G(c, a) += uc * grad[a];
+    }
+    const double pv = x[node * 3 + 2];
+    pw += W * pv;
+#pragma unroll
+    for (int a = 0; a < 2; ++a) gp[a] += pv * grad[a];
+  });
+  Mat<double, 2> f_inc = G;
+  f_inc(0, 0) += 1.0;
+  f_inc(1, 1) += 1.0;
+  Mat<double, 2> Fn;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) Fn.e[i] = pd[(PF<D>::F + i) * cap + p];
+  const Mat<double, 2> F_new = matmul(f_inc, Fn);
+  double* q = Q + static_cast<int64_t>(p) * 8;
+  if (!(det(F_new) > 0.0)) {  // porous.hpp:159-160
+    atomicMin(&st->err_domain, orig[p]);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) q[i] = 0.0;
+    return;
+  }
+  const StressOut<double> su = neo_hookean_update<double, 2>(F_new, pc.lam, pc.mu);
+  const double V0 = pd[PF<D>::V0 * cap + p];
+  q[0] = V0 * su.sigma(0, 0);
+  q[1] = V0 * su.sigma(0, 1);
+  q[2] = V0 * su.sigma(1, 0);
+  q[3] = V0 * su.sigma(1, 1);
+  q[4] = V0 * pw;
+  q[5] = V0 * (G(0, 0) + G(1, 1));
+  q[6] = V0 * (pc.mob * gp[0]);
+  q[7] = V0 * (pc.mob * gp[1]);
+}
+
+// residual phase B (nodes), porous.hpp:165-184 (masked, + partial r.r)
+template <int SHAPE>
+__global__ void k_up_nodes(GridC g, const double* __restrict__ pd, int64_t cap, const double* __restrict__ xs,
+                           const int* __restrict__ bin_start, const int* __restrict__ sup,
+                           const double* __restrict__ Q, const double* __restrict__ bext,
+                           const int* __restrict__ act_flag, const uint8_t* __restrict__ freem, PoroC pc, double dt,
+                           double* __restrict__ r, double* __restrict__ partials) {
+  constexpr int D = 2;
+  double rr[1] = {0.0};
+  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < g.N; n += gridDim.x * blockDim.x) {
+    double acc[3] = {0.0, 0.0, 0.0};
+    if (act_flag[n]) {
+      int idx[3];
+      unflat<D>(g, n, idx);
+      for_each_particle_of_node<D>(g, idx, bin_start, sup, [&](int p, const int*) {
+        double w[3], dw[3];
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          const WeightValue wv = weight_1d<SHAPE>(xs[a * cap + p] - node_coord(g, a, idx[a]),
+                                                  pd[(PF<D>::lp + a) * cap + p], g.h);
+          w[a] = wv.w;
+          dw[a] = wv.dw;
+        }
+        double W, gr[3];
+        tensor_weight<D>(w, dw, W, gr);
+        const double* q = Q + static_cast<int64_t>(p) * 8;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const double fint = gr[0] * q[c * 2] + gr[1] * q[c * 2 + 1] - gr[c] * q[4];
+          acc[c] += fint - W * bext[c * cap + p];
+        }
+        const double V0 = pd[PF<D>::V0 * cap + p];
+        const double flux = gr[0] * q[6] + gr[1] * q[7] - V0 * pc.mob * pc.rho_f * (gr[0] * pc.g0 + gr[1] * pc.g1);
+        acc[2] += W * q[5] + dt * flux;
+      });
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double v = freem[n * 3 + c] ? acc[c] : 0.0;
+      r[n * 3 + c] = v;
+      rr[0] += v * v;
+    }
+  }
+  block_sum_store<1>(rr, partials);
+}
+
+// dP/dG with P = V0 sigma'(f_inc F_n) (the u-p internal force uses reference
+// gradients and V0, porous.hpp:171-173); duals over the 4 entries of G.
+template <int SHAPE>
+__global__ void k_up_tangent(GridC g, const double* __restrict__ pd, int64_t cap, int P,
+                             const double* __restrict__ xs, const int* __restrict__ key,
+                             const int* __restrict__ sup, const double* __restrict__ x, PoroC pc,
+                             double* __restrict__ A) {
+  constexpr int D = 2;
+  using T = Dual<4>;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  int first[3], cnt[3];
+  AxisW aw[3];
+  particle_weights<D, SHAPE>(g, pd, cap, xs, p, key[p], sup[p], first, cnt, aw);
+  Mat<double, 2> G = Mat<double, 2>::zero();
+  for_each_support<D>(g, first, cnt, aw, [&](int node, double, const double* grad) {
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const double uc = x[node * 3 + c];
+#pragma unroll
+      for (int a = 0; a < 2; ++a) G(c, a) += uc * grad[a];
+    }
+  });
+  Mat<T, 2> f_inc;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    f_inc.e[i] = T(G.e[i]);
+    f_inc.e[i].d[i] = 1.0;
+  }
+  f_inc(0, 0) += 1.0;
+  f_inc(1, 1) += 1.0;
+  Mat<T, 2> FnT;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) FnT.e[i] = T(pd[(PF<D>::F + i) * cap + p]);
+  const Mat<T, 2> F_new = matmul(f_inc, FnT);
+  double* out = A + static_cast<int64_t>(p) * 16;
+  if (!(value_of(det(F_new)) > 0.0)) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) out[i] = 0.0;
+    return;
+  }
+  const StressOut<T> su = neo_hookean_update<T, 2>(F_new, T(pc.lam), T(pc.mu));
+  const double V0 = pd[PF<D>::V0 * cap + p];
+#pragma unroll
+  for (int c = 0; c < 2; ++c)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) out[(c * 2 + b) * 4 + j] = V0 * su.sigma(c, b).d[j];
+}
+
+// colour-batched bin-centric assembly of the 3x3 u-p blocks:
+//   uu(c,d) = sum_f H_k[c][d][f] g^l_f,   up(c) = -V0 g^k_c w^l,
+//   pu(d)   = V0 w^k g^l_d,               pp    = V0 dt mob g^k . g^l
+template <int SHAPE, int PPL, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_up_assemble_bins(
+    GridC g, const double* __restrict__ pd, int64_t cap, const double* __restrict__ xs,
+    const int* __restrict__ bin_start, const uint8_t* __restrict__ bflag, const double* __restrict__ A,
+    const int* __restrict__ act_idx, const unsigned* __restrict__ row_mask, const int* __restrict__ row_nzb,
+    double* __restrict__ vals, int64_t row_len, double dtmob, int c0, int c1, int nb0, int nb1) {
+  constexpr int D = 2, F = 3, DD = 4, D3 = 8, NK = 9;
+  __shared__ double W1s[WARPS][2][3], DW1s[WARPS][2][3];
+  __shared__ double Gs[WARPS][NK][3];
+  __shared__ double Hs[WARPS][NK * D3];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nbins = nb0 * nb1;
+  for (int bi = blockIdx.x * WARPS + warp; bi < nbins; bi += gridDim.x * WARPS) {
+    const int bidx[2] = {3 * (bi / nb1) + c0, 3 * (bi % nb1) + c1};
+    const int b = bidx[0] * g.stride[0] + bidx[1];
+    const int fl = bflag[b];
+    if (!(fl & 0x80)) continue;
+    const int cn[2] = {2 + (fl & 1), 2 + ((fl >> 1) & 1)};
+    const int nk = cn[0] * cn[1];
+    const int npairs = nk * nk;
+    const int p0 = bin_start[b], p1 = bin_start[b + 1];
+    for (int q0 = 0; q0 < npairs; q0 += 32 * PPL) {
+      double acc[PPL][9];
+#pragma unroll
+      for (int t = 0; t < PPL; ++t)
+#pragma unroll
+        for (int e = 0; e < 9; ++e) acc[t][e] = 0.0;
+      for (int p = p0; p < p1; ++p) {
+        if (lane < 6) {
+          const int a = lane / 3, i = lane % 3;
+          double w = 0.0, dw = 0.0;
+          if (i < cn[a]) {
+            const WeightValue wv = weight_1d<SHAPE>(xs[a * cap + p] - node_coord(g, a, bidx[a] + i),
+                                                    pd[(PF<D>::lp + a) * cap + p], g.h);
+            w = wv.w;
+            dw = wv.dw;
+          }
+          W1s[warp][a][i] = w;
+          DW1s[warp][a][i] = dw;
+        }
+        __syncwarp();
+        if (lane < nk) {
+          const int li0 = lane / cn[1], li1 = lane % cn[1];
+          const double w[2] = {W1s[warp][0][li0], W1s[warp][1][li1]};
+          const double dw[2] = {DW1s[warp][0][li0], DW1s[warp][1][li1]};
+          double W, gk[3];
+          tensor_weight<D>(w, dw, W, gk);
+          Gs[warp][lane][0] = gk[0];
+          Gs[warp][lane][1] = gk[1];
+          Gs[warp][lane][2] = W;
+        }
+        __syncwarp();
+        const double* Ap = A + static_cast<int64_t>(p) * 16;
+        for (int e = lane; e < nk * D3; e += 32) {
+          const int k = e / D3, cdf = e - k * D3, c = cdf / DD, df = cdf - c * DD;
+          Hs[warp][e] = Gs[warp][k][0] * __ldg(Ap + (c * 2 + 0) * DD + df) +
+                        Gs[warp][k][1] * __ldg(Ap + (c * 2 + 1) * DD + df);
+        }
+        __syncwarp();
+        const double V0 = pd[PF<D>::V0 * cap + p];
+#pragma unroll
+        for (int t = 0; t < PPL; ++t) {
+          const int q = q0 + lane + 32 * t;
+          if (q < npairs) {
+            const int k = q / nk, l = q - k * nk;
+            const double* Hk = &Hs[warp][k * D3];
+            const double gl0 = Gs[warp][l][0], gl1 = Gs[warp][l][1], wl = Gs[warp][l][2];
+            const double gk0 = Gs[warp][k][0], gk1 = Gs[warp][k][1], wk = Gs[warp][k][2];
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+#pragma unroll
+              for (int d = 0; d < 2; ++d) acc[t][c * 3 + d] += Hk[(c * 2 + d) * 2] * gl0 + Hk[(c * 2 + d) * 2 + 1] * gl1;
+            acc[t][2] += -V0 * gk0 * wl;
+            acc[t][5] += -V0 * gk1 * wl;
+            acc[t][6] += V0 * wk * gl0;
+            acc[t][7] += V0 * wk * gl1;
+            acc[t][8] += V0 * dtmob * (gk0 * gl0 + gk1 * gl1);
+          }
+        }
+        __syncwarp();
+      }
+#pragma unroll
+      for (int t = 0; t < PPL; ++t) {
+        const int q = q0 + lane + 32 * t;
+        if (q >= npairs) continue;
+        const int k = q / nk, l = q - k * nk;
+        const int lk0 = k / cn[1], lk1 = k % cn[1], ll0 = l / cn[1], ll1 = l % cn[1];
+        const int node = (bidx[0] + lk0) * g.stride[0] + bidx[1] + lk1;
+        const int sl = (ll0 - lk0 + 2) * 5 + (ll1 - lk1 + 2);
+        const int row = act_idx[node];
+        if (row < 0) continue;
+        const unsigned* m = row_mask + static_cast<int64_t>(row) * 4;
+        const int pos = mask_pos(m, sl);
+        const int cp = cpad(row_nzb[row], F);
+        double* rv = vals + static_cast<int64_t>(row) * row_len + pos * F;
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int d = 0; d < 3; ++d) rv[c * cp + d] += acc[t][c * 3 + d];
+      }
+    }
+  }
+}
+
+// commit (src/porous.cpp:139-151): F, V, sigma, accumulated vertical displacement
+template <int SHAPE>
+__global__ void k_up_commit(GridC g, double* __restrict__ pd, int64_t cap, int P, const double* __restrict__ xs,
+                            const int* __restrict__ key, const int* __restrict__ sup, const double* __restrict__ x,
+                            PoroC pc, double* __restrict__ uty) {
+  constexpr int D = 2;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  int first[3], cnt[3];
+  AxisW aw[3];
+  particle_weights<D, SHAPE>(g, pd, cap, xs, p, key[p], sup[p], first, cnt, aw);
+  Mat<double, 2> G = Mat<double, 2>::zero();
+  double duy = 0.0;
+  for_each_support<D>(g, first, cnt, aw, [&](int node, double W, const double* grad) {
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const double uv = x[node * 3 + c];
+      if (c == 1) duy += W * uv;
+#pragma unroll
+      for (int a = 0; a < 2; ++a) G(c, a) += uv * grad[a];
+    }
+  });
+  Mat<double, 2> f_inc = G;
+  f_inc(0, 0) += 1.0;
+  f_inc(1, 1) += 1.0;
+  Mat<double, 2> Fn;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) Fn.e[i] = pd[(PF<D>::F + i) * cap + p];
+  const Mat<double, 2> F = matmul(f_inc, Fn);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) pd[(PF<D>::F + i) * cap + p] = F.e[i];
+  pd[PF<D>::V * cap + p] = det(F) * pd[PF<D>::V0 * cap + p];
+  const StressOut<double> su = neo_hookean_update<double, 2>(F, pc.lam, pc.mu);
+#pragma unroll
+  for (int i = 0; i < 9; ++i) pd[(PF<D>::sigma + i) * cap + p] = su.sigma.e[i];
+  uty[p] += duy;
+}
+
+// dst[n] field f of a grid vector (only where free), other entries untouched
+__global__ void k_copy_field(int N, int F, int f, const uint8_t* __restrict__ freem, const double* __restrict__ src,
+                             double* __restrict__ dst) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n < N && freem[static_cast<int64_t>(n) * F + f]) dst[static_cast<int64_t>(n) * F + f] = src[static_cast<int64_t>(n) * F + f];
+}
+
+// per-particle accumulator in ORIGINAL order
+__global__ void k_gather_orig(const double* __restrict__ v, const int* __restrict__ orig, int n, double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[orig[i]] = v[i];
 }
 
 // -------------------------------------------------- parity taps / export --

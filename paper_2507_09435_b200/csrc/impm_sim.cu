@@ -205,6 +205,12 @@ struct Sim {
   DevStatus* h_st = nullptr;  // pinned mirror
   double* h_sc = nullptr;
 
+  // coupled u-p mode (CoupledSim, porous.hpp:48-125)
+  bool coupled = false;
+  PoroC pc{};
+  double up_dt = 0.0, up_time = 0.0, up_rscale = 0.0;
+  DBuf<double> uty;  // accumulated vertical displacement per particle (sorted order)
+
   // controller state (mpm_solver.hpp:466-477)
   bool step_built = false;
   bool have_prev = false;
@@ -232,6 +238,17 @@ struct Sim {
     }
   }
 
+  template <class Fn>
+  void dispatch_df(Fn&& fn) {
+    switch (D * 10 + F) {
+      case 11: fn(IC<1>{}, IC<1>{}); break;
+      case 22: fn(IC<2>{}, IC<2>{}); break;
+      case 33: fn(IC<3>{}, IC<3>{}); break;
+      case 23: fn(IC<2>{}, IC<3>{}); break;
+      default: throw SimError(IMPM_ERR_CONFIG, "unsupported dimension/field combination");
+    }
+  }
+
   MatParams matp() const {
     MatParams m;
     m.kind = mat.kind;
@@ -242,10 +259,23 @@ struct Sim {
     return m;
   }
 
-  Sim(const impm_grid* gr, const impm_material* m, const impm_options* o, int dev) {
+  Sim(const impm_grid* gr, const impm_material* m, const impm_options* o, int dev, const impm_poro* poro = nullptr) {
     D = gr->dim;
     if (D < 1 || D > 3) throw SimError(IMPM_ERR_CONFIG, "grid dimension must be 1, 2 or 3");
     F = D;
+    if (poro) {
+      if (D != 2) throw SimError(IMPM_ERR_CONFIG, "coupled u-p is 2D (porous.hpp:48)");
+      if (!(poro->k > 0.0)) throw SimError(IMPM_ERR_CONFIG, "permeability must be positive");  // porous.hpp:32-37
+      if (!(poro->mu_f > 0.0)) throw SimError(IMPM_ERR_CONFIG, "fluid viscosity must be positive");
+      if (!(poro->mu > 0.0) || !(poro->lambda + 2.0 * poro->mu > 0.0))
+        throw SimError(IMPM_ERR_CONFIG, "solid moduli must give a positive constrained modulus");
+      coupled = true;
+      F = 3;
+      pc.lam = poro->lambda;
+      pc.mu = poro->mu;
+      pc.mob = poro->k / poro->mu_f;
+      pc.rho_f = poro->rho_f;
+    }
     device = dev;
     CK(cudaSetDevice(device));
     int N = 1;
@@ -261,7 +291,7 @@ struct Sim {
     g.h = gr->h;
     g.N = N;
     if (!(g.h > 0.0)) throw SimError(IMPM_ERR_CONFIG, "grid spacing must be positive");
-    set_material(m);
+    if (!coupled) set_material(m);
     set_options(o);
     CK(cudaStreamCreateWithFlags(&own_stream, cudaStreamNonBlocking));
     s = own_stream;
@@ -301,7 +331,7 @@ struct Sim {
     if (!(opt.abs_floor >= 0.0)) opt.abs_floor = 1e-14;
     if (!(opt.krylov_rtol > 0.0)) opt.krylov_rtol = 1e-12;
     shape = opt.shape == IMPM_SHAPE_BSPLINE2 ? 2 : 1;
-    if (opt.total_lagrangian && mat.kind == kHenckyJ2)  // mpm_solver.hpp:66-67
+    if (!coupled && opt.total_lagrangian && mat.kind == kHenckyJ2)  // mpm_solver.hpp:66-67
       throw SimError(IMPM_ERR_CONFIG, "total-Lagrangian stepping supports elastic materials only");
     prof.on = opt.profile != 0;
   }
@@ -344,7 +374,9 @@ struct Sim {
     sup.ensure(cap);
     rank.ensure(cap);
     perm.ensure(cap);
-    Pst.ensure(cap * D * D);
+    Pst.ensure(cap * std::max(D * D, 8));
+    uty.ensure(cap);
+    CK(cudaMemsetAsync(uty.p, 0, sizeof(double) * cap, s));
     Atan.ensure(cap * D * D * D * D);
     DBuf<double> staging;
     staging.ensure(std::max<int64_t>(1, n * (stride / 8)));
@@ -401,7 +433,7 @@ struct Sim {
   }
 
   void begin_step() {
-    if (opt.total_lagrangian && step_built) return;  // mpm_solver.hpp:94
+    if ((opt.total_lagrangian || coupled) && step_built) return;  // mpm_solver.hpp:94, porous.cpp:92
     const int N = g.N;
     reset_status();
     bin_count.ensure(N + 1);
@@ -424,7 +456,8 @@ struct Sim {
       dispatch([&](auto Dc, auto Sc) {
         constexpr int DD = decltype(Dc)::value, SH = decltype(Sc)::value;
         if (P > 0) {
-          k_support<DD, SH><<<blocks_for(P), kThreads, 0, s>>>(pd.p, cap, P, g, orig.p, key.p, sup.p, xs.p, st.p); ++g_launches;
+          k_support<DD, SH><<<blocks_for(P), kThreads, 0, s>>>(pd.p, cap, P, g, orig.p, key.p, sup.p, xs.p, st.p,
+                                                                coupled ? 1 : 0); ++g_launches;
           CKL();
         }
       });
@@ -458,6 +491,8 @@ struct Sim {
       k_gather_fields<<<grid, kThreads, 0, s>>>(pd.p, pd_tmp.p, cap, perm.p, P); ++g_launches;
       CKL();
       k_gather_int<<<blocks_for(P), kThreads, 0, s>>>(orig.p, orig_tmp.p, perm.p, P); ++g_launches;
+      k_gather_fields<<<dim3(blocks_for(P), 1), kThreads, 0, s>>>(uty.p, xs.p, cap, perm.p, P); ++g_launches;
+      CK(cudaMemcpyAsync(uty.p, xs.p, sizeof(double) * P, cudaMemcpyDeviceToDevice, s));
       CKL();
       std::swap(pd.p, pd_tmp.p);
       std::swap(pd.cap, pd_tmp.cap);
@@ -465,7 +500,8 @@ struct Sim {
       std::swap(orig.cap, orig_tmp.cap);
       dispatch([&](auto Dc, auto Sc) {
         constexpr int DD = decltype(Dc)::value, SH = decltype(Sc)::value;
-        k_support<DD, SH><<<blocks_for(P), kThreads, 0, s>>>(pd.p, cap, P, g, orig.p, key.p, sup.p, xs.p, st.p); ++g_launches;
+        k_support<DD, SH><<<blocks_for(P), kThreads, 0, s>>>(pd.p, cap, P, g, orig.p, key.p, sup.p, xs.p, st.p,
+                                                                coupled ? 1 : 0); ++g_launches;
         CKL();
       });
     }
@@ -477,8 +513,14 @@ struct Sim {
           k_bext<DD><<<blocks_for(P), kThreads, 0, s>>>(pd.p, cap, P, gravity[0], gravity[1], gravity[2], bext.p, st.p); ++g_launches;
           CKL();
         }
-        k_node_mass<DD, DD, SH><<<blocks_for(N), kThreads, 0, s>>>(g, pd.p, cap, xs.p, bin_start.p, sup.p, fixed.p,
-                                                                    st.p, mass.p, act_flag.p, free_flag.p); ++g_launches;
+        if (coupled) {
+          if constexpr (DD == 2)
+            k_node_mass<2, 3, SH><<<blocks_for(N), kThreads, 0, s>>>(g, pd.p, cap, xs.p, bin_start.p, sup.p, fixed.p,
+                                                                      st.p, mass.p, act_flag.p, free_flag.p);
+        } else {
+          k_node_mass<DD, DD, SH><<<blocks_for(N), kThreads, 0, s>>>(g, pd.p, cap, xs.p, bin_start.p, sup.p, fixed.p,
+                                                                      st.p, mass.p, act_flag.p, free_flag.p);
+        } ++g_launches;
         CKL();
       });
     }
@@ -525,6 +567,7 @@ struct Sim {
       CK(cudaMemcpyAsync(&h_nzb_total, nzb_total.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     }
     CK(cudaMemsetAsync(u.p, 0, sizeof(double) * NF(), s));
+    if (coupled) CK(cudaMemsetAsync(prev.p, 0, sizeof(double) * NF(), s));  // p_nodes_ = 0 (porous.cpp:70)
     matrix_valid = false;
     step_built = true;
     sync();
@@ -534,6 +577,7 @@ struct Sim {
   // r = r(u) in grid layout; returns ||r||; throws DomainError on det <= 0
   double residual_dev(const double* ud, double load_scale, double* rd) {
     clear_errors_only();
+    if (coupled) return residual_up(ud, load_scale, rd);
     const MatParams mp = matp();
     dispatch([&](auto Dc, auto Sc) {
       constexpr int DD = decltype(Dc)::value, SH = decltype(Sc)::value;
@@ -562,6 +606,7 @@ struct Sim {
 
   // ------------------------------------------------------ Jacobian (K6)
   void jacobian_dev(const double* ud) {
+    if (coupled) return jacobian_up(ud, up_dt);
     const MatParams mp = matp();
     dispatch([&](auto Dc, auto Sc) {
       constexpr int DD = decltype(Dc)::value, SH = decltype(Sc)::value;
@@ -603,16 +648,13 @@ struct Sim {
   // ------------------------------------------------------- Krylov (K7)
   void spmv(const double* x, double* y, const double* dotv, double* parts) {
     Prof::Scope ps(&prof, kcSpmv);
-    auto launch = [&](auto Dc) {
-      constexpr int DD = decltype(Dc)::value;
+    dispatch_df([&](auto Dc, auto Fc) {
+      constexpr int DD = decltype(Dc)::value, FE = decltype(Fc)::value;
       constexpr int W = 8;
-      k_spmv<DD, DD, W><<<kRedBlocks, W * 32, 0, s>>>(g, act_list.p, n_act, vals.p, row_len, row_slots.p,
+      k_spmv<DD, FE, W><<<kRedBlocks, W * 32, 0, s>>>(g, act_list.p, n_act, vals.p, row_len, row_slots.p,
                                                       row_nzb.p, x, freem.p, y, dotv, parts, dflag.p); ++g_launches;
       CKL();
-    };
-    if (D == 1) launch(IC<1>{});
-    else if (D == 2) launch(IC<2>{});
-    else launch(IC<3>{});
+    });
   }
 
   template <int FF>
@@ -684,10 +726,26 @@ struct Sim {
     k_precond<FF><<<blocks_for(g.N), kThreads, 0, s>>>(g.N, act_idx.p, dinv.p, rin, z); ++g_launches;
     CKL();
   }
-  template <int FF>
-  int bicgstab_solve(const double* b, double* x) {
+  // z = M^-1 v: MG V-cycle or block Jacobi
+  template <int DD, int FE>
+  const double* apply_precond(bool mgp, const double* v, double* z) {
+    if (mgp) {
+      vcycle<DD, FE>(0, v);
+      CK(cudaMemcpyAsync(z, mg[0]->x, sizeof(double) * NF(), cudaMemcpyDeviceToDevice, s));
+      return z;
+    }
+    precond<FE>(v, z);
+    return z;
+  }
+
+  template <int DD, int FE>
+  int bicgstab_solve(const double* b, double* x, bool mgp) {
+    if (mgp) mg_setup<DD, FE>();
     CK(cudaMemsetAsync(dflag.p, 0, sizeof(int), s));
-    const int max_it = opt.krylov_max_iter > 0 ? opt.krylov_max_iter : std::min(20000, std::max(100, 10 * n_dofs));
+    // the u-p saddle point (cond ~1e15) needs far more than n iterations
+    const int max_it = opt.krylov_max_iter > 0 ? opt.krylov_max_iter
+                       : coupled              ? std::max(4000, 50 * n_dofs)
+                                              : std::min(20000, std::max(100, 10 * n_dofs));
     CK(cudaMemsetAsync(x, 0, sizeof(double) * NF(), s));
     CK(cudaMemcpyAsync(kr.p, b, sizeof(double) * NF(), cudaMemcpyDeviceToDevice, s));
     CK(cudaMemcpyAsync(khat.p, b, sizeof(double) * NF(), cudaMemcpyDeviceToDevice, s));
@@ -703,7 +761,7 @@ struct Sim {
       const double beta = (rho_new / rho) * (alpha / omega);
       // p = r + beta (p - omega v)
       axpbypcz(1.0, kr.p, beta, kp.p, -beta * omega, kv.p);
-      precond<FF>(kp.p, kz.p);  // phat in kz
+      apply_precond<DD, FE>(mgp, kp.p, kz.p);  // phat in kz
       spmv(kz.p, kv.p, nullptr, nullptr);
       const double rv = dot(khat.p, kv.p);
       alpha = rho_new / rv;
@@ -713,7 +771,7 @@ struct Sim {
       axpbypcz(alpha, kz.p, 1.0, x);  // x += alpha phat
       const double ss = dot(ks.p, ks.p);
       if (ss <= tol2) return it;
-      precond<FF>(ks.p, tmp1.p);  // shat
+      apply_precond<DD, FE>(mgp, ks.p, tmp1.p);  // shat
       spmv(tmp1.p, kt.p, nullptr, nullptr);
       const double ts = dot(kt.p, ks.p), tt = dot(kt.p, kt.p);
       omega = ts / tt;
@@ -731,20 +789,20 @@ struct Sim {
 
 
   // ------------------------------------------------ multigrid (K7 precond)
-  template <int DD, int MODE>
+  template <int DD, int FE, int MODE>
   void level_spmv(MgLevel& L, const double* x, double* y, const double* b, double omega, const double* dotv,
                   double* parts) {
     constexpr int W = 8;
-    k_spmv<DD, DD, W, MODE><<<kRedBlocks, W * 32, 0, s>>>(L.g, L.act_list, L.n_act, L.vals, L.row_len, L.row_slots,
+    k_spmv<DD, FE, W, MODE><<<kRedBlocks, W * 32, 0, s>>>(L.g, L.act_list, L.n_act, L.vals, L.row_len, L.row_slots,
                                                           L.row_nzb, x, L.freem, y, dotv, parts, dflag.p, b, L.dinv,
                                                           omega); ++g_launches;
     CKL();
   }
 
-  template <int DD>
+  template <int DD, int FE>
   void mg_setup() {
     constexpr int S = ipow_c(5, DD);
-    constexpr int FF = DD * DD;
+    constexpr int FF = FE * FE;
     // level objects (and their device buffers) persist across setups; only
     // growth reallocates
     std::vector<std::unique_ptr<MgLevel>> pool;
@@ -770,7 +828,7 @@ struct Sim {
     mg_stored_blocks = 0;
     const int coarsest_max = 200;  // unknowns solved densely at the bottom
     mg_nzb.ensure(1);
-    while (static_cast<int64_t>(mg.back()->n_act) * DD > coarsest_max && mg.size() < 16) {
+    while (static_cast<int64_t>(mg.back()->n_act) * FE > coarsest_max && mg.size() < 16) {
       MgLevel& F0 = *mg.back();
       auto C = take();
       GridC gc{};
@@ -801,13 +859,13 @@ struct Sim {
       CK(cudaMemcpyAsync(&na, C->act_scan_b.p + N, sizeof(int), cudaMemcpyDeviceToHost, s));
       sync();
       C->n_act = na;
-      C->row_len = row_len_for(S, DD);
+      C->row_len = row_len_for(S, FE);
       C->vals_b.ensure(std::max<int64_t>(1, static_cast<int64_t>(na) * C->row_len));
       C->row_slots_b.ensure(std::max<int64_t>(1, static_cast<int64_t>(na) * S));
       C->row_nzb_b.ensure(std::max(1, na));
       C->dinv_b.ensure(std::max<int64_t>(1, static_cast<int64_t>(na) * FF));
-      C->freem_b.ensure(static_cast<int64_t>(N) * DD);
-      CK(cudaMemsetAsync(C->freem_b.p, 0, static_cast<int64_t>(N) * DD, s));
+      C->freem_b.ensure(static_cast<int64_t>(N) * FE);
+      CK(cudaMemsetAsync(C->freem_b.p, 0, static_cast<int64_t>(N) * FE, s));
       C->act_idx = C->act_idx_b.p;
       C->act_list = C->act_list_b.p;
       C->row_nzb = C->row_nzb_b.p;
@@ -822,13 +880,13 @@ struct Sim {
         mg_T.ensure(std::max<int64_t>(1, static_cast<int64_t>(F0.n_act) * NT * FF));
         constexpr int W = 8;
         if (F0.n_act > 0) {
-          k_galerkin_ap<DD, DD, W><<<std::min<unsigned>(blocks_for(F0.n_act, W), 148 * 8), W * 32, 0, s>>>(
+          k_galerkin_ap<DD, FE, W><<<std::min<unsigned>(blocks_for(F0.n_act, W), 148 * 8), W * 32, 0, s>>>(
               F0.g, gc, F0.n_act, F0.act_list, F0.vals, F0.row_len, F0.row_slots, F0.row_nzb, F0.freem, mg_T.p);
           ++g_launches;
           CKL();
         }
         if (na > 0) {
-          k_galerkin_ptap<DD, DD, W><<<std::min<unsigned>(blocks_for(na, W), 148 * 8), W * 32, 0, s>>>(
+          k_galerkin_ptap<DD, FE, W><<<std::min<unsigned>(blocks_for(na, W), 148 * 8), W * 32, 0, s>>>(
               F0.g, gc, F0.act_idx, F0.freem, mg_T.p, C->act_list, na, C->vals_b.p, C->row_len, C->row_slots_b.p,
               C->row_nzb_b.p, C->freem_b.p, C->dinv_b.p, mg_nzb.p);
           ++g_launches;
@@ -840,7 +898,7 @@ struct Sim {
     // level vectors (zero outside active rows / free components)
     for (auto& Lp : mg) {
       MgLevel& L = *Lp;
-      const int64_t n = static_cast<int64_t>(L.g.N) * DD;
+      const int64_t n = static_cast<int64_t>(L.g.N) * FE;
       L.xa.ensure(n);
       L.xb.ensure(n);
       L.r.ensure(n);
@@ -858,12 +916,12 @@ struct Sim {
       Prof::Scope psp(&prof, kcMgPower);
       for (size_t l = 0; l + 1 < mg.size(); ++l) {
         MgLevel& L = *mg[l];
-        const int64_t n = static_cast<int64_t>(L.g.N) * DD;
+        const int64_t n = static_cast<int64_t>(L.g.N) * FE;
         k_fill_free<<<blocks_for(n), kThreads, 0, s>>>(n, L.freem, L.bvec.p); ++g_launches;
         CKL();
         for (int it = 0; it < 8; ++it) {
-          level_spmv<DD, kSpmvY>(L, L.bvec.p, L.r.p, nullptr, 0.0, nullptr, nullptr);
-          k_precond<DD><<<blocks_for(L.g.N), kThreads, 0, s>>>(L.g.N, L.act_idx, L.dinv, L.r.p, L.t); ++g_launches;
+          level_spmv<DD, FE, kSpmvY>(L, L.bvec.p, L.r.p, nullptr, 0.0, nullptr, nullptr);
+          k_precond<FE><<<blocks_for(L.g.N), kThreads, 0, s>>>(L.g.N, L.act_idx, L.dinv, L.r.p, L.t); ++g_launches;
           k_dot2<<<kRedBlocks, kThreads, 0, s>>>(n, L.t, L.t, L.bvec.p, L.bvec.p, partials.p); ++g_launches;
           k_finalize_sum<2><<<1, 1024, 0, s>>>(partials.p, kRedBlocks, sums.p); ++g_launches;
           k_power_step<<<kRedBlocks, kThreads, 0, s>>>(n, sums.p, L.t, L.bvec.p, mg_lam.p + l); ++g_launches;
@@ -878,7 +936,7 @@ struct Sim {
       sync();
       for (size_t l = 0; l + 1 < mg.size(); ++l) {
         MgLevel& L = *mg[l];
-        const int64_t n = static_cast<int64_t>(L.g.N) * DD;
+        const int64_t n = static_cast<int64_t>(L.g.N) * FE;
         L.omega = 4.0 / (3.0 * 1.1 * (lam[l] > 0 ? lam[l] : 1.0));
         CK(cudaMemsetAsync(L.t, 0, sizeof(double) * n, s));
         CK(cudaMemsetAsync(L.bvec.p, 0, sizeof(double) * n, s));
@@ -888,11 +946,11 @@ struct Sim {
     Prof::Scope psc(&prof, kcMgCoarsest);
     // coarsest: dense inverse over (active row, component), identity on non-free
     MgLevel& B = *mg.back();
-    const int nb = B.n_act, n = nb * DD;
+    const int nb = B.n_act, n = nb * FE;
     mg_dense_n = n;
     if (n > 0) {
       std::vector<int> slots_nzb(nb);
-      std::vector<uint8_t> slots(static_cast<size_t>(nb) * S), fm(static_cast<size_t>(B.g.N) * DD);
+      std::vector<uint8_t> slots(static_cast<size_t>(nb) * S), fm(static_cast<size_t>(B.g.N) * FE);
       std::vector<int> alist(nb), aidx(B.g.N);
       std::vector<double> vals_h(static_cast<size_t>(nb) * B.row_len), dense(static_cast<size_t>(n) * n, 0.0);
       CK(cudaMemcpyAsync(slots_nzb.data(), B.row_nzb, sizeof(int) * nb, cudaMemcpyDeviceToHost, s));
@@ -922,14 +980,14 @@ struct Sim {
           if (!ok) continue;
           const int crow = aidx[nbn];
           if (crow < 0) continue;
-          for (int c = 0; c < DD; ++c)
-            for (int d = 0; d < DD; ++d)
-              if (fm[static_cast<size_t>(k) * DD + c] && fm[static_cast<size_t>(nbn) * DD + d])
-                dense[static_cast<size_t>(rrow * DD + c) * n + crow * DD + d] =
-                    vals_h[static_cast<size_t>(rrow) * B.row_len + c * cpad(slots_nzb[rrow], DD) + pos * DD + d];
+          for (int c = 0; c < FE; ++c)
+            for (int d = 0; d < FE; ++d)
+              if (fm[static_cast<size_t>(k) * FE + c] && fm[static_cast<size_t>(nbn) * FE + d])
+                dense[static_cast<size_t>(rrow * FE + c) * n + crow * FE + d] =
+                    vals_h[static_cast<size_t>(rrow) * B.row_len + c * cpad(slots_nzb[rrow], FE) + pos * FE + d];
         }
-        for (int c = 0; c < DD; ++c)
-          if (!fm[static_cast<size_t>(k) * DD + c]) dense[static_cast<size_t>(rrow * DD + c) * n + rrow * DD + c] = 1.0;
+        for (int c = 0; c < FE; ++c)
+          if (!fm[static_cast<size_t>(k) * FE + c]) dense[static_cast<size_t>(rrow * FE + c) * n + rrow * FE + c] = 1.0;
       }
       std::vector<double> inv = invert_dense(dense, n);
       mg_dense.ensure(static_cast<size_t>(n) * n);
@@ -971,43 +1029,43 @@ struct Sim {
   }
 
   // z = V-cycle(b) at level l; result in mg[l]->x
-  template <int DD>
+  template <int DD, int FE>
   void vcycle(size_t l, const double* b) {
     MgLevel& L = *mg[l];
     if (l + 1 == mg.size()) {
       if (mg_dense_n > 0) {
         k_dense_apply<<<std::min<unsigned>(blocks_for(mg_dense_n, 128), 148), 128, 0, s>>>(
-            mg_dense_n, DD, dflag.p, L.act_list, mg_dense.p, b, L.x); ++g_launches;
+            mg_dense_n, FE, dflag.p, L.act_list, mg_dense.p, b, L.x); ++g_launches;
         CKL();
       }
       return;
     }
     const int nu = opt.mg_smooth > 0 ? opt.mg_smooth : 1;
     // pre-smoothing from x = 0
-    k_jacobi0<DD><<<kRedBlocks, kThreads, 0, s>>>(L.n_act, dflag.p, L.act_list, L.dinv, L.freem, L.omega, b, L.x);
+    k_jacobi0<FE><<<kRedBlocks, kThreads, 0, s>>>(L.n_act, dflag.p, L.act_list, L.dinv, L.freem, L.omega, b, L.x);
     ++g_launches;
     CKL();
     for (int i = 1; i < nu; ++i) {
-      level_spmv<DD, kSpmvJacobi>(L, L.x, L.t, b, L.omega, nullptr, nullptr);
+      level_spmv<DD, FE, kSpmvJacobi>(L, L.x, L.t, b, L.omega, nullptr, nullptr);
       std::swap(L.x, L.t);
     }
-    level_spmv<DD, kSpmvResid>(L, L.x, L.r.p, b, 0.0, nullptr, nullptr);
+    level_spmv<DD, FE, kSpmvResid>(L, L.x, L.r.p, b, 0.0, nullptr, nullptr);
     MgLevel& C = *mg[l + 1];
-    k_restrict<DD, DD><<<blocks_for(C.g.N), kThreads, 0, s>>>(L.g, C.g, dflag.p, L.r.p, C.freem, C.bvec.p);
+    k_restrict<DD, FE><<<blocks_for(C.g.N), kThreads, 0, s>>>(L.g, C.g, dflag.p, L.r.p, C.freem, C.bvec.p);
     ++g_launches;
     CKL();
-    vcycle<DD>(l + 1, C.bvec.p);
-    k_prolong_add<DD, DD><<<blocks_for(L.g.N), kThreads, 0, s>>>(L.g, C.g, dflag.p, C.x, L.freem, L.x);
+    vcycle<DD, FE>(l + 1, C.bvec.p);
+    k_prolong_add<DD, FE><<<blocks_for(L.g.N), kThreads, 0, s>>>(L.g, C.g, dflag.p, C.x, L.freem, L.x);
     ++g_launches;
     CKL();
     for (int i = 0; i < nu; ++i) {
-      level_spmv<DD, kSpmvJacobi>(L, L.x, L.t, b, L.omega, nullptr, nullptr);
+      level_spmv<DD, FE, kSpmvJacobi>(L, L.x, L.t, b, L.omega, nullptr, nullptr);
       std::swap(L.x, L.t);
     }
   }
 
   // MG-preconditioned CG (device-resident scalars, batched host checks)
-  template <int DD>
+  template <int DD, int FE>
   int cg_mg_solve(const double* b, double* x) {
     const int N = g.N;
     const int64_t n = NF();
@@ -1015,7 +1073,7 @@ struct Sim {
     const double rtol2 = opt.krylov_rtol * opt.krylov_rtol;
     {
       Prof::Scope ps(&prof, kcMgSetup);
-      mg_setup<DD>();
+      mg_setup<DD, FE>();
     }
     CK(cudaMemsetAsync(dflag.p, 0, sizeof(int), s));
     double* partA = partials.p;
@@ -1024,7 +1082,7 @@ struct Sim {
     CK(cudaMemcpyAsync(kr.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
     {
       Prof::Scope ps(&prof, kcVcycle);
-      vcycle<DD>(0, kr.p);
+      vcycle<DD, FE>(0, kr.p);
     }
     const double* z = mg[0]->x;
     CK(cudaMemcpyAsync(kp.p, z, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
@@ -1043,18 +1101,18 @@ struct Sim {
         spmv(kp.p, kq.p, kp.p, partA);
         {
           Prof::Scope ps(&prof, kcKrylov);
-          k_cg_update_mg<DD><<<kRedBlocks, kThreads, 0, s>>>(N, act_idx.p, sc.p, dflag.p, par, partA, kRedBlocks, x,
+          k_cg_update_mg<FE><<<kRedBlocks, kThreads, 0, s>>>(N, act_idx.p, sc.p, dflag.p, par, partA, kRedBlocks, x,
                                                              kr.p, kp.p, kq.p, partB + kRedBlocks); ++g_launches;
           CKL();
         }
         {
           Prof::Scope ps(&prof, kcVcycle);
-          vcycle<DD>(0, kr.p);
+          vcycle<DD, FE>(0, kr.p);
         }
         z = mg[0]->x;
         Prof::Scope ps(&prof, kcKrylov);
         k_dot1<<<kRedBlocks, kThreads, 0, s>>>(n, dflag.p, kr.p, z, partB); ++g_launches;
-        k_cg_p2<DD><<<kRedBlocks, kThreads, 0, s>>>(N, act_idx.p, sc.p, dflag.p, par, it, partB, kRedBlocks, rtol2,
+        k_cg_p2<FE><<<kRedBlocks, kThreads, 0, s>>>(N, act_idx.p, sc.p, dflag.p, par, it, partB, kRedBlocks, rtol2,
                                                     max_it, z, kp.p); ++g_launches;
         CKL();
       }
@@ -1074,21 +1132,124 @@ struct Sim {
     return iters;
   }
 
-  // delta = J^-1 rhs (grid layout); returns Krylov iterations
-  int solve_dev(const double* rhs, double* x) {
-    auto run = [&](auto Fc) -> int {
-      constexpr int FF = decltype(Fc)::value;
-      if (opt.krylov != IMPM_KRYLOV_BICGSTAB) {
-        const int it = opt.precond == IMPM_PRECOND_MG ? cg_mg_solve<FF>(rhs, x) : cg_solve<FF>(rhs, x);
-        if (it >= 0) return it;
-        if (opt.krylov == IMPM_KRYLOV_CG) throw SimError(IMPM_ERR_LINEAR_SOLVER, "CG breakdown: J not SPD");
-        return -it - 1 + bicgstab_solve<FF>(rhs, x);
+
+  // GMRES(m), right-preconditioned (block Jacobi or MG), modified
+  // Gram-Schmidt on device vectors, Hessenberg/Givens on the host.
+  // Robust path for the nonsymmetric, badly scaled u-p saddle point.
+  DBuf<double> gm_V;
+  double dot_sync(const double* a, const double* b) {
+    k_dot2<<<kRedBlocks, kThreads, 0, s>>>(NF(), a, b, nullptr, nullptr, partials.p); ++g_launches;
+    k_finalize_sum<2><<<1, 1024, 0, s>>>(partials.p, kRedBlocks, sums.p); ++g_launches;
+    CKL();
+    double hh[2];
+    CK(cudaMemcpyAsync(hh, sums.p, sizeof(hh), cudaMemcpyDeviceToHost, s));
+    sync();
+    return hh[0];
+  }
+
+  template <int DD, int FE>
+  int gmres_solve(const double* b, double* x, bool mgp) {
+    const int64_t n = NF();
+    const int m = std::max(2, std::min(60, n_dofs));
+    const int max_it = opt.krylov_max_iter > 0 ? opt.krylov_max_iter : std::max(2000, 20 * n_dofs);
+    if (mgp) mg_setup<DD, FE>();
+    CK(cudaMemsetAsync(dflag.p, 0, sizeof(int), s));
+    gm_V.ensure(static_cast<size_t>(m + 1) * n);
+    CK(cudaMemsetAsync(x, 0, sizeof(double) * n, s));
+    const double bnorm = std::sqrt(dot_sync(b, b));
+    if (bnorm == 0.0) return 0;
+    const double tol = opt.krylov_rtol * bnorm;
+    std::vector<double> H(static_cast<size_t>(m + 1) * m), cs(m), sn(m), gv(m + 1), y(m);
+    int total = 0;
+    CK(cudaMemcpyAsync(kr.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));  // r = b (x = 0)
+    double beta = bnorm;
+    while (total < max_it) {
+      double* V0 = gm_V.p;
+      axpbypcz(1.0 / beta, kr.p, 0.0, V0);
+      std::fill(gv.begin(), gv.end(), 0.0);
+      gv[0] = beta;
+      int j = 0;
+      for (; j < m && total < max_it; ++j, ++total) {
+        double* Vj = gm_V.p + static_cast<size_t>(j) * n;
+        double* w = gm_V.p + static_cast<size_t>(j + 1) * n;
+        apply_precond<DD, FE>(mgp, Vj, kz.p);
+        spmv(kz.p, w, nullptr, nullptr);
+        for (int i = 0; i <= j; ++i) {
+          const double* Vi = gm_V.p + static_cast<size_t>(i) * n;
+          const double hij = dot_sync(w, Vi);
+          H[static_cast<size_t>(i) * m + j] = hij;
+          axpbypcz(-hij, Vi, 1.0, w);
+        }
+        const double hn = std::sqrt(dot_sync(w, w));
+        H[static_cast<size_t>(j + 1) * m + j] = hn;
+        if (hn > 0.0) axpbypcz(1.0 / hn, w, 0.0, w);
+        for (int i = 0; i < j; ++i) {  // apply previous rotations
+          const double a = H[static_cast<size_t>(i) * m + j], bb = H[static_cast<size_t>(i + 1) * m + j];
+          H[static_cast<size_t>(i) * m + j] = cs[i] * a + sn[i] * bb;
+          H[static_cast<size_t>(i + 1) * m + j] = -sn[i] * a + cs[i] * bb;
+        }
+        const double a = H[static_cast<size_t>(j) * m + j], bb = H[static_cast<size_t>(j + 1) * m + j];
+        const double rr = std::hypot(a, bb);
+        cs[j] = rr > 0 ? a / rr : 1.0;
+        sn[j] = rr > 0 ? bb / rr : 0.0;
+        H[static_cast<size_t>(j) * m + j] = rr;
+        H[static_cast<size_t>(j + 1) * m + j] = 0.0;
+        gv[j + 1] = -sn[j] * gv[j];
+        gv[j] = cs[j] * gv[j];
+        if (std::abs(gv[j + 1]) <= tol || hn == 0.0) {
+          ++j;
+          ++total;
+          break;
+        }
       }
-      return bicgstab_solve<FF>(rhs, x);
-    };
-    if (F == 1) return run(IC<1>{});
-    if (F == 2) return run(IC<2>{});
-    return run(IC<3>{});
+      // y = H^-1 g (upper triangular j x j); u = V y; x += M^-1 u
+      for (int i = j - 1; i >= 0; --i) {
+        double acc = gv[i];
+        for (int k2 = i + 1; k2 < j; ++k2) acc -= H[static_cast<size_t>(i) * m + k2] * y[k2];
+        y[i] = H[static_cast<size_t>(i) * m + i] != 0.0 ? acc / H[static_cast<size_t>(i) * m + i] : 0.0;
+      }
+      CK(cudaMemsetAsync(tmp1.p, 0, sizeof(double) * n, s));
+      for (int i = 0; i < j; ++i) axpbypcz(y[i], gm_V.p + static_cast<size_t>(i) * n, 1.0, tmp1.p);
+      apply_precond<DD, FE>(mgp, tmp1.p, kz.p);
+      axpbypcz(1.0, kz.p, 1.0, x);
+      // true residual
+      spmv(x, kq.p, nullptr, nullptr);
+      CK(cudaMemcpyAsync(kr.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+      axpbypcz(-1.0, kq.p, 1.0, kr.p);
+      beta = std::sqrt(dot_sync(kr.p, kr.p));
+      if (!(beta == beta)) throw SimError(IMPM_ERR_LINEAR_SOLVER, "GMRES breakdown: NaN residual");
+      if (beta <= tol) return total;
+    }
+    const double rel = beta / bnorm;
+    if (!(rel <= 1e-6)) throw SimError(IMPM_ERR_LINEAR_SOLVER, "GMRES did not converge: relative residual " +
+                                                                   std::to_string(rel));
+    return total;
+  }
+  // delta = J^-1 rhs (grid layout); returns Krylov iterations. Symmetric
+  // single-field J: CG (MG or block-Jacobi preconditioned), falling back to
+  // BiCGStab on breakdown; coupled u-p (nonsymmetric): BiCGStab.
+  int solve_dev(const double* rhs, double* x) {
+    int out = 0;
+    dispatch_df([&](auto Dc, auto Fc) {
+      constexpr int DD = decltype(Dc)::value, FE = decltype(Fc)::value;
+      const bool mgp = opt.precond == IMPM_PRECOND_MG && !coupled;  // u-p: block Jacobi (saddle point)
+      if (!coupled && opt.krylov != IMPM_KRYLOV_BICGSTAB) {
+        const int it = mgp ? cg_mg_solve<DD, FE>(rhs, x) : cg_solve<FE>(rhs, x);
+        if (it >= 0) {
+          out = it;
+          return;
+        }
+        if (opt.krylov == IMPM_KRYLOV_CG) throw SimError(IMPM_ERR_LINEAR_SOLVER, "CG breakdown: J not SPD");
+        out = -it - 1 + bicgstab_solve<DD, FE>(rhs, x, mgp);
+        return;
+      }
+      if (coupled || opt.krylov == IMPM_KRYLOV_GMRES) {
+        out = gmres_solve<DD, FE>(rhs, x, mgp);
+        return;
+      }
+      out = bicgstab_solve<DD, FE>(rhs, x, mgp);
+    });
+    return out;
   }
 
   // ------------------------------------------------------ Newton (a16/a17)
@@ -1108,9 +1269,9 @@ struct Sim {
     rowlen.ensure(std::max(n_dofs, 1) + 1);
     rowptr.ensure(std::max(n_dofs, 1) + 1);
     if (n_dofs == 0) return ref_nnz_cache = 0;
-    dispatch([&](auto Dc, auto) {
-      constexpr int DD = decltype(Dc)::value;
-      k_csr_count<DD, DD><<<blocks_for(n_dofs), kThreads, 0, s>>>(g, n_dofs, node_of.p, dof_of.p, rowlen.p); ++g_launches;
+    dispatch_df([&](auto Dc, auto Fc) {
+      constexpr int DD = decltype(Dc)::value, FE = decltype(Fc)::value;
+      k_csr_count<DD, FE><<<blocks_for(n_dofs), kThreads, 0, s>>>(g, n_dofs, node_of.p, dof_of.p, rowlen.p); ++g_launches;
       CKL();
     });
     int64_t tot = 0;
@@ -1251,6 +1412,140 @@ struct Sim {
     CKL();
   }
 
+
+  // ----------------------------------------------- coupled u-p (2D, F=3)
+  PoroC poro_c() const {
+    PoroC q = pc;
+    q.g0 = gravity[0];
+    q.g1 = gravity[1];
+    return q;
+  }
+
+  // CoupledSim::assemble<double> (porous.hpp:127-186); dt > 0 required
+  double residual_up(const double* xd, double dt, double* rd) {
+    if (!(dt > 0.0)) throw SimError(IMPM_ERR_CONFIG, "coupled step requires dt > 0");
+    const PoroC q = poro_c();
+    auto run = [&](auto Sc) {
+      constexpr int SH = decltype(Sc)::value;
+      if (P > 0) {
+        Prof::Scope ps(&prof, kcResP);
+        k_up_particles<SH><<<blocks_for(P), kThreads, 0, s>>>(g, pd.p, cap, P, xs.p, key.p, sup.p, orig.p, xd, q,
+                                                              Pst.p, st.p); ++g_launches;
+        CKL();
+      }
+      Prof::Scope ps(&prof, kcResN);
+      k_up_nodes<SH><<<kRedBlocks, kThreads, 0, s>>>(g, pd.p, cap, xs.p, bin_start.p, sup.p, Pst.p, bext.p,
+                                                     act_flag.p, freem.p, q, dt, rd, partials.p); ++g_launches;
+      k_finalize_sum<1><<<1, 1024, 0, s>>>(partials.p, kRedBlocks, &st.p->norm2); ++g_launches;
+      CKL();
+    };
+    if (shape == 2) run(IC<2>{});
+    else run(IC<1>{});
+    read_status();
+    prof.flush();
+    if (h_st->err_domain != INT_MAX)
+      throw SimError(IMPM_ERR_DOMAIN, "non-positive det(F) at particle " + std::to_string(h_st->err_domain));
+    return std::sqrt(h_st->norm2);
+  }
+
+  void jacobian_up(const double* xd, double dt) {
+    const PoroC q = poro_c();
+    auto run = [&](auto Sc) {
+      constexpr int SH = decltype(Sc)::value;
+      if (P > 0) {
+        Prof::Scope ps(&prof, kcTangent);
+        k_up_tangent<SH><<<blocks_for(P, 128), 128, 0, s>>>(g, pd.p, cap, P, xs.p, key.p, sup.p, xd, q, Atan.p);
+        ++g_launches;
+        CKL();
+      }
+      if (n_act > 0) {
+        Prof::Scope ps(&prof, kcAssemble);
+        k_zero_rows<<<blocks_for(static_cast<int64_t>(n_act) * 32), kThreads, 0, s>>>(n_act, 3, row_nzb.p, vals.p,
+                                                                                    row_len); ++g_launches;
+        constexpr int W = 4;
+        for (int col = 0; col < 9; ++col) {
+          const int c0 = col / 3, c1 = col % 3;
+          const int nb0 = std::max(0, (g.nodes[0] - c0 + 2) / 3), nb1 = std::max(0, (g.nodes[1] - c1 + 2) / 3);
+          if (nb0 * nb1 == 0) continue;
+          k_up_assemble_bins<SH, 3, W><<<std::min<unsigned>(blocks_for(nb0 * nb1, W), 148 * 16), W * 32, 0, s>>>(
+              g, pd.p, cap, xs.p, bin_start.p, bflag.p, Atan.p, act_idx.p, row_mask.p, row_nzb.p, vals.p, row_len,
+              dt * q.mob, c0, c1, nb0, nb1); ++g_launches;
+        }
+        k_diag_inverse<2, 3><<<blocks_for(n_act), kThreads, 0, s>>>(n_act, act_list.p, freem.p, row_mask.p,
+                                                                    row_nzb.p, vals.p, row_len, dinv.p); ++g_launches;
+        CKL();
+      }
+    };
+    if (shape == 2) run(IC<2>{});
+    else run(IC<1>{});
+    matrix_valid = true;
+  }
+
+  // CoupledSim::step (src/porous.cpp:91-168): no line search, convergence on
+  // |r| / (largest r0 seen), then commit F / V / sigma / p_nodes / settlement
+  void coupled_step(double dt, impm_step_record* rec) {
+    if (!step_built) begin_step();
+    up_dt = dt;
+    ++step_counter;
+    std::vector<double> rels;
+    const auto t0 = std::chrono::steady_clock::now();
+    double diff_s = 0.0, solve_s = 0.0;
+    int kry = 0, iters = 0;
+    // x = (0 for u, committed nodal pressure for p), masked to free DOFs
+    mask_copy(prev.p, u.p);
+    double rn = residual_up(u.p, dt, r.p);
+    const double r0 = rn;
+    up_rscale = std::max(up_rscale, r0);
+    const double denom = up_rscale;
+    bool converged = r0 < opt.abs_floor;
+    for (int it = 1; it <= opt.max_iterations && !converged; ++it) {
+      auto tj = std::chrono::steady_clock::now();
+      jacobian_up(u.p, dt);
+      sync();
+      diff_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - tj).count();
+      auto ts = std::chrono::steady_clock::now();
+      axpbypcz(-1.0, r.p, 0.0, tmp2.p);
+      kry += solve_dev(tmp2.p, delta.p);
+      solve_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - ts).count();
+      axpbypcz(1.0, delta.p, 1.0, u.p);
+      rn = residual_up(u.p, dt, r.p);
+      rels.push_back(rn / denom);
+      iters = it;
+      if (rn / denom <= opt.tol || rn < opt.abs_floor) converged = true;
+    }
+    if (rec) {
+      rec->step = step_counter;
+      rec->iterations = iters;
+      rec->r0_norm = r0;
+      rec->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      rec->diff_seconds = diff_s;
+      rec->solve_seconds = solve_s;
+      rec->krylov_iterations = kry;
+      rec->backward_passes = iters * F * 25;
+      rec->nnz_assembled = iters * ref_nnz();
+      finish_record(rec, rels);
+    }
+    if (!converged)
+      throw SimError(IMPM_ERR_NONCONVERGENCE, "coupled Newton did not converge at step " + std::to_string(step_counter),
+                     rels);
+    // commit (src/porous.cpp:139-163)
+    const PoroC q = poro_c();
+    if (P > 0) {
+      Prof::Scope ps(&prof, kcCommit);
+      if (shape == 2)
+        k_up_commit<2><<<blocks_for(P), kThreads, 0, s>>>(g, pd.p, cap, P, xs.p, key.p, sup.p, u.p, q, uty.p);
+      else
+        k_up_commit<1><<<blocks_for(P), kThreads, 0, s>>>(g, pd.p, cap, P, xs.p, key.p, sup.p, u.p, q, uty.p);
+      ++g_launches;
+      CKL();
+    }
+    // p_nodes <- pressure DOFs of x (displacement components are not kept)
+    CK(cudaMemsetAsync(prev.p, 0, sizeof(double) * NF(), s));
+    k_copy_field<<<blocks_for(g.N), kThreads, 0, s>>>(g.N, 3, 2, freem.p, u.p, prev.p); ++g_launches;
+    CKL();
+    up_time += dt;
+    sync();
+  }
   // ------------------------------------------------------- commit (K9)
   void commit_step() {
     if (!step_built) throw SimError(IMPM_ERR_CONFIG, "commit_step before begin_step");
@@ -1310,9 +1605,9 @@ struct Sim {
     DBuf<double> dvals;
     dcols.ensure(z);
     dvals.ensure(z);
-    dispatch([&](auto Dc, auto) {
-      constexpr int DD = decltype(Dc)::value;
-      k_csr_fill<DD, DD><<<blocks_for(n_dofs), kThreads, 0, s>>>(g, n_dofs, node_of.p, field_of.p, dof_of.p, act_idx.p,
+    dispatch_df([&](auto Dc, auto Fc) {
+      constexpr int DD = decltype(Dc)::value, FE = decltype(Fc)::value;
+      k_csr_fill<DD, FE><<<blocks_for(n_dofs), kThreads, 0, s>>>(g, n_dofs, node_of.p, field_of.p, dof_of.p, act_idx.p,
                                                                  vals.p, row_len, row_slots.p, row_nzb.p, rowptr.p,
                                                                  dcols.p,
                                                                  vals_h ? dvals.p : nullptr); ++g_launches;
@@ -1373,6 +1668,22 @@ impm_status impm_sim_create(const impm_grid* grid, const impm_material* mat, con
 }
 
 const char* impm_create_error(void) { return g_create_error.c_str(); }
+
+impm_status impm_coupled_create(const impm_grid* grid, const impm_poro* poro, const impm_options* opt, int32_t device,
+                                impm_sim** out) {
+  if (!grid || !poro || !opt || !out) return IMPM_ERR_CONFIG;
+  try {
+    impm_material dummy{IMPM_NEO_HOOKEAN, 0, 1.0, 0.0, 0.0};
+    *out = reinterpret_cast<impm_sim*>(new Sim(grid, &dummy, opt, device, poro));
+    return IMPM_OK;
+  } catch (const SimError& e) {
+    g_create_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_create_error = e.what();
+    return IMPM_ERR_CUDA;
+  }
+}
 
 impm_status impm_sim_destroy(impm_sim* h) {
   delete reinterpret_cast<Sim*>(h);
@@ -1517,7 +1828,9 @@ impm_status impm_sim_jacobian_csr(impm_sim* h, const double* uh, double load_sca
                                   int32_t* cols, double* vals) {
   SIM;
   API_BEGIN(sim)
-  (void)load_scale;  // J does not depend on the load scale (external loads are constant in u)
+  // J does not depend on the load scale (external loads are constant in u);
+  // in coupled mode the argument is the time step dt (K_pp = V0 dt mob g.g)
+  if (sim->coupled) sim->up_dt = load_scale;
   if (!sim->step_built) throw SimError(IMPM_ERR_CONFIG, "jacobian before begin_step");
   if (row_ptr && uh) {
     sim->upload_dof_vec(uh, sim->tmp1.p);
@@ -1532,7 +1845,7 @@ impm_status impm_sim_linear_solve(impm_sim* h, const double* uh, double load_sca
                                   int32_t* kit) {
   SIM;
   API_BEGIN(sim)
-  (void)load_scale;
+  if (sim->coupled) sim->up_dt = load_scale;
   if (!sim->step_built) throw SimError(IMPM_ERR_CONFIG, "linear_solve before begin_step");
   sim->upload_dof_vec(uh, sim->tmp1.p);
   sim->jacobian_dev(sim->tmp1.p);
@@ -1563,6 +1876,46 @@ impm_status impm_sim_step(impm_sim* h, double load_scale, impm_step_record* rec)
   sim->commit_step();
   API_END(sim)
 }
+impm_status impm_coupled_initialize(impm_sim* h) {
+  SIM;
+  API_BEGIN(sim)
+  if (!sim->coupled) throw SimError(IMPM_ERR_CONFIG, "not a coupled simulation");
+  sim->begin_step();
+  API_END(sim)
+}
+impm_status impm_coupled_step(impm_sim* h, double dt, impm_step_record* rec) {
+  SIM;
+  API_BEGIN(sim)
+  if (!sim->coupled) throw SimError(IMPM_ERR_CONFIG, "not a coupled simulation");
+  sim->coupled_step(dt, rec);
+  API_END(sim)
+}
+impm_status impm_coupled_nodal_pressure(impm_sim* h, double* p) {
+  SIM;
+  API_BEGIN(sim)
+  if (!sim->coupled) throw SimError(IMPM_ERR_CONFIG, "not a coupled simulation");
+  std::vector<double> gv(sim->NF());
+  CK(cudaMemcpyAsync(gv.data(), sim->prev.p, sizeof(double) * gv.size(), cudaMemcpyDeviceToHost, sim->s));
+  sim->sync();
+  for (int n = 0; n < sim->g.N; ++n) p[n] = gv[static_cast<size_t>(n) * 3 + 2];
+  API_END(sim)
+}
+impm_status impm_coupled_settlement(impm_sim* h, double* u_total_y, double* time) {
+  SIM;
+  API_BEGIN(sim)
+  if (!sim->coupled) throw SimError(IMPM_ERR_CONFIG, "not a coupled simulation");
+  if (time) *time = sim->up_time;
+  if (u_total_y && sim->P > 0) {
+    DBuf<double> o;
+    o.ensure(sim->P);
+    k_gather_orig<<<blocks_for(sim->P), kThreads, 0, sim->s>>>(sim->uty.p, sim->orig.p, sim->P, o.p); ++g_launches;
+    CKL();
+    CK(cudaMemcpyAsync(u_total_y, o.p, sizeof(double) * sim->P, cudaMemcpyDeviceToHost, sim->s));
+    sim->sync();
+  }
+  API_END(sim)
+}
+
 impm_status impm_sim_nodal_solution(impm_sim* h, double* uh) {
   SIM;
   API_BEGIN(sim)

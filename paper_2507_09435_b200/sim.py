@@ -17,7 +17,7 @@ from .particles import GridSpec, ParticleArray, particle_doubles
 
 MATERIAL_KINDS = {"hencky": 0, "hencky_j2": 1, "neo_hookean": 2}
 SHAPES = {"gimp": 1, "quadratic-bspline": 2, "quadratic_bspline": 2}
-KRYLOV = {"auto": 0, "cg": 1, "bicgstab": 2}
+KRYLOV = {"auto": 0, "cg": 1, "bicgstab": 2, "gmres": 3}
 PRECOND = {"mg": 0, "multigrid": 0, "block_jacobi": 1, "jacobi": 1}
 
 
@@ -333,3 +333,168 @@ class MpmSim:
 
     def set_stream(self, stream_ptr):
         self._h.call("impm_sim_set_stream", ctypes.c_void_p(stream_ptr))
+
+
+@dataclass
+class PoroParams:
+    """impm::PoroParams (porous.hpp:22-38)."""
+    lambda_: float
+    mu: float
+    k: float
+    mu_f: float
+    rho_f: float = 1000.0
+
+    def mobility(self):
+        return self.k / self.mu_f
+
+    def consolidation_coefficient(self):
+        return self.k * (self.lambda_ + 2.0 * self.mu) / self.mu_f
+
+
+class CoupledSim:
+    """impm::CoupledSim (porous.hpp:48-125): 2D small-strain u-p on reference-
+    configuration weights, fields (ux, uy, p) per node, stepped on the GPU."""
+
+    def __init__(self, grid: GridSpec, particles, poro: PoroParams, options: Optional[SolverOptions] = None,
+                 device: int = 0):
+        if grid.dim != 2:
+            from .errors import ConfigError
+            raise ConfigError("coupled u-p is 2D")
+        self.grid = grid
+        self.D = 2
+        self.poro = poro
+        self.options = options or SolverOptions()
+        L = _abi.lib()
+        g = _abi.Grid()
+        g.dim = 2
+        for a in range(3):
+            g.nodes[a] = int(grid.nodes[a]) if a < 2 else 1
+            g.origin[a] = float(grid.origin[a]) if a < 2 else 0.0
+        g.h = float(grid.h)
+        pc = _abi.Poro(poro.lambda_, poro.mu, poro.k, poro.mu_f, poro.rho_f)
+        o = self.options.to_c()
+        h = ctypes.c_void_p()
+        st = L.impm_coupled_create(ctypes.byref(g), ctypes.byref(pc), ctypes.byref(o), device, ctypes.byref(h))
+        if st != _abi.OK:
+            raise_for(st, L.impm_create_error().decode())
+        self._h = _Handle.__new__(_Handle)
+        self._h._L = L
+        self._h.h = h
+        self._N = grid.node_count()
+        self.fixed_u = np.zeros(self._N * 2, dtype=np.uint8)  # [node*2 + comp]
+        self.fixed_p = np.zeros(self._N, dtype=np.uint8)
+        self._gravity = np.zeros(2)
+        data = np.ascontiguousarray(particles.data if isinstance(particles, ParticleArray) else particles,
+                                    dtype=np.float64)
+        self._h.call("impm_sim_set_particles", _abi.ptr(data), data.shape[0], data.strides[0])
+        self._n_particles = data.shape[0]
+        self._X1 = data[:, 1].copy()  # reference y (Particle<2>::X[1])
+        self._initialized = False
+        self.gravity = np.zeros(2)
+
+    @property
+    def gravity(self):
+        return self._gravity.copy()
+
+    @gravity.setter
+    def gravity(self, gv):
+        self._gravity = np.asarray(gv, dtype=np.float64).reshape(2).copy()
+        g3 = np.zeros(3)
+        g3[:2] = self._gravity
+        self._h.call("impm_sim_set_gravity", _abi.ptr(g3))
+
+    @property
+    def particles(self) -> ParticleArray:
+        out = np.zeros((self._n_particles, particle_doubles(2)))
+        self._h.call("impm_sim_get_particles", _abi.ptr(out), self._n_particles, out.strides[0])
+        return ParticleArray(out, 2)
+
+    def fix_displacement(self, predicate, component=-1):
+        pos = self.grid.node_positions()
+        mask = np.asarray(predicate(pos), dtype=bool).reshape(-1)
+        for c in range(2):
+            if component < 0 or component == c:
+                self.fixed_u[np.nonzero(mask)[0] * 2 + c] = 1
+
+    def fix_pressure(self, predicate):
+        pos = self.grid.node_positions()
+        mask = np.asarray(predicate(pos), dtype=bool).reshape(-1)
+        self.fixed_p[mask] = 1
+
+    def initialize(self):
+        """src/porous.cpp:25-72"""
+        fixed3 = np.zeros(self._N * 3, dtype=np.uint8)
+        fixed3[0::3] = self.fixed_u[0::2]
+        fixed3[1::3] = self.fixed_u[1::2]
+        fixed3[2::3] = self.fixed_p
+        self._h.call("impm_sim_set_fixed", _abi.ptr(fixed3))
+        self._h.call("impm_coupled_initialize")
+        self._initialized = True
+
+    def n_dofs(self):
+        n = ctypes.c_int32()
+        self._h.call("impm_sim_n_dofs", ctypes.byref(n))
+        return n.value
+
+    def dofs(self) -> DofMap:
+        n = self.n_dofs()
+        dof_of = np.zeros(self._N * 3, dtype=np.int32)
+        node_of = np.zeros(max(n, 1), dtype=np.int32)
+        field_of = np.zeros(max(n, 1), dtype=np.int32)
+        self._h.call("impm_sim_dof_map", _abi.ptr(dof_of), _abi.ptr(node_of), _abi.ptr(field_of))
+        return DofMap(3, n, dof_of, node_of[:n], field_of[:n])
+
+    def residual(self, x, dt):
+        x = _abi.f64(x)
+        r = np.zeros(max(self.n_dofs(), 1))
+        self._h.call("impm_sim_residual", _abi.ptr(x), float(dt), _abi.ptr(r))
+        return r[: self.n_dofs()]
+
+    def jacobian_csr(self, x, dt):
+        return MpmSim.jacobian_csr(self, x, dt)
+
+    def step(self, dt) -> StepRecord:
+        if not self._initialized:
+            self.initialize()
+        rec, buf = MpmSim._record(self)
+        self._h.call("impm_coupled_step", float(dt), ctypes.byref(rec))
+        return MpmSim._to_record(rec, buf)
+
+    def nodal_pressure(self):
+        out = np.zeros(self._N)
+        self._h.call("impm_coupled_nodal_pressure", _abi.ptr(out))
+        return out
+
+    def _settlement(self):
+        out = np.zeros(max(self._n_particles, 1))
+        t = ctypes.c_double()
+        self._h.call("impm_coupled_settlement", _abi.ptr(out), ctypes.byref(t))
+        return out[: self._n_particles], t.value
+
+    def time(self):
+        return self._settlement()[1]
+
+    def top_settlement(self):
+        """mean downward displacement of the top particle row (src/porous.cpp:170-183)"""
+        uty, _ = self._settlement()
+        top = self._X1 >= self._X1.max() - 1e-9
+        return float(-uty[top].sum() / top.sum()) if top.any() else 0.0
+
+    def pressure_profile(self, x_index, surface_y):
+        """nodal pressures on one grid column by depth (src/porous.cpp:185-199)"""
+        mass = np.zeros(self._N)
+        self._h.call("impm_sim_node_mass", _abi.ptr(mass))
+        pm = self.particles.m[:, 0].max() if self._n_particles else 0.0
+        active = mass > 1e-12 * pm
+        pos = self.grid.node_positions()
+        p = self.nodal_pressure()
+        ny = int(self.grid.nodes[1])
+        out = []
+        for n in range(self._N):
+            if not active[n] or n // ny != x_index:
+                continue
+            y = pos[n, 1]
+            if y < -1e-9 or y > surface_y + 1e-9:
+                continue
+            out.append((surface_y - y, 0.0 if self.fixed_p[n] else p[n]))
+        return sorted(out)

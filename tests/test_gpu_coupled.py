@@ -1,0 +1,58 @@
+"""GPU parity of the coupled u-p path (CoupledSim, porous.hpp:48-186,
+src/porous.cpp:25-168) against the reference-generated `upcol` fixture
+(10-cell consolidation column, scenarios.cpp:387-418)."""
+import numpy as np
+import pytest
+
+import golden_util as gu
+
+pytestmark = pytest.mark.gpu
+
+
+def make():
+    import paper_2507_09435_b200 as impm
+
+    fx = gu.load("upcol")
+    g = fx["grid"]
+    grid = impm.GridSpec(2, tuple(g[0:2]), float(g[3]), (int(g[4]), int(g[5])))
+    lam, mu, k, mu_f, rho_f, tol = fx["poro"]
+    sim = impm.CoupledSim(grid, fx["particles0"], impm.PoroParams(lam, mu, k, mu_f, rho_f),
+                          impm.SolverOptions(tol=tol))
+    sim.fixed_u[:] = fx["fixed_u"]
+    sim.fixed_p[:] = fx["fixed_p"]
+    sim.gravity = fx["gravity"]
+    return sim, fx
+
+
+def test_coupled_dofs_pattern_bit_exact():
+    sim, fx = make()
+    sim.initialize()
+    np.testing.assert_array_equal(sim.dofs().dof_of, fx["dof_of"])
+    rp, cols, _ = sim.jacobian_csr(np.zeros(sim.n_dofs()), 100.0)
+    np.testing.assert_array_equal(rp, fx["row_ptr"])
+    np.testing.assert_array_equal(cols, fx["cols"])
+
+
+def test_coupled_residual_and_jacobian():
+    sim, fx = make()
+    sim.initialize()
+    r = sim.residual(fx["x1"], 100.0)
+    assert gu.rel_err(r, fx["r1"]) <= 1e-9
+    rp, cols, vals = sim.jacobian_csr(fx["x1"], 100.0)
+    assert gu.csr_row_scaled_err(rp, vals, fx["J1_vals"]) <= 1e-9
+
+
+def test_coupled_steps_counts_settlement_pressure():
+    sim, fx = make()
+    its, settle = [], []
+    for _ in range(len(fx["newton_iters"])):
+        rec = sim.step(100.0)
+        its.append(rec.iterations)
+        settle.append(sim.top_settlement())
+    np.testing.assert_array_equal(its, fx["newton_iters"])
+    assert gu.rel_err(settle, fx["settlement"]) <= 1e-7
+    assert gu.rel_err(sim.nodal_pressure(), fx["p_nodes"]) <= 1e-7
+    got, ref = sim.particles.data, fx["particles_final"]
+    scale = np.maximum(np.abs(ref).max(axis=0), 1e-300)
+    err = np.abs(got - ref).max(axis=0) / scale
+    assert err[np.abs(ref).max(axis=0) > 1e-12].max() <= 1e-7
