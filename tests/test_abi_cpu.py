@@ -131,3 +131,17 @@ def test_gimp_weight_known_answers():
     assert impm.block_size("cubic-bspline") == 7
     with pytest.raises(impm.ConfigError):
         impm.gimp_weight_1d(0.0, 0.6, 1.0)
+
+
+def build_facade_smoke(out_path):
+    """Compiles tests/cpp/facade_smoke.cpp against include/impm_gpu.hpp and
+    libimpm_gpu.so (the C++ drop-in facade)."""
+    subprocess.run(["g++", "-std=c++20", "-O2", "-I", os.path.join(REPO, "include"), "-o", out_path,
+                    os.path.join(REPO, "tests", "cpp", "facade_smoke.cpp"),
+                    "-L", os.path.join(REPO, "paper_2507_09435_b200"), "-limpm_gpu",
+                    "-Wl,-rpath," + os.path.join(REPO, "paper_2507_09435_b200")], check=True)
+    return out_path
+
+
+def test_cpp_facade_compiles_and_links(lib, tmp_path):
+    assert os.path.exists(build_facade_smoke(str(tmp_path / "facade_smoke")))
