@@ -17,7 +17,8 @@ __all__ = [
     "ConfigError", "CudaError", "DomainError", "Error", "LinearSolverError", "NonConvergenceError",
     "OutOfDomainError", "SeedingFault", "UnsupportedOperation", "GridSpec", "ParticleArray", "particle_doubles",
     "particle_fields", "seed_box", "DofMap", "ElasticParams", "MaterialSpec", "MpmSim", "SolverOptions",
-    "StepRecord", "gimp_weight_1d", "block_size", "CoupledSim", "PoroParams",
+    "StepRecord", "gimp_weight_1d", "block_size", "CoupledSim", "PoroParams", "Config", "run_scenario",
+    "run_scenario_text", "bench_scenario",
 ]
 
 
@@ -45,3 +46,7 @@ def block_size(kind):
     if kind not in _BLOCK:
         raise ConfigError("unknown shape function kind: " + kind)
     return _BLOCK[kind]
+
+
+from .config import Config  # noqa: E402
+from .scenarios import bench_scenario, run_scenario, run_scenario_text  # noqa: E402

@@ -1269,6 +1269,42 @@ __global__ void k_dot2(int64_t n, const double* __restrict__ a, const double* __
   block_sum_store<2>(v, partials);
 }
 
+// h_i = V_i . w for i < nv (blockIdx.y = i), per-block partials [i][block]
+__global__ void k_vdot(int64_t n, const double* __restrict__ V, int64_t ldv, const double* __restrict__ w,
+                       double* __restrict__ partials) {
+  const double* Vi = V + static_cast<int64_t>(blockIdx.y) * ldv;
+  double v[1] = {0.0};
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    v[0] += Vi[i] * w[i];
+  block_sum_store<1>(v, partials + static_cast<int64_t>(blockIdx.y) * gridDim.x);
+}
+// out[row] = sum of partials row (one block per row, fixed order)
+__global__ void k_finalize_rows(const double* __restrict__ partials, int nb, double* __restrict__ out) {
+  const double* p = partials + static_cast<int64_t>(blockIdx.x) * nb;
+  double v = 0.0;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) v += p[i];
+  __shared__ double red[32];
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) out[blockIdx.x] = v;
+  }
+}
+// w -= sum_i h_i V_i  (h on the device)
+__global__ void k_vsub(int64_t n, const double* __restrict__ V, int64_t ldv, int nv, const double* __restrict__ h,
+                       double* __restrict__ w) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double acc = w[i];
+    for (int j = 0; j < nv; ++j) acc -= h[j] * V[static_cast<int64_t>(j) * ldv + i];
+    w[i] = acc;
+  }
+}
+
 // y = a*x + b*y + c*z  (z optional)
 __global__ void k_axpbypcz(int64_t n, double a, const double* __restrict__ x, double b, double* __restrict__ y,
                            double c, const double* __restrict__ z) {

@@ -1136,7 +1136,8 @@ struct Sim {
   // GMRES(m), right-preconditioned (block Jacobi or MG), modified
   // Gram-Schmidt on device vectors, Hessenberg/Givens on the host.
   // Robust path for the nonsymmetric, badly scaled u-p saddle point.
-  DBuf<double> gm_V;
+  DBuf<double> gm_V, gm_part, gm_h;
+  static constexpr int kGmBlocks = 148;
   double dot_sync(const double* a, const double* b) {
     k_dot2<<<kRedBlocks, kThreads, 0, s>>>(NF(), a, b, nullptr, nullptr, partials.p); ++g_launches;
     k_finalize_sum<2><<<1, 1024, 0, s>>>(partials.p, kRedBlocks, sums.p); ++g_launches;
@@ -1150,7 +1151,10 @@ struct Sim {
   template <int DD, int FE>
   int gmres_solve(const double* b, double* x, bool mgp) {
     const int64_t n = NF();
-    const int m = std::max(2, std::min(60, n_dofs));
+    const int m = std::max(2, std::min(300, n_dofs));
+    gm_part.ensure(static_cast<size_t>(m + 1) * kGmBlocks);
+    gm_h.ensure(m + 1);
+    std::vector<double> hbuf(m + 1);
     const int max_it = opt.krylov_max_iter > 0 ? opt.krylov_max_iter : std::max(2000, 20 * n_dofs);
     if (mgp) mg_setup<DD, FE>();
     CK(cudaMemsetAsync(dflag.p, 0, sizeof(int), s));
@@ -1174,11 +1178,16 @@ struct Sim {
         double* w = gm_V.p + static_cast<size_t>(j + 1) * n;
         apply_precond<DD, FE>(mgp, Vj, kz.p);
         spmv(kz.p, w, nullptr, nullptr);
-        for (int i = 0; i <= j; ++i) {
-          const double* Vi = gm_V.p + static_cast<size_t>(i) * n;
-          const double hij = dot_sync(w, Vi);
-          H[static_cast<size_t>(i) * m + j] = hij;
-          axpbypcz(-hij, Vi, 1.0, w);
+        // classical Gram-Schmidt, twice (CGS2): batched dots on the device
+        for (int i = 0; i <= j; ++i) H[static_cast<size_t>(i) * m + j] = 0.0;
+        for (int pass = 0; pass < 2; ++pass) {
+          k_vdot<<<dim3(kGmBlocks, j + 1), kThreads, 0, s>>>(n, gm_V.p, n, w, gm_part.p); ++g_launches;
+          k_finalize_rows<<<j + 1, 256, 0, s>>>(gm_part.p, kGmBlocks, gm_h.p); ++g_launches;
+          k_vsub<<<kRedBlocks, kThreads, 0, s>>>(n, gm_V.p, n, j + 1, gm_h.p, w); ++g_launches;
+          CKL();
+          CK(cudaMemcpyAsync(hbuf.data(), gm_h.p, sizeof(double) * (j + 1), cudaMemcpyDeviceToHost, s));
+          sync();
+          for (int i = 0; i <= j; ++i) H[static_cast<size_t>(i) * m + j] += hbuf[i];
         }
         const double hn = std::sqrt(dot_sync(w, w));
         H[static_cast<size_t>(j + 1) * m + j] = hn;
