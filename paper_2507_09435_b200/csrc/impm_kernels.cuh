@@ -923,7 +923,7 @@ struct SpmvTab {
 enum SpmvMode { kSpmvY = 0, kSpmvJacobi = 1, kSpmvResid = 2 };
 
 template <int D, int F, int WARPS, int MODE = kSpmvY>
-__global__ void __launch_bounds__(WARPS * 32) k_spmv(GridC g, const int* __restrict__ act_list, int n_act,
+__global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC g, const int* __restrict__ act_list, int n_act,
                                                      const double* __restrict__ vals, int64_t row_len,
                                                      const uint8_t* __restrict__ row_slots,
                                                      const int* __restrict__ row_nzb,
@@ -935,6 +935,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_spmv(GridC g, const int* __restr
   constexpr int S = ipow_c(5, D);
   constexpr int FF = F * F;
   constexpr int XS = cpad(S, F);
+  constexpr int NB = 6;  // double2 per lane buffered ahead of the x gathers
   __shared__ int offt[S];
   __shared__ __align__(16) double xs_all[WARPS][XS];
   for (int sl = threadIdx.x; sl < S; sl += blockDim.x) {
@@ -951,10 +952,26 @@ __global__ void __launch_bounds__(WARPS * 32) k_spmv(GridC g, const int* __restr
   if (done == nullptr || *done == 0) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double* xs = xs_all[warp];
-    for (int row = blockIdx.x * WARPS + warp; row < n_act; row += gridDim.x * WARPS) {
+    // contiguous row chunks per CTA: consecutive rows share 4/5 of their x
+    // neighbourhood, so the x gathers of a chunk hit in this SM's L1
+    constexpr int CH = 16 * WARPS;
+    const int nchunks = (n_act + CH - 1) / CH;
+    for (int ci = blockIdx.x; ci < nchunks; ci += gridDim.x)
+    for (int row = ci * CH + warp; row < min(n_act, (ci + 1) * CH); row += WARPS) {
       const int k = act_list[row];
       const int nzb = row_nzb[row];
       const int cp = cpad(nzb, F);
+      const int h = cp >> 1, tot2 = F * h;
+      // 1. the first NB double2 per lane of the row (independent of x) go in
+      //    flight before the x gathers
+      const double2* rv = reinterpret_cast<const double2*>(vals + static_cast<int64_t>(row) * row_len);
+      double2 buf[NB];
+#pragma unroll
+      for (int t = 0; t < NB; ++t) {
+        const int j2 = lane + 32 * t;
+        buf[t] = j2 < tot2 ? __ldcs(rv + j2) : make_double2(0.0, 0.0);  // streamed once: evict-first
+      }
+      // 2. stage the x records of the stored neighbours
       const uint8_t* rsl = row_slots + static_cast<int64_t>(row) * S;
       for (int pos = lane; pos < nzb; pos += 32) {
         const int64_t nb = static_cast<int64_t>(k + offt[rsl[pos]]) * F;
@@ -963,23 +980,24 @@ __global__ void __launch_bounds__(WARPS * 32) k_spmv(GridC g, const int* __restr
       }
       if (lane == 0 && cp != nzb * F) xs[nzb * F] = 0.0;
       __syncwarp();
+      // 3. component-major dot products (buffered head, streamed tail)
       double acc[3] = {0.0, 0.0, 0.0};
-      const double* rbase = vals + static_cast<int64_t>(row) * row_len;
-      const int h = cp >> 1;
+      const double2* xv = reinterpret_cast<const double2*>(xs);
+      auto consume = [&](int j2, const double2 v) {
+        const int c = F == 1 ? 0 : (F == 2 ? (j2 >= h) : (j2 >= h) + (j2 >= 2 * h));
+        const double2 xx = xv[j2 - c * h];
+        const double p = fma(v.x, xx.x, v.y * xx.y);
+        acc[0] += c == 0 ? p : 0.0;
+        if (F > 1) acc[1] += c == 1 ? p : 0.0;
+        if (F > 2) acc[2] += c == 2 ? p : 0.0;
+      };
 #pragma unroll
-      for (int c = 0; c < F; ++c) {
-        const double2* rv = reinterpret_cast<const double2*>(rbase + c * cp);
-        const double2* xv = reinterpret_cast<const double2*>(xs);
-        double a = 0.0;
-#pragma unroll 4
-        for (int j2 = lane; j2 < h; j2 += 32) {
-          const double2 v = __ldcs(rv + j2);  // streamed once: evict-first
-          const double2 xx = xv[j2];
-          a = fma(v.x, xx.x, a);
-          a = fma(v.y, xx.y, a);
-        }
-        acc[c] = a;
+      for (int t = 0; t < NB; ++t) {
+        const int j2 = lane + 32 * t;
+        if (j2 < tot2) consume(j2, buf[t]);
       }
+#pragma unroll 4
+      for (int j2 = lane + 32 * NB; j2 < tot2; j2 += 32) consume(j2, __ldcs(rv + j2));
 #pragma unroll
       for (int c = 0; c < F; ++c)
         for (int o = 16; o > 0; o >>= 1) acc[c] += __shfl_down_sync(0xffffffffu, acc[c], o);

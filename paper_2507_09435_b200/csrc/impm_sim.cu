@@ -68,7 +68,8 @@ struct DBuf {
 };
 
 constexpr int kThreads = 256;
-constexpr int kRedBlocks = 148 * 4;  // fixed partial count for deterministic reductions
+constexpr int kRedBlocks = 148 * 4;    // fixed partial count for deterministic reductions
+constexpr int kSpmvBlocks = 148 * 12;  // SpMV grid (4-warp CTAs, 8 resident per SM)
 inline unsigned blocks_for(int64_t n, int t = kThreads) { return static_cast<unsigned>(std::max<int64_t>(1, (n + t - 1) / t)); }
 
 template <int V>
@@ -195,6 +196,8 @@ struct Sim {
   // multigrid hierarchy (rebuilt with every Jacobian)
   std::vector<std::unique_ptr<MgLevel>> mg;
   DBuf<double> mg_dense, mg_lam, mg_T;
+  std::vector<double> mg_lam_host;
+  int mg_power_step = -1;
   DBuf<unsigned long long> mg_nzb;
   int mg_dense_n = 0;
   unsigned long long mg_stored_blocks = 0;
@@ -301,7 +304,7 @@ struct Sim {
     st.ensure(1);
     dflag.ensure(4);
     sc.ensure(kNSlots);
-    partials.ensure(8 * kRedBlocks);
+    partials.ensure(8 * kRedBlocks + kSpmvBlocks);
     sums.ensure(8);
     CK(cudaMallocHost(&h_st, sizeof(DevStatus)));
     CK(cudaMallocHost(&h_sc, sizeof(double) * kNSlots));
@@ -650,8 +653,8 @@ struct Sim {
     Prof::Scope ps(&prof, kcSpmv);
     dispatch_df([&](auto Dc, auto Fc) {
       constexpr int DD = decltype(Dc)::value, FE = decltype(Fc)::value;
-      constexpr int W = 8;
-      k_spmv<DD, FE, W><<<kRedBlocks, W * 32, 0, s>>>(g, act_list.p, n_act, vals.p, row_len, row_slots.p,
+      constexpr int W = 4;
+      k_spmv<DD, FE, W><<<kSpmvBlocks, W * 32, 0, s>>>(g, act_list.p, n_act, vals.p, row_len, row_slots.p,
                                                       row_nzb.p, x, freem.p, y, dotv, parts, dflag.p); ++g_launches;
       CKL();
     });
@@ -679,13 +682,13 @@ struct Sim {
     const int batch = n_dofs < 20000 ? 16 : 4;
     int done = 0;
     double* partA = partials.p;
-    double* partB = partials.p + 2 * kRedBlocks;
+    double* partB = partials.p + kSpmvBlocks;
     for (int it = 0; !done;) {
       for (int i = 0; i < batch; ++i, ++it) {
         const int par = it & 1;
         spmv(kp.p, kq.p, kp.p, partA);
         Prof::Scope ps(&prof, kcKrylov);
-        k_cg_update2<FF><<<kRedBlocks, kThreads, 0, s>>>(N, act_idx.p, dinv.p, sc.p, dflag.p, par, partA, kRedBlocks,
+        k_cg_update2<FF><<<kRedBlocks, kThreads, 0, s>>>(N, act_idx.p, dinv.p, sc.p, dflag.p, par, partA, kSpmvBlocks,
                                                          x, kr.p, kz.p, kp.p, kq.p, partB); ++g_launches;
         k_cg_p2<FF><<<kRedBlocks, kThreads, 0, s>>>(N, act_idx.p, sc.p, dflag.p, par, it, partB, kRedBlocks, rtol2,
                                                     max_it, kz.p, kp.p); ++g_launches;
@@ -792,8 +795,8 @@ struct Sim {
   template <int DD, int FE, int MODE>
   void level_spmv(MgLevel& L, const double* x, double* y, const double* b, double omega, const double* dotv,
                   double* parts) {
-    constexpr int W = 8;
-    k_spmv<DD, FE, W, MODE><<<kRedBlocks, W * 32, 0, s>>>(L.g, L.act_list, L.n_act, L.vals, L.row_len, L.row_slots,
+    constexpr int W = 4;
+    k_spmv<DD, FE, W, MODE><<<kSpmvBlocks, W * 32, 0, s>>>(L.g, L.act_list, L.n_act, L.vals, L.row_len, L.row_slots,
                                                           L.row_nzb, x, L.freem, y, dotv, parts, dflag.p, b, L.dinv,
                                                           omega); ++g_launches;
     CKL();
@@ -911,8 +914,11 @@ struct Sim {
     // lambda_max(Dinv A): omega = 4 / (3 lambda) (Chebyshev-optimal
     // smoothing); device-resident, one host read for all levels
     CK(cudaMemsetAsync(dflag.p, 0, sizeof(int), s));
+    // lambda_max(Dinv A) moves little between the Newton iterations of one
+    // load step: estimate it on the first setup of the step, then reuse
+    const bool need_power = mg_power_step != step_counter || mg_lam_host.size() != mg.size();
     mg_lam.ensure(std::max<size_t>(mg.size(), 1));
-    {
+    if (need_power) {
       Prof::Scope psp(&prof, kcMgPower);
       for (size_t l = 0; l + 1 < mg.size(); ++l) {
         MgLevel& L = *mg[l];
@@ -931,9 +937,15 @@ struct Sim {
     }
     {
       std::vector<double> lam(mg.size(), 1.0);
-      if (mg.size() > 1)
-        CK(cudaMemcpyAsync(lam.data(), mg_lam.p, sizeof(double) * (mg.size() - 1), cudaMemcpyDeviceToHost, s));
-      sync();
+      if (need_power) {
+        if (mg.size() > 1)
+          CK(cudaMemcpyAsync(lam.data(), mg_lam.p, sizeof(double) * (mg.size() - 1), cudaMemcpyDeviceToHost, s));
+        sync();
+        mg_lam_host = lam;
+        mg_power_step = step_counter;
+      } else {
+        lam = mg_lam_host;
+      }
       for (size_t l = 0; l + 1 < mg.size(); ++l) {
         MgLevel& L = *mg[l];
         const int64_t n = static_cast<int64_t>(L.g.N) * FE;
@@ -1077,7 +1089,7 @@ struct Sim {
     }
     CK(cudaMemsetAsync(dflag.p, 0, sizeof(int), s));
     double* partA = partials.p;
-    double* partB = partials.p + 2 * kRedBlocks;
+    double* partB = partials.p + kSpmvBlocks;
     CK(cudaMemsetAsync(x, 0, sizeof(double) * n, s));
     CK(cudaMemcpyAsync(kr.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
     {
@@ -1101,7 +1113,7 @@ struct Sim {
         spmv(kp.p, kq.p, kp.p, partA);
         {
           Prof::Scope ps(&prof, kcKrylov);
-          k_cg_update_mg<FE><<<kRedBlocks, kThreads, 0, s>>>(N, act_idx.p, sc.p, dflag.p, par, partA, kRedBlocks, x,
+          k_cg_update_mg<FE><<<kRedBlocks, kThreads, 0, s>>>(N, act_idx.p, sc.p, dflag.p, par, partA, kSpmvBlocks, x,
                                                              kr.p, kp.p, kq.p, partB + kRedBlocks); ++g_launches;
           CKL();
         }
