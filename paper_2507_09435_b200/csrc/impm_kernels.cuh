@@ -877,6 +877,166 @@ __global__ void __launch_bounds__(WARPS * 32) k_assemble_bins(
   }
 }
 
+// Staged variant of k_assemble_bins: the bin's particles are processed in
+// chunks of PCH; per chunk the tangent blocks A_p (contiguous for a bin's
+// sorted particles) and the 1D weights / node gradients of every particle
+// are staged in shared memory with all loads in flight at once, so the
+// per-particle loop (H_k = g^k . A_p, then the lane-owned block pairs) runs
+// from shared memory only.
+template <int D, int SHAPE, int PPL, int WARPS, int PCH>
+__global__ void __launch_bounds__(WARPS * 32) k_assemble_bins_staged(
+    GridC g, const double* __restrict__ pd, int64_t cap, const double* __restrict__ xs,
+    const int* __restrict__ bin_start, const uint8_t* __restrict__ bflag, const double* __restrict__ A,
+    const int* __restrict__ act_idx, const unsigned* __restrict__ row_mask, const int* __restrict__ row_nzb,
+    double* __restrict__ vals, int64_t row_len, int c0, int c1, int c2, int nb0, int nb1, int nb2) {
+  constexpr int DD = D * D;
+  constexpr int D3 = D * D * D;
+  constexpr int NA = DD * DD;
+  constexpr int NK = ipow_c(3, D);
+  __shared__ double As[WARPS][PCH * NA];
+  __shared__ double Gs[WARPS][PCH][NK][D];
+  __shared__ double Hs[WARPS][NK * D3];
+  __shared__ double W1[WARPS][PCH][D][3][2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nbins = nb0 * nb1 * nb2;
+  const int col[3] = {c0, c1, c2};
+  const int nbv[3] = {nb0, nb1, nb2};
+  for (int bi = blockIdx.x * WARPS + warp; bi < nbins; bi += gridDim.x * WARPS) {
+    int bidx[3] = {0, 0, 0}, r = bi, b = 0;
+#pragma unroll
+    for (int a = D - 1; a >= 0; --a) {
+      bidx[a] = 3 * (r % nbv[a]) + col[a];
+      r /= nbv[a];
+      b += bidx[a] * g.stride[a];
+    }
+    const int fl = bflag[b];
+    if (!(fl & 0x80)) continue;
+    int cn[3] = {1, 1, 1};
+#pragma unroll
+    for (int a = 0; a < D; ++a) cn[a] = 2 + ((fl >> a) & 1);
+    const int nk = cn[0] * cn[1] * cn[2];
+    // lane task = (row node k, run of PPL column nodes l0..l0+PPL-1)
+    const int nchunk = (nk + PPL - 1) / PPL;
+    const int ntasks = nk * nchunk;
+    const int p0 = bin_start[b], p1 = bin_start[b + 1];
+    for (int r0 = 0; r0 < ntasks; r0 += 32) {
+      const int task = r0 + lane;
+      const bool has_task = task < ntasks;
+      const int tk = has_task ? task / nchunk : 0;
+      const int tl0 = has_task ? (task - tk * nchunk) * PPL : nk;
+      double acc[PPL][DD];
+#pragma unroll
+      for (int t = 0; t < PPL; ++t)
+#pragma unroll
+        for (int e = 0; e < DD; ++e) acc[t][e] = 0.0;
+      for (int pc = p0; pc < p1; pc += PCH) {
+        const int np = min(PCH, p1 - pc);
+        __syncwarp();
+        // stage A_p (contiguous) and the 1D weights of the chunk
+        const double* Ab = A + static_cast<int64_t>(pc) * NA;
+        for (int e = lane; e < np * NA; e += 32) As[warp][e] = __ldg(Ab + e);
+        for (int e = lane; e < np * D * 3; e += 32) {
+          const int pl = e / (D * 3), rem = e - pl * D * 3, a = rem / 3, i = rem - a * 3;
+          double w = 0.0, dw = 0.0;
+          if (i < cn[a]) {
+            const int p = pc + pl;
+            const WeightValue wv = weight_1d<SHAPE>(xs[a * cap + p] - node_coord(g, a, bidx[a] + i),
+                                                    pd[(PF<D>::lp + a) * cap + p], g.h);
+            w = wv.w;
+            dw = wv.dw;
+          }
+          W1[warp][pl][a][i][0] = w;
+          W1[warp][pl][a][i][1] = dw;
+        }
+        __syncwarp();
+        for (int e = lane; e < np * nk; e += 32) {
+          const int pl = e / nk, k = e - pl * nk;
+          int li[3] = {0, 0, 0}, rr = k;
+#pragma unroll
+          for (int a = D - 1; a >= 0; --a) {
+            li[a] = rr % cn[a];
+            rr /= cn[a];
+          }
+          double w[3], dw[3], W, gk[3];
+#pragma unroll
+          for (int a = 0; a < D; ++a) {
+            w[a] = W1[warp][pl][a][li[a]][0];
+            dw[a] = W1[warp][pl][a][li[a]][1];
+          }
+          tensor_weight<D>(w, dw, W, gk);
+#pragma unroll
+          for (int a = 0; a < D; ++a) Gs[warp][pl][k][a] = gk[a];
+        }
+        __syncwarp();
+        for (int pl = 0; pl < np; ++pl) {
+          const double* Ap = &As[warp][pl * NA];
+          for (int e = lane; e < nk * D3; e += 32) {
+            const int k = e / D3, cdf = e - k * D3, c = cdf / DD, df = cdf - c * DD;
+            double sacc = 0.0;
+#pragma unroll
+            for (int bb = 0; bb < D; ++bb) sacc += Gs[warp][pl][k][bb] * Ap[(c * D + bb) * DD + df];
+            Hs[warp][e] = sacc;
+          }
+          __syncwarp();
+          if (has_task) {
+            double gl[PPL][3];
+#pragma unroll
+            for (int t = 0; t < PPL; ++t)
+#pragma unroll
+              for (int f = 0; f < D; ++f) gl[t][f] = (tl0 + t < nk) ? Gs[warp][pl][tl0 + t][f] : 0.0;
+            const double* Hk = &Hs[warp][tk * D3];
+#pragma unroll
+            for (int cd = 0; cd < DD; ++cd) {
+              double hv[3];
+#pragma unroll
+              for (int f = 0; f < D; ++f) hv[f] = Hk[cd * D + f];
+#pragma unroll
+              for (int t = 0; t < PPL; ++t)
+#pragma unroll
+                for (int f = 0; f < D; ++f) acc[t][cd] = fma(hv[f], gl[t][f], acc[t][cd]);
+            }
+          }
+          __syncwarp();
+        }
+      }
+      if (has_task) {
+        int lk[3] = {0, 0, 0}, rk = tk, node = 0;
+#pragma unroll
+        for (int a = D - 1; a >= 0; --a) {
+          lk[a] = rk % cn[a];
+          rk /= cn[a];
+        }
+#pragma unroll
+        for (int a = 0; a < D; ++a) node += (bidx[a] + lk[a]) * g.stride[a];
+        const int row = act_idx[node];
+        if (row >= 0) {
+          const unsigned* m = row_mask + static_cast<int64_t>(row) * 4;
+          const int cp = cpad(row_nzb[row], D);
+          double* rbase = vals + static_cast<int64_t>(row) * row_len;
+#pragma unroll
+          for (int t = 0; t < PPL; ++t) {
+            const int l = tl0 + t;
+            if (l >= nk) continue;
+            int ll[3] = {0, 0, 0}, rl = l, sl = 0;
+#pragma unroll
+            for (int a = D - 1; a >= 0; --a) {
+              ll[a] = rl % cn[a];
+              rl /= cn[a];
+            }
+#pragma unroll
+            for (int a = 0; a < D; ++a) sl = sl * 5 + (ll[a] - lk[a] + 2);
+            double* rv = rbase + mask_pos(m, sl) * D;
+#pragma unroll
+            for (int c = 0; c < D; ++c)
+#pragma unroll
+              for (int d = 0; d < D; ++d) rv[c * cp + d] += acc[t][c * D + d];
+          }
+        }
+      }
+    }
+  }
+}
+
 // masked diagonal block inverse per row (block-Jacobi / MG smoother)
 template <int D, int F = D>
 __global__ void k_diag_inverse(int n_act, const int* __restrict__ act_list, const uint8_t* __restrict__ freem,

@@ -636,7 +636,8 @@ struct Sim {
           }
           const int nbins = nb[0] * nb[1] * nb[2];
           if (nbins == 0) continue;
-          k_assemble_bins<DD, SH, PPL, W><<<std::min<unsigned>(blocks_for(nbins, W), 148 * 16), W * 32, 0, s>>>(
+          constexpr int WS = 4;
+          k_assemble_bins_staged<DD, SH, (DD == 3 ? 3 : PPL), WS, 4><<<std::min<unsigned>(blocks_for(nbins, WS), 148 * 32), WS * 32, 0, s>>>(
               g, pd.p, cap, xs.p, bin_start.p, bflag.p, Atan.p, act_idx.p, row_mask.p, row_nzb.p, vals.p, row_len,
               cc[0], cc[1], cc[2], nb[0], nb[1], nb[2]); ++g_launches;
         }
