@@ -557,6 +557,105 @@ __global__ void k_residual_nodes(GridC g, const double* __restrict__ pd, int64_t
   block_sum_store<1>(rr, partials);
 }
 
+// Residual phase B, bin-centric push in 3^D colour batches (bins of one
+// colour have disjoint supports): a warp owns a bin, lane k < nk owns box
+// node k and sums the bin's particle contributions
+// sum_b grad_{k,b} P_cb - w_k b_c s in fixed order, then adds them to r[k]
+// (exclusive within the colour; r zeroed first). Masking and r.r follow in
+// k_mask_norm.
+template <int D, int SHAPE, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_residual_bins(
+    GridC g, const double* __restrict__ pd, int64_t cap, const double* __restrict__ xs,
+    const int* __restrict__ bin_start, const uint8_t* __restrict__ bflag, const double* __restrict__ Pst,
+    const double* __restrict__ bext, double load_scale, double* __restrict__ r, int c0, int c1, int c2, int nb0,
+    int nb1, int nb2) {
+  __shared__ double W1[WARPS][D][3][2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nbins = nb0 * nb1 * nb2;
+  const int col[3] = {c0, c1, c2};
+  const int nbv[3] = {nb0, nb1, nb2};
+  for (int bi = blockIdx.x * WARPS + warp; bi < nbins; bi += gridDim.x * WARPS) {
+    int bidx[3] = {0, 0, 0}, rr = bi, b = 0;
+#pragma unroll
+    for (int a = D - 1; a >= 0; --a) {
+      bidx[a] = 3 * (rr % nbv[a]) + col[a];
+      rr /= nbv[a];
+      b += bidx[a] * g.stride[a];
+    }
+    const int fl = bflag[b];
+    if (!(fl & 0x80)) continue;
+    int cn[3] = {1, 1, 1};
+#pragma unroll
+    for (int a = 0; a < D; ++a) cn[a] = 2 + ((fl >> a) & 1);
+    const int nk = cn[0] * cn[1] * cn[2];
+    int li[3] = {0, 0, 0};
+    {
+      int rk = lane;
+#pragma unroll
+      for (int a = D - 1; a >= 0; --a) {
+        li[a] = rk % cn[a];
+        rk /= cn[a];
+      }
+    }
+    double acc[3] = {0.0, 0.0, 0.0};
+    const int p0 = bin_start[b], p1 = bin_start[b + 1];
+    for (int p = p0; p < p1; ++p) {
+      __syncwarp();
+      if (lane < 3 * D) {
+        const int a = lane / 3, i = lane % 3;
+        double w = 0.0, dw = 0.0;
+        if (i < cn[a]) {
+          const WeightValue wv = weight_1d<SHAPE>(xs[a * cap + p] - node_coord(g, a, bidx[a] + i),
+                                                  pd[(PF<D>::lp + a) * cap + p], g.h);
+          w = wv.w;
+          dw = wv.dw;
+        }
+        W1[warp][a][i][0] = w;
+        W1[warp][a][i][1] = dw;
+      }
+      __syncwarp();
+      if (lane < nk) {
+        double w[3], dw[3], W, gr[3];
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          w[a] = W1[warp][a][li[a]][0];
+          dw[a] = W1[warp][a][li[a]][1];
+        }
+        tensor_weight<D>(w, dw, W, gr);
+        const double* Pp = Pst + static_cast<int64_t>(p) * D * D;
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          double fint = gr[0] * __ldg(Pp + c * D);
+#pragma unroll
+          for (int bb = 1; bb < D; ++bb) fint += gr[bb] * __ldg(Pp + c * D + bb);
+          const double fext = W * __ldg(bext + c * cap + p) * load_scale;
+          acc[c] += fint - fext;
+        }
+      }
+    }
+    if (lane < nk) {
+      int node = 0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) node += (bidx[a] + li[a]) * g.stride[a];
+#pragma unroll
+      for (int c = 0; c < D; ++c) r[static_cast<int64_t>(node) * D + c] += acc[c];
+    }
+  }
+}
+
+// r <- r at free DOFs, 0 elsewhere; partial sums of r.r
+__global__ void k_mask_norm(int64_t n, const uint8_t* __restrict__ freem, double* __restrict__ r,
+                            double* __restrict__ partials) {
+  double v[1] = {0.0};
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double x = freem[i] ? r[i] : 0.0;
+    r[i] = x;
+    v[0] += x * x;
+  }
+  block_sum_store<1>(v, partials);
+}
+
 // ------------------------------------------------------- K6 tangent (AD) --
 // dP/dG per particle by forward-mode duals over the same expression graph as
 // the residual (hand-written AD replacing the tape, tape.hpp:107-122):

@@ -592,9 +592,23 @@ struct Sim {
       }
       {
         Prof::Scope ps(&prof, kcResN);
-        k_residual_nodes<DD, SH><<<kRedBlocks, kThreads, 0, s>>>(g, pd.p, cap, xs.p, bin_start.p, sup.p, Pst.p,
-                                                                 bext.p, act_flag.p, freem.p, load_scale, rd,
-                                                                 partials.p); ++g_launches;
+        CK(cudaMemsetAsync(rd, 0, sizeof(double) * NF(), s));
+        constexpr int W = 4;
+        const int nc = ipow_c(3, DD);
+        for (int col = 0; col < nc; ++col) {
+          int cc[3] = {0, 0, 0}, nb[3] = {1, 1, 1}, rr = col;
+          for (int a = DD - 1; a >= 0; --a) {
+            cc[a] = rr % 3;
+            rr /= 3;
+            nb[a] = std::max(0, (g.nodes[a] - cc[a] + 2) / 3);
+          }
+          const int nbins = nb[0] * nb[1] * nb[2];
+          if (nbins == 0) continue;
+          k_residual_bins<DD, SH, W><<<std::min<unsigned>(blocks_for(nbins, W), 148 * 16), W * 32, 0, s>>>(
+              g, pd.p, cap, xs.p, bin_start.p, bflag.p, Pst.p, bext.p, load_scale, rd, cc[0], cc[1], cc[2], nb[0],
+              nb[1], nb[2]); ++g_launches;
+        }
+        k_mask_norm<<<kRedBlocks, kThreads, 0, s>>>(NF(), freem.p, rd, partials.p); ++g_launches;
         CKL();
         k_finalize_sum<1><<<1, 1024, 0, s>>>(partials.p, kRedBlocks, &st.p->norm2); ++g_launches;
         CKL();
