@@ -52,7 +52,8 @@ typedef struct impm_grid {
 typedef enum impm_material_kind {
   IMPM_HENCKY = 0,
   IMPM_HENCKY_J2 = 1,
-  IMPM_NEO_HOOKEAN = 2
+  IMPM_NEO_HOOKEAN = 2,
+  IMPM_DRUCKER_PRAGER = 3  /* extension, parity unpinned (D <= 2) */
 } impm_material_kind;
 
 /* impm::MaterialSpec (mpm_solver.hpp:21-25) */
@@ -61,6 +62,8 @@ typedef struct impm_material {
   int32_t pad_;
   double E, nu;       /* ElasticParams (materials.hpp:12-23) */
   double kappa;       /* J2 yield strength */
+  double friction_deg;  /* Drucker-Prager friction angle [deg] */
+  double cohesion;      /* Drucker-Prager cohesion [Pa] (apex shift) */
 } impm_material;
 
 /* Transfer functions: impm::ShapeFunctionKind (gimp.hpp:11). */

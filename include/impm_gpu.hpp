@@ -215,7 +215,7 @@ class MpmSim {
       cg.origin[a] = a < D ? grid.origin[a] : 0.0;
     }
     cg.h = grid.h;
-    impm_material cm{static_cast<std::int32_t>(mat.kind), 0, mat.elastic.E, mat.elastic.nu, mat.kappa};
+    impm_material cm{static_cast<std::int32_t>(mat.kind), 0, mat.elastic.E, mat.elastic.nu, mat.kappa, 30.0, 0.0};
     const impm_options co = detail::to_c(options);
     detail::check(impm_sim_create(&cg, &cm, &co, device, &h_), nullptr);
   }

@@ -434,7 +434,11 @@ __device__ __forceinline__ void for_each_support(const GridC& g, const int* firs
 struct MatParams {
   int kind;
   double lam, mu, kappa;
+  double dp_alpha;  // Drucker-Prager sqrt(2/3) 2 sin(phi) / (3 - sin(phi))
+  double dp_ec;     // apex strain shift 3 c / (3 lam + 2 mu)
 };
+
+__host__ __device__ __forceinline__ bool has_history(int kind) { return kind == kHenckyJ2 || kind == kDruckerPrager; }
 
 // update_stress (mpm_solver.hpp:445-454) over scalar T
 template <class T, int D>
@@ -445,6 +449,7 @@ __device__ __forceinline__ StressOut<T> update_stress(const MatParams& mp, const
   if (mp.kind == kNeoHookean) return neo_hookean_update<T, D>(F_new, lam, mu);
   if constexpr (D <= 2) {
     if (mp.kind == kHencky) return hencky_update<T, D>(F_new, lam, mu);
+    if (mp.kind == kDruckerPrager) return dp_update<T, D>(F_new, f_inc, Be_n, lam, mu, mp.dp_alpha, mp.dp_ec, Be_out, dg_out);
     return j2_update<T, D>(f_inc, Be_n, lam, mu, mp.kappa, Be_out, dg_out);
   }
   return neo_hookean_update<T, D>(F_new, lam, mu);
@@ -493,7 +498,7 @@ __global__ void k_residual_particles(GridC g, const double* __restrict__ pd, int
     return;
   }
   double Be_n[9];
-  if (mp.kind == kHenckyJ2)
+  if (has_history(mp.kind))
 #pragma unroll
     for (int i = 0; i < 9; ++i) Be_n[i] = pd[(PF<D>::Be + i) * cap + p];
   const StressOut<double> su = update_stress<double, D>(mp, F_new, f_inc, Be_n);
@@ -685,7 +690,7 @@ __global__ void k_tangent(GridC g, const double* __restrict__ pd, int64_t cap, i
 #pragma unroll
   for (int i = 0; i < DD; ++i) Fn[i] = pd[(PF<D>::F + i) * cap + p];
   double Be_n[9];
-  if (mp.kind == kHenckyJ2)
+  if (has_history(mp.kind))
 #pragma unroll
     for (int i = 0; i < 9; ++i) Be_n[i] = pd[(PF<D>::Be + i) * cap + p];
   const double V0 = pd[PF<D>::V0 * cap + p];
@@ -1136,6 +1141,32 @@ __global__ void __launch_bounds__(WARPS * 32) k_assemble_bins_staged(
   }
 }
 
+// Block inverse for the smoother / block-Jacobi preconditioner, safeguarded:
+// a free component can carry an exactly zero diagonal (a lone particle with
+// dw = 0 at that node), making the block singular; then fall back to the
+// inverse of the positive diagonal entries (0 for a zero diagonal).
+template <int F>
+__device__ __forceinline__ Mat<double, F> safe_block_inverse(const Mat<double, F>& Mb) {
+  double mx = 0.0;
+#pragma unroll
+  for (int i = 0; i < F * F; ++i) mx = fmax(mx, fabs(Mb.e[i]));
+  const double d = det(Mb);
+  double tol = 1e-13;
+#pragma unroll
+  for (int i = 0; i < F; ++i) tol *= mx;
+  if (fabs(d) > tol && isfinite(d)) {
+    const Mat<double, F> Mi = inverse(Mb);
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < F * F; ++i) ok = ok && isfinite(Mi.e[i]);
+    if (ok) return Mi;
+  }
+  Mat<double, F> Mi = Mat<double, F>::zero();
+#pragma unroll
+  for (int c = 0; c < F; ++c) Mi(c, c) = Mb(c, c) > 0.0 ? 1.0 / Mb(c, c) : 0.0;
+  return Mi;
+}
+
 // masked diagonal block inverse per row (block-Jacobi / MG smoother)
 template <int D, int F = D>
 __global__ void k_diag_inverse(int n_act, const int* __restrict__ act_list, const uint8_t* __restrict__ freem,
@@ -1160,7 +1191,7 @@ __global__ void k_diag_inverse(int n_act, const int* __restrict__ act_list, cons
       const bool fr = freem[static_cast<int64_t>(k) * F + c] && freem[static_cast<int64_t>(k) * F + d];
       Mb(c, d) = (has && fr) ? rv[c * cp + d] : (c == d ? 1.0 : 0.0);
     }
-  const Mat<double, F> Mi = inverse(Mb);
+  const Mat<double, F> Mi = safe_block_inverse<F>(Mb);
 #pragma unroll
   for (int i = 0; i < DD; ++i) dinv[static_cast<int64_t>(row) * DD + i] = Mi.e[i];
 }
@@ -1842,7 +1873,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_galerkin_ptap(GridC gf, GridC gc
         for (int c = 0; c < F; ++c)
 #pragma unroll
           for (int d = 0; d < F; ++d) Mb(c, d) = (fr[c] && fr[d]) ? acc[t][c * F + d] : (c == d ? 1.0 : 0.0);
-        const Mat<double, F> Mi = inverse(Mb);
+        const Mat<double, F> Mi = safe_block_inverse<F>(Mb);
 #pragma unroll
         for (int e2 = 0; e2 < FF; ++e2) c_dinv[static_cast<int64_t>(row) * FF + e2] = Mi.e[e2];
       }
@@ -2056,7 +2087,7 @@ __global__ void k_commit(GridC g, double* __restrict__ pd, int64_t cap, int P, c
     F_new = matmul(f_inc, Fn);
   }
   double Be_n[9], Be_new[9], dg = 0.0;
-  if (mp.kind == kHenckyJ2)
+  if (has_history(mp.kind))
 #pragma unroll
     for (int i = 0; i < 9; ++i) Be_n[i] = pd[(PF<D>::Be + i) * cap + p];
   const StressOut<double> su = update_stress<double, D>(mp, F_new, f_inc, Be_n, Be_new, &dg);
@@ -2072,7 +2103,7 @@ __global__ void k_commit(GridC g, double* __restrict__ pd, int64_t cap, int P, c
   pd[PF<D>::V * cap + p] = su.J * pd[PF<D>::V0 * cap + p];
 #pragma unroll
   for (int i = 0; i < 9; ++i) pd[(PF<D>::sigma + i) * cap + p] = su.sigma.e[i];
-  if (mp.kind == kHenckyJ2) {
+  if (has_history(mp.kind)) {
 #pragma unroll
     for (int i = 0; i < 9; ++i) pd[(PF<D>::Be + i) * cap + p] = Be_new[i];
     pd[PF<D>::alpha * cap + p] += dg;

@@ -327,7 +327,7 @@ __device__ __forceinline__ void gimp_support_1d(double x, double lp, double orig
 }
 
 // ---------------------------------------------------------- constitutive --
-enum MaterialKind : int { kHencky = 0, kHenckyJ2 = 1, kNeoHookean = 2 };
+enum MaterialKind : int { kHencky = 0, kHenckyJ2 = 1, kNeoHookean = 2, kDruckerPrager = 3 };
 
 template <class T>
 struct StressOut {
@@ -557,6 +557,76 @@ IMPM_HD StressOut<T> j2_update(const Mat<T, D>& f_incr, const double* Be_n /*3x3
       if (i == j) tau += p_tau;
       out.sigma(i, j) = tau / J;
     }
+  return out;
+}
+
+// Drucker-Prager on Hencky strain, plane strain / uniaxial (D <= 2), with a
+// non-associative return (Klar et al. 2016): extension -> tip projection
+// (eps = 0); otherwise dgamma = |dev eps| + (3 lam + 2 mu)/(2 mu) tr(eps)
+// alpha, radial return of the deviator when dgamma > 0. Extension beyond the
+// reference (parity unpinned): no DP in /root/reference.
+// J = det(F_new) (plastic flow is not isochoric here). B_e = exp(2 eps_e).
+template <class T, int D>
+IMPM_HD StressOut<T> dp_update(const Mat<T, D>& F_new, const Mat<T, D>& f_incr, const double* Be_n, const T& lam,
+                               const T& mu, double alpha, double e_c, double* Be_out = nullptr,
+                               double* dgamma_out = nullptr) {
+  const Mat<T, 3> f3 = embed_F<T, D>(f_incr);
+  Mat<T, 3> Ben;
+#pragma unroll
+  for (int i = 0; i < 9; ++i) Ben.e[i] = T(Be_n[i]);
+  const Mat<T, 3> b_tr = matmul(matmul(f3, Ben), transpose(f3));
+  const Mat<T, 3> eps_tr = scale3(0.5, embedded_sym_log<T, D>(b_tr));
+  const T tr = trace(eps_tr);
+  Mat<T, 3> dev = eps_tr;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) dev(i, i) -= tr * (1.0 / 3.0);
+  T s2 = T(0.0);
+#pragma unroll
+  for (int i = 0; i < 9; ++i) s2 += dev.e[i] * dev.e[i];
+  const T dnorm = dsqrt(s2 + 1e-300);
+  Mat<T, 3> eps = eps_tr;
+  double dg = 0.0;
+  // the stress-free apex (eps = 0 exactly) stays elastic so the initial
+  // tangent is the elastic one; strict thresholds in strain units
+  // cohesion shifts the apex to tr = e_c (mean Kirchhoff stress = cohesion)
+  if (value_of(tr) > e_c + 1e-14) {  // extension: project to the cone tip
+    eps = Mat<T, 3>::zero();
+#pragma unroll
+    for (int i = 0; i < 3; ++i) eps(i, i) = T(e_c / 3.0);
+    T e2 = T(0.0);
+#pragma unroll
+    for (int i = 0; i < 9; ++i) e2 += (eps_tr.e[i] - eps.e[i]) * (eps_tr.e[i] - eps.e[i]);
+    dg = value_of(dsqrt(e2 + 1e-300));
+  } else {
+    const T gam = dnorm + (3.0 * lam + 2.0 * mu) / (2.0 * mu) * (tr - e_c) * alpha;
+    if (value_of(gam) > 1e-14) {
+      const T sc = gam / dnorm;
+#pragma unroll
+      for (int i = 0; i < 9; ++i) eps.e[i] = eps_tr.e[i] - sc * dev.e[i];
+      dg = value_of(gam);
+    }
+  }
+  const T tre = trace(eps);
+  const T J = det(F_new);
+  StressOut<T> out;
+  out.J = J;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      T tau = 2.0 * mu * eps(i, j);
+      if (i == j) tau += lam * tre;
+      out.sigma(i, j) = tau / J;
+    }
+  if (Be_out) {
+    Mat<double, 3> e2;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) e2.e[i] = 2.0 * value_of(eps.e[i]);
+    const Mat<double, 3> Be = embedded_sym_exp<double, D>(e2);
+#pragma unroll
+    for (int i = 0; i < 9; ++i) Be_out[i] = Be.e[i];
+    *dgamma_out = dg;
+  }
   return out;
 }
 

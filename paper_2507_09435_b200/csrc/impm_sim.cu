@@ -259,6 +259,9 @@ struct Sim {
     m.lam = E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu));  // materials.hpp:16-17
     m.mu = E / (2.0 * (1.0 + nu));
     m.kappa = mat.kappa;
+    const double sphi = std::sin(mat.friction_deg * M_PI / 180.0);
+    m.dp_alpha = std::sqrt(2.0 / 3.0) * 2.0 * sphi / (3.0 - sphi);
+    m.dp_ec = 3.0 * mat.cohesion / (3.0 * m.lam + 2.0 * m.mu);
     return m;
   }
 
@@ -321,8 +324,10 @@ struct Sim {
     mat = *m;
     if (!(mat.E > 0.0)) throw SimError(IMPM_ERR_CONFIG, "Young's modulus must be positive");
     if (!(mat.nu > -1.0 && mat.nu < 0.5)) throw SimError(IMPM_ERR_CONFIG, "Poisson's ratio must lie in (-1, 0.5)");
-    if (mat.kind != kHencky && mat.kind != kHenckyJ2 && mat.kind != kNeoHookean)
+    if (mat.kind != kHencky && mat.kind != kHenckyJ2 && mat.kind != kNeoHookean && mat.kind != kDruckerPrager)
       throw SimError(IMPM_ERR_CONFIG, "unknown material kind");
+    if (mat.kind == kDruckerPrager && !(mat.friction_deg > 0.0 && mat.friction_deg < 90.0))
+      throw SimError(IMPM_ERR_CONFIG, "Drucker-Prager friction angle must lie in (0, 90) degrees");
     if (D == 3 && mat.kind != kNeoHookean)  // mpm_solver.hpp:448-453
       throw SimError(IMPM_ERR_CONFIG, "material kind not available in 3D");
     if (mat.kind == kHenckyJ2 && !(mat.kappa > 0.0)) throw SimError(IMPM_ERR_CONFIG, "yield strength must be positive");
@@ -334,7 +339,7 @@ struct Sim {
     if (!(opt.abs_floor >= 0.0)) opt.abs_floor = 1e-14;
     if (!(opt.krylov_rtol > 0.0)) opt.krylov_rtol = 1e-12;
     shape = opt.shape == IMPM_SHAPE_BSPLINE2 ? 2 : 1;
-    if (!coupled && opt.total_lagrangian && mat.kind == kHenckyJ2)  // mpm_solver.hpp:66-67
+    if (!coupled && opt.total_lagrangian && has_history(mat.kind))  // mpm_solver.hpp:66-67
       throw SimError(IMPM_ERR_CONFIG, "total-Lagrangian stepping supports elastic materials only");
     prof.on = opt.profile != 0;
   }
@@ -454,6 +459,9 @@ struct Sim {
     field_of.ensure(NF());
     for (auto* v : {&u, &r, &delta, &utry, &rtry, &prev, &tmp1, &tmp2, &kx, &kr, &kz, &kp, &kq, &kv, &ks, &kt, &khat})
       v->ensure(NF());
+    // work vectors are only ever written at active rows: keep the rest zero
+    for (auto* v : {&delta, &utry, &rtry, &tmp1, &tmp2, &kx, &kr, &kz, &kp, &kq, &kv, &ks, &kt, &khat})
+      CK(cudaMemsetAsync(v->p, 0, sizeof(double) * NF(), s));
     {
       Prof::Scope ps(&prof, kcSort);
       dispatch([&](auto Dc, auto Sc) {
@@ -1186,6 +1194,9 @@ struct Sim {
     if (mgp) mg_setup<DD, FE>();
     CK(cudaMemsetAsync(dflag.p, 0, sizeof(int), s));
     gm_V.ensure(static_cast<size_t>(m + 1) * n);
+    // SpMV / preconditioners write active rows only: the basis must start at
+    // zero so inactive entries never carry stale memory into the dots
+    CK(cudaMemsetAsync(gm_V.p, 0, sizeof(double) * static_cast<size_t>(m + 1) * n, s));
     CK(cudaMemsetAsync(x, 0, sizeof(double) * n, s));
     const double bnorm = std::sqrt(dot_sync(b, b));
     if (bnorm == 0.0) return 0;
@@ -1268,18 +1279,23 @@ struct Sim {
     int out = 0;
     dispatch_df([&](auto Dc, auto Fc) {
       constexpr int DD = decltype(Dc)::value, FE = decltype(Fc)::value;
-      const bool mgp = opt.precond == IMPM_PRECOND_MG && !coupled;  // u-p: block Jacobi (saddle point)
-      if (!coupled && opt.krylov != IMPM_KRYLOV_BICGSTAB) {
+      // non-associative Drucker-Prager flow gives a nonsymmetric J -> GMRES;
+      // MG right-preconditions GMRES for DP; the u-p saddle point uses block Jacobi
+      const bool nonsym = coupled || mat.kind == kDruckerPrager;
+      const bool mgp = opt.precond == IMPM_PRECOND_MG && !coupled;
+      if (!nonsym && opt.krylov != IMPM_KRYLOV_BICGSTAB && opt.krylov != IMPM_KRYLOV_GMRES) {
         const int it = mgp ? cg_mg_solve<DD, FE>(rhs, x) : cg_solve<FE>(rhs, x);
         if (it >= 0) {
           out = it;
           return;
         }
         if (opt.krylov == IMPM_KRYLOV_CG) throw SimError(IMPM_ERR_LINEAR_SOLVER, "CG breakdown: J not SPD");
-        out = -it - 1 + bicgstab_solve<DD, FE>(rhs, x, mgp);
+        // p.Jp <= 0: J is indefinite or numerically singular (fringe nodes
+        // carrying ~1e-14 of the bulk stiffness) -> GMRES, same preconditioner
+        out = -it - 1 + gmres_solve<DD, FE>(rhs, x, mgp);
         return;
       }
-      if (coupled || opt.krylov == IMPM_KRYLOV_GMRES) {
+      if (nonsym || opt.krylov == IMPM_KRYLOV_GMRES) {
         out = gmres_solve<DD, FE>(rhs, x, mgp);
         return;
       }
@@ -1709,7 +1725,7 @@ impm_status impm_coupled_create(const impm_grid* grid, const impm_poro* poro, co
                                 impm_sim** out) {
   if (!grid || !poro || !opt || !out) return IMPM_ERR_CONFIG;
   try {
-    impm_material dummy{IMPM_NEO_HOOKEAN, 0, 1.0, 0.0, 0.0};
+    impm_material dummy{IMPM_NEO_HOOKEAN, 0, 1.0, 0.0, 0.0, 30.0, 0.0};
     *out = reinterpret_cast<impm_sim*>(new Sim(grid, &dummy, opt, device, poro));
     return IMPM_OK;
   } catch (const SimError& e) {

@@ -71,6 +71,28 @@ def column2d_nh(cells=64, ppc=2, h=1.0, steps=10):
                    np.array([0.0, -9.81]), steps, note="GIMP transfer (pinned); B-spline variant unpinned")
 
 
+def slope2d(cells=(256, 128), ppc=4, h=0.5, steps=20, friction_deg=30.0, E=10e6, nu=0.3, material="drucker_prager",
+            slope_deg=45.0, kappa=20e3, cohesion=0.0):
+    """cfg 2: 2D granular slope collapse, 256x128 cells, ppc 4 (~0.5 M
+    particles). Drucker-Prager is an extension (parity unpinned); the pinned
+    substitute of SURVEY.md §8(d) is hencky_j2 (pass material="hencky_j2").
+    Body = seed_box filtered by y <= (x - x_toe) tan(beta) up to the crest,
+    base fixed, lateral rollers, gravity ramped over `steps` increments."""
+    W, H = cells[0] * h, cells[1] * h
+    grid = GridSpec(2, (-h, -h), h, (cells[0] + 3, cells[1] + 3))
+    parts = seed_box(grid, (0.0, 0.0), (W, H), ppc, 2000.0)
+    pa = ParticleArray(parts, 2)
+    x_toe = W - H / np.tan(np.radians(slope_deg))
+    keep = pa.X[:, 1] <= np.maximum(0.25 * H, (W - pa.X[:, 0]) * np.tan(np.radians(slope_deg)) + 0.0 * x_toe)
+    parts = np.ascontiguousarray(parts[keep])
+    mat = MaterialSpec(material, ElasticParams(E, nu), kappa if material == "hencky_j2" else 0.0, friction_deg,
+                       cohesion)
+    return Problem("cfg2_slope2d_" + material, grid, parts, mat, SolverOptions(tol=1e-10),
+                   _column_fixed(grid, (W, H)), np.array([0.0, -9.81]), steps,
+                   note=("Drucker-Prager (extension, parity unpinned)" if material == "drucker_prager"
+                         else "hencky_j2 pinned substitute for Drucker-Prager"))
+
+
 def footing3d(cells=(128, 128, 64), ppc=2, h=0.5, steps=20, t_hat=100e3, frac=0.125, E=10e6, nu=0.3):
     """cfg 4 / cfg 5 slab: 3D strip footing, 128x128x64 cells, ppc 2 (8,388,608
     particles). Modified Cam-Clay is absent from the reference: the pinned
@@ -89,5 +111,5 @@ def footing3d(cells=(128, 128, 64), ppc=2, h=0.5, steps=20, t_hat=100e3, frac=0.
 
 
 def by_name(name, **kw):
-    table = {"cfg1": column2d_nh, "cfg4": footing3d, "cfg5": footing3d}
+    table = {"cfg1": column2d_nh, "cfg2": slope2d, "cfg4": footing3d, "cfg5": footing3d}
     return table[name](**kw)
