@@ -326,6 +326,47 @@ __global__ void k_act_finalize(int N, const int* __restrict__ act_flag, const in
   }
 }
 
+// Row order of the box-BSR: brick-major (4^D node bricks, flat order of bricks
+// and of nodes inside a brick). A CTA's chunk of 64 rows is then one 4x4x4
+// brick whose SpMV x-neighbourhood (8^3 nodes, 12 KB) stays in L1. Row order
+// is internal: DOF numbering, grid vectors and exports are node-indexed.
+template <int D>
+__device__ __forceinline__ int brick_pos(const GridC& g, const int* idx) {
+  int p = 0, l = 0;
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    const int nb = (g.nodes[a] + 3) >> 2;
+    p = p * nb + (idx[a] >> 2);
+    l = l * 4 + (idx[a] & 3);
+  }
+  return (p << (2 * D)) | l;
+}
+
+template <int D>
+__global__ void k_brick_flags(GridC g, const int* __restrict__ act_flag, int* __restrict__ bflags) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= g.N) return;
+  int idx[3];
+  unflat<D>(g, n, idx);
+  bflags[brick_pos<D>(g, idx)] = act_flag[n];
+}
+
+template <int D>
+__global__ void k_act_finalize_brick(GridC g, const int* __restrict__ act_flag, const int* __restrict__ bscan,
+                                     int* __restrict__ act_idx, int* __restrict__ act_list) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= g.N) return;
+  if (act_flag[n]) {
+    int idx[3];
+    unflat<D>(g, n, idx);
+    const int r = bscan[brick_pos<D>(g, idx)];
+    act_idx[n] = r;
+    act_list[r] = n;
+  } else {
+    act_idx[n] = -1;
+  }
+}
+
 // ------------------------------------------------------ block reductions --
 template <int NV>
 __device__ __forceinline__ void block_sum_store(double (&v)[NV], double* __restrict__ partials) {
