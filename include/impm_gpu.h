@@ -203,6 +203,58 @@ impm_status impm_sim_kernel_times(impm_sim* sim, const char** names, double* ms,
 /* Bytes of the stored BSR (values) and algorithmic per-launch traffic figures. */
 impm_status impm_sim_matrix_info(impm_sim* sim, int64_t* n_rows, int64_t* row_values, int64_t* ref_nnz);
 
+/* ---------------------------------------------------------------------------
+ * Slab decomposition along grid axis 0 (multi-GPU, one rank per GPU).
+ *
+ * Replaces nothing in the reference, which is single-process
+ * (mpm_solver.hpp:56-477); this is the "multi-GPU create variant" of
+ * SURVEY.md §8(b)/(e). Axis 0 is the slowest index of Grid::flat
+ * (grid.hpp:30-34) and DofMap::build numbers nodes in ascending flat order
+ * (grid.hpp:76-85), so rank r owns the node planes [cuts[r], cuts[r+1]), a
+ * contiguous range of global DOFs and Jacobian rows. Its simulation is
+ * created on the LOCAL grid {global origin, h, nodes[0] = hi - lo, other
+ * axes global} with [lo, hi) = [max(0, cuts[r]-2), min(n0, cuts[r+1]+2)), and
+ * holds its owned particles plus the ghost particles whose first support node
+ * lies in [cuts[r]-2, cuts[r]). Per Newton iteration the ranks exchange a
+ * 2-plane vector halo before each SpMV / residual and sum the reduction
+ * partials of every dot product; the MG preconditioner is rank-local (block
+ * Jacobi across slabs). All calls on a slab simulation are collective over
+ * the communicator: every rank makes the same sequence of calls.
+ * ------------------------------------------------------------------------- */
+typedef struct impm_comm impm_comm; /* opaque communicator (NCCL or in-process) */
+
+/* NCCL: rank 0 creates the unique id (cap >= 128 bytes), ships it to the
+ * other ranks out of band (e.g. torch.distributed broadcast), then every
+ * rank creates its communicator on its own device. */
+impm_status impm_comm_nccl_id(uint8_t* id, int32_t cap);
+impm_status impm_comm_nccl_create(const uint8_t* id, int32_t rank, int32_t nranks, int32_t device, impm_comm** out);
+/* In-process group: `nranks` communicators for ranks driven by host threads
+ * of one process on one device (host-ordered collectives; test transport). */
+impm_status impm_comm_local_group(int32_t nranks, int32_t device, impm_comm** out /* [nranks] */);
+impm_status impm_comm_destroy(impm_comm* comm);
+impm_status impm_comm_info(impm_comm* comm, int32_t* rank, int32_t* nranks, const char** kind);
+
+/* Attach the slab decomposition: global node count along axis 0 and the
+ * ownership cuts [nranks + 1] (cuts[0] = 0, cuts[nranks] = n0, every slab
+ * >= 4 planes when nranks > 1). Single-field MpmSim only. */
+impm_status impm_sim_set_slab(impm_sim* sim, impm_comm* comm, int32_t global_n0, const int32_t* cuts);
+/* Particles with their global ids (the single-GPU AoS index; < 2^29). */
+impm_status impm_sim_set_particles_ids(impm_sim* sim, const double* aos, const int64_t* ids, int64_t n,
+                                       int64_t stride_bytes);
+/* Local particles (owned + ghost copies) in local order with their ids. */
+impm_status impm_sim_get_particles_ids(impm_sim* sim, double* aos, int64_t* ids, int64_t n, int64_t stride_bytes);
+/* After commit_step: send owned particles to the rank(s) that keep them for
+ * the next step (impm_sim_step does this itself on a slab). */
+impm_status impm_sim_migrate(impm_sim* sim);
+/* Global free-DOF count, this rank's first global DOF (the local DofMap of
+ * the owned nodes is the global one shifted by it), global axis-0 index of
+ * local node 0. */
+impm_status impm_sim_slab_info(impm_sim* sim, int64_t* n_dofs_global, int64_t* dof_offset, int32_t* base0);
+/* Parity tap: assemble J(u) (u = local free-DOF vector) and y = J x in grid
+ * layout [N*D] of the local grid (owned rows; halo columns from the
+ * neighbours). */
+impm_status impm_sim_apply_jacobian(impm_sim* sim, const double* u, double load_scale, const double* x, double* y);
+
 #ifdef __cplusplus
 }
 #endif

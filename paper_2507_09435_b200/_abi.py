@@ -108,6 +108,18 @@ _SIGNATURES = {
     "impm_sim_last_error": (c_int32, [c_void_p, ctypes.c_char_p, ctypes.c_size_t, c_void_p, _P(c_int32)]),
     "impm_sim_kernel_times": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, _P(c_int32), c_int32]),
     "impm_sim_matrix_info": (c_int32, [c_void_p, _P(c_int64), _P(c_int64), _P(c_int64)]),
+    # slab decomposition
+    "impm_comm_nccl_id": (c_int32, [c_void_p, c_int32]),
+    "impm_comm_nccl_create": (c_int32, [c_void_p, c_int32, c_int32, c_int32, _P(c_void_p)]),
+    "impm_comm_local_group": (c_int32, [c_int32, c_int32, c_void_p]),
+    "impm_comm_destroy": (c_int32, [c_void_p]),
+    "impm_comm_info": (c_int32, [c_void_p, _P(c_int32), _P(c_int32), _P(ctypes.c_char_p)]),
+    "impm_sim_set_slab": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p]),
+    "impm_sim_set_particles_ids": (c_int32, [c_void_p, c_void_p, c_void_p, c_int64, c_int64]),
+    "impm_sim_get_particles_ids": (c_int32, [c_void_p, c_void_p, c_void_p, c_int64, c_int64]),
+    "impm_sim_migrate": (c_int32, [c_void_p]),
+    "impm_sim_slab_info": (c_int32, [c_void_p, _P(c_int64), _P(c_int64), _P(c_int32)]),
+    "impm_sim_apply_jacobian": (c_int32, [c_void_p, c_void_p, c_double, c_void_p, c_void_p]),
 }
 
 # every symbol include/impm_gpu.h declares (checked by tests without a GPU)

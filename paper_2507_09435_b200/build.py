@@ -18,6 +18,21 @@ FLAGS = [
 ]
 
 
+def nccl_flags():
+    """NCCL of the torch wheel (2.28; the same libnccl.so.2 torch.distributed
+    loads, so one copy is mapped per process), else the system one."""
+    try:
+        import nvidia.nccl as nn
+        root = list(nn.__path__)[0]
+    except ImportError:
+        root = None
+    if root and os.path.exists(os.path.join(root, "include", "nccl.h")):
+        lib = os.path.join(root, "lib")
+        return ["-I" + os.path.join(root, "include"), "-L" + lib, "-l:libnccl.so.2",
+                "-Xlinker", "-rpath=" + lib]
+    return ["-lnccl"]
+
+
 def sources():
     return [os.path.join(HERE, "csrc", f) for f in sorted(os.listdir(os.path.join(HERE, "csrc")))] + \
         [os.path.join(os.path.dirname(HERE), "include", "impm_gpu.h")]
@@ -33,7 +48,7 @@ def up_to_date():
 def build(force=False, verbose=False):
     if not force and up_to_date():
         return OUT
-    cmd = [NVCC, *FLAGS, "-o", OUT, SRC]
+    cmd = [NVCC, *FLAGS, "-o", OUT, SRC, *nccl_flags()]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)

@@ -45,6 +45,10 @@ struct GridC {
   double origin[3];
   double h;
   int N;
+  // global axis-0 index of local node 0 (slab decomposition): node positions
+  // and supports stay relative to the GLOBAL origin, so a slab computes the
+  // same fp64 weights, bit for bit, as the single-GPU grid
+  int base0;
 };
 
 template <int D>
@@ -54,7 +58,8 @@ __device__ __forceinline__ void unflat(const GridC& g, int n, int* idx) {
 }
 
 __device__ __forceinline__ double node_coord(const GridC& g, int a, int i) {
-  return __dadd_rn(g.origin[a], __dmul_rn(static_cast<double>(i), g.h));  // grid.hpp:180-185
+  const int gi = a == 0 ? i + g.base0 : i;
+  return __dadd_rn(g.origin[a], __dmul_rn(static_cast<double>(gi), g.h));  // grid.hpp:180-185
 }
 
 // packed support counts: 2 bits per axis
@@ -121,7 +126,7 @@ struct DevStatus {
   int err_cfg;        // min original id with lp outside (0, h/2)
   int perm_moved;     // counting sort moved at least one particle
   int err_lp;         // commit: min original id with lp >= h/2 or <= 0
-  int pad;
+  int err_migrate;    // slab migration: min original id that left the neighbour slabs
 };
 
 template <int D, int SHAPE>
@@ -147,6 +152,7 @@ __global__ void k_support(const double* __restrict__ pd, int64_t cap, int P, Gri
     } else {
       gimp_support_1d(x, lp, g.origin[a], g.h, first, count);
     }
+    if (a == 0) first -= g.base0;
     if (ok && (first < 0 || first + count > g.nodes[a])) {
       atomicMin(&st->err_ood, orig[i] * 4 + a);  // mpm_solver.hpp:105-110
       ok = false;
@@ -2645,6 +2651,94 @@ __global__ void k_scan_add(T* __restrict__ out, int64_t n, const T* __restrict__
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) out[i] += sums[i / 4096];
   if (i == 0 && out_total_slot) *out_total_slot = *total;
+}
+
+// ------------------------------------------------- slab decomposition (§8e) --
+// Nodes outside the owned axis-0 range [own_lo, own_hi) are neither rows nor
+// DOFs of this rank: their activity and freedom belong to the owner.
+__global__ void k_mask_owned(int N, int F, int stride0, int own_lo, int own_hi, int* __restrict__ act_flag,
+                             int* __restrict__ free_flag) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  const int i0 = n / stride0;
+  if (i0 >= own_lo && i0 < own_hi) return;
+  act_flag[n] = 0;
+  for (int c = 0; c < F; ++c) free_flag[n * F + c] = 0;
+}
+
+// Destinations of every particle this rank OWNED during the step (first
+// support node along axis 0 in [own_lo, own_hi) at begin_step) from its
+// committed position: rank r keeps f in [A-2, B); r-1 needs f < A; r+1 needs
+// f >= B-2 (f = new global first support node). Ghost copies are dropped.
+template <int D, int SHAPE>
+__global__ void k_migrate_flags(const double* __restrict__ pd, int64_t cap, int P, GridC g,
+                                const int* __restrict__ key, int use_X, int own_lo, int own_hi, int A, int B,
+                                int has_left, int has_right, int lo_ok, int hi_ok, const int* __restrict__ orig,
+                                int* __restrict__ fk, int* __restrict__ fl, int* __restrict__ fr, DevStatus* st) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  const int f0 = key[i] / g.stride[0];
+  int k = 0, l = 0, r = 0;
+  if (f0 >= own_lo && f0 < own_hi) {
+    const double x = pd[((use_X ? PF<D>::X : PF<D>::x) + 0) * cap + i];
+    const double lp = pd[(PF<D>::lp + 0) * cap + i];
+    int first, count;
+    if constexpr (SHAPE == 2) {
+      const double lo = __dsub_rn(__dsub_rn(x, g.origin[0]), 1.5 * g.h);
+      first = static_cast<int>(floor(__ddiv_rn(lo, g.h))) + 1;
+    } else {
+      gimp_support_1d(x, lp, g.origin[0], g.h, first, count);
+    }
+    k = (!has_left || first >= A - 2) && (!has_right || first < B);
+    l = has_left && first < A;
+    r = has_right && first >= B - 2;
+    if (first < lo_ok || first >= hi_ok) atomicMin(&st->err_migrate, orig[i]);
+  }
+  fk[i] = k;
+  fl[i] = l;
+  fr[i] = r;
+}
+
+// record = nd particle doubles + the global id (exact in fp64)
+__global__ void k_pack_records(const double* __restrict__ pd, int64_t cap, int P, int nd,
+                               const int* __restrict__ orig, const int* __restrict__ flag,
+                               const int* __restrict__ pos, double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P || !flag[i]) return;
+  const int64_t o = static_cast<int64_t>(pos[i]) * (nd + 1);
+  for (int f = 0; f < nd; ++f) out[o + f] = pd[f * cap + i];
+  out[o + nd] = static_cast<double>(orig[i]);
+}
+
+__global__ void k_unpack_records(const double* __restrict__ in, int n, int nd, double* __restrict__ pd,
+                                 int64_t cap, int off, int* __restrict__ orig) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int64_t o = static_cast<int64_t>(j) * (nd + 1);
+  for (int f = 0; f < nd; ++f) pd[f * cap + off + j] = in[o + f];
+  orig[off + j] = static_cast<int>(in[o + nd]);
+}
+
+// stable compaction of the kept particles into the new SoA block at `off`
+__global__ void k_keep_gather(const double* __restrict__ pd, int64_t cap, int P, int nd,
+                              const int* __restrict__ orig, const int* __restrict__ flag,
+                              const int* __restrict__ pos, double* __restrict__ pd_new, int64_t cap_new, int off,
+                              int* __restrict__ orig_new) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P || !flag[i]) return;
+  const int j = off + pos[i];
+  for (int f = 0; f < nd; ++f) pd_new[f * cap_new + j] = pd[f * cap + i];
+  orig_new[j] = orig[i];
+}
+
+// local particles -> AoS in local (sorted) order + their global ids
+__global__ void k_soa_to_aos_ids(const double* __restrict__ soa, int64_t cap, int n, int nd,
+                                 const int* __restrict__ orig, double* __restrict__ aos, int64_t stride_dbl,
+                                 long long* __restrict__ ids) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int f = 0; f < nd; ++f) aos[static_cast<int64_t>(i) * stride_dbl + f] = soa[f * cap + i];
+  ids[i] = orig[i];
 }
 
 }  // namespace impm_gpu

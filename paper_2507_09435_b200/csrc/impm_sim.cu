@@ -20,6 +20,7 @@
 
 #include "../../include/impm_gpu.h"
 #include "impm_kernels.cuh"
+#include "impm_comm.cuh"
 
 using namespace impm_gpu;
 
@@ -217,6 +218,58 @@ struct Sim {
   // relative Krylov tolerance of the current solve (see newton_attempt)
   double cur_rtol = 1e-12;
 
+  // slab decomposition along axis 0; comm == nullptr or a
+  // single rank -> the plain single-GPU path
+  std::shared_ptr<Comm> comm;
+  bool slab = false;
+  int own_lo = 0, own_hi = 0;  // owned axis-0 node range, local indices
+  int glob_n0 = 0;
+  std::vector<int> cuts;       // global ownership cuts [nranks + 1]
+  int64_t n_dofs_glob = 0, dof_offset = 0;
+  DBuf<long long> slab_counts;
+  DBuf<int> mig_flag, mig_pos;
+  DBuf<double> mig_send_l, mig_send_r, mig_recv_l, mig_recv_r;
+  bool multi() const { return comm && comm->nranks > 1; }
+  int ndg() const { return static_cast<int>(std::min<int64_t>(n_dofs_glob, INT_MAX)); }
+  template <class Fn>
+  void comm_call(Fn&& fn) {
+    try {
+      fn();
+    } catch (const CommError& e) {
+      throw SimError(IMPM_ERR_NCCL, e.what());
+    }
+  }
+  // elementwise sum over ranks of reduction partials (then every rank's
+  // fixed-order finalize yields the same global value)
+  void gsum(double* d, size_t n) {
+    if (multi()) comm_call([&] { comm->allreduce(d, n, RedType::F64, RedOp::Sum, s); });
+  }
+  void gmin_int(int* d, size_t n) {
+    if (multi()) comm_call([&] { comm->allreduce(d, n, RedType::I32, RedOp::Min, s); });
+  }
+  // 2-plane halo of a grid-layout vector [node][F] along axis 0: my first /
+  // last two owned planes go to the neighbours, theirs fill my halo planes
+  void halo(const double* vc, int comps = -1) {
+    if (!multi()) return;
+    double* v = const_cast<double*>(vc);
+    const size_t plane = static_cast<size_t>(g.stride[0]) * (comps > 0 ? comps : F);
+    const size_t bytes = 2 * plane * sizeof(double);
+    std::vector<Comm::Msg> snd, rcv;
+    const int rk = comm->rank;
+    if (rk > 0) {
+      snd.push_back({rk - 1, v + own_lo * plane, bytes});
+      rcv.push_back({rk - 1, v + (own_lo - 2) * plane, bytes});
+    }
+    if (rk < comm->nranks - 1) {
+      snd.push_back({rk + 1, v + (own_hi - 2) * plane, bytes});
+      rcv.push_back({rk + 1, v + own_hi * plane, bytes});
+    }
+    comm_call([&] { comm->exchange(snd, rcv, s); });
+  }
+  // local colour-batch start along axis 0 for GLOBAL colour c0, so slabs push
+  // bins in the single-GPU batch order (bitwise-identical owned rows)
+  int colour0(int c0) const { return ((c0 - g.base0) % 3 + 3) % 3; }
+
   // controller state (mpm_solver.hpp:466-477)
   bool step_built = false;
   bool have_prev = false;
@@ -377,19 +430,9 @@ struct Sim {
     P = static_cast<int>(n);
     cap = std::max<int64_t>(P, 1);
     pd.ensure(cap * ND);
-    pd_tmp.ensure(cap * ND);
-    xs.ensure(cap * 3);
-    bext.ensure(cap * 3);
     orig.ensure(cap);
-    orig_tmp.ensure(cap);
-    key.ensure(cap);
-    sup.ensure(cap);
-    rank.ensure(cap);
-    perm.ensure(cap);
-    Pst.ensure(cap * std::max(D * D, 8));
-    uty.ensure(cap);
+    ensure_particle_buffers();
     CK(cudaMemsetAsync(uty.p, 0, sizeof(double) * cap, s));
-    Atan.ensure(cap * D * D * D * D);
     DBuf<double> staging;
     staging.ensure(std::max<int64_t>(1, n * (stride / 8)));
     if (n > 0) {
@@ -401,7 +444,22 @@ struct Sim {
     step_built = false;
     matrix_valid = false;
   }
+  // per-particle work arrays sized by `cap` (the SoA field stride)
+  void ensure_particle_buffers() {
+    pd_tmp.ensure(cap * ND);
+    xs.ensure(cap * 3);
+    bext.ensure(cap * 3);
+    orig_tmp.ensure(cap);
+    key.ensure(cap);
+    sup.ensure(cap);
+    rank.ensure(cap);
+    perm.ensure(cap);
+    Pst.ensure(cap * std::max(D * D, 8));
+    uty.ensure(cap);
+    Atan.ensure(cap * D * D * D * D);
+  }
   void get_particles(double* aos, int64_t n, int64_t stride) {
+    if (slab) throw SimError(IMPM_ERR_UNSUPPORTED, "a slab holds a subset of the particles: use get_particles_ids");
     if (n != P) throw SimError(IMPM_ERR_CONFIG, "particle count mismatch");
     if (stride % 8 != 0 || stride < ND * 8) throw SimError(IMPM_ERR_CONFIG, "bad particle stride");
     if (n == 0) return;
@@ -413,7 +471,186 @@ struct Sim {
     CK(cudaMemcpyAsync(aos, staging.p, n * stride, cudaMemcpyDeviceToHost, s));
     sync();
   }
+  // slab particles carry their global ids (= the single-GPU AoS index), used
+  // for error messages and as the identity of migrated particles
+  void set_particles_ids(const double* aos, const int64_t* ids, int64_t n, int64_t stride) {
+    set_particles(aos, n, stride);
+    if (n == 0) return;
+    std::vector<int> h(n);
+    for (int64_t i = 0; i < n; ++i) {
+      if (ids[i] < 0 || ids[i] > INT_MAX / 4) throw SimError(IMPM_ERR_CONFIG, "particle ids must lie in [0, 2^29)");
+      h[i] = static_cast<int>(ids[i]);
+    }
+    CK(cudaMemcpyAsync(orig.p, h.data(), sizeof(int) * n, cudaMemcpyHostToDevice, s));
+    sync();
+  }
+  // local particles (owned + ghost copies) in local order, with global ids
+  void get_particles_ids(double* aos, int64_t* ids, int64_t n, int64_t stride) {
+    if (n != P) throw SimError(IMPM_ERR_CONFIG, "particle count mismatch");
+    if (stride % 8 != 0 || stride < ND * 8) throw SimError(IMPM_ERR_CONFIG, "bad particle stride");
+    if (n == 0) return;
+    DBuf<double> staging;
+    DBuf<long long> dids;
+    staging.ensure(n * (stride / 8));
+    dids.ensure(n);
+    if (stride != ND * 8) CK(cudaMemsetAsync(staging.p, 0, n * stride, s));
+    k_soa_to_aos_ids<<<blocks_for(n), kThreads, 0, s>>>(pd.p, cap, P, ND, orig.p, staging.p, stride / 8, dids.p);
+    ++g_launches;
+    CKL();
+    CK(cudaMemcpyAsync(aos, staging.p, n * stride, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(ids, dids.p, sizeof(long long) * n, cudaMemcpyDeviceToHost, s));
+    sync();
+  }
+
+  // ---------------------------------------------------- slab decomposition
+  // The caller creates the Sim on the LOCAL grid: global origin, nodes[0] =
+  // hi - lo with [lo, hi) = [max(0, A - 2), min(n0, B + 2)) for the owned
+  // planes [A, B) = [cuts[rank], cuts[rank + 1]).
+  void set_slab(std::shared_ptr<Comm> c, int n0, const int* cuts_in) {
+    if (coupled) throw SimError(IMPM_ERR_UNSUPPORTED, "slab decomposition supports the single-field MpmSim only");
+    const int nr = c->nranks, rk = c->rank;
+    std::vector<int> cu(cuts_in, cuts_in + nr + 1);
+    if (cu[0] != 0 || cu[nr] != n0) throw SimError(IMPM_ERR_CONFIG, "slab cuts must span [0, n0]");
+    for (int q = 0; q < nr; ++q)
+      if (cu[q + 1] - cu[q] < (nr > 1 ? 4 : 1))
+        throw SimError(IMPM_ERR_CONFIG, "every slab needs at least 4 owned node planes along axis 0");
+    const int lo = std::max(0, cu[rk] - 2), hi = std::min(n0, cu[rk + 1] + 2);
+    if (g.nodes[0] != hi - lo)
+      throw SimError(IMPM_ERR_CONFIG, "slab grid must hold the owned planes plus a 2-plane halo: nodes[0] = " +
+                                          std::to_string(hi - lo));
+    g.base0 = lo;
+    own_lo = cu[rk] - lo;
+    own_hi = cu[rk + 1] - lo;
+    glob_n0 = n0;
+    cuts = cu;
+    comm = std::move(c);
+    slab = true;
+    step_built = false;
+    matrix_valid = false;
+  }
+
+  // After commit_step: every owned particle goes to the rank(s) that keep it
+  // for the next step (owner + the neighbour that needs it as a ghost),
+  // ghost copies are dropped; the new local array is [from left | kept |
+  // from right], i.e. the global sorted order restricted to this slab, so
+  // the stable bin sort reproduces the single-GPU particle order per bin.
+  void migrate() {
+    if (!slab) throw SimError(IMPM_ERR_CONFIG, "migrate on a simulation without a slab decomposition");
+    if (!multi() || opt.total_lagrangian) return;  // TL supports never move (support on X)
+    const int rk = comm->rank, nr = comm->nranks;
+    const bool hl = rk > 0, hr = rk < nr - 1;
+    const int A = cuts[rk], B = cuts[rk + 1];
+    const int lo_ok = hl ? cuts[rk - 1] : INT_MIN;
+    const int hi_ok = hr ? (rk + 2 < nr ? cuts[rk + 2] - 2 : glob_n0) : INT_MAX;
+    mig_flag.ensure(3 * cap);
+    mig_pos.ensure(3 * (cap + 1));
+    int* fk = mig_flag.p;
+    int* fl = mig_flag.p + cap;
+    int* fr = mig_flag.p + 2 * cap;
+    int* pk = mig_pos.p;
+    int* pl = mig_pos.p + (cap + 1);
+    int* pr = mig_pos.p + 2 * (cap + 1);
+    const int big = INT_MAX;
+    CK(cudaMemcpyAsync(&st.p->err_migrate, &big, sizeof(int), cudaMemcpyHostToDevice, s));
+    if (P > 0) {
+      dispatch([&](auto Dc, auto Sc) {
+        constexpr int DD = decltype(Dc)::value, SH = decltype(Sc)::value;
+        k_migrate_flags<DD, SH><<<blocks_for(P), kThreads, 0, s>>>(pd.p, cap, P, g, key.p, 0, own_lo, own_hi, A, B,
+                                                                    hl, hr, lo_ok, hi_ok, orig.p, fk, fl, fr, st.p);
+        ++g_launches;
+        CKL();
+      });
+    }
+    scan<int>(fk, P, pk, scan_sums_i, pk + P);
+    scan<int>(fl, P, pl, scan_sums_i, pl + P);
+    scan<int>(fr, P, pr, scan_sums_i, pr + P);
+    gmin_int(&st.p->err_migrate, 1);
+    int cnt[3];
+    CK(cudaMemcpyAsync(&cnt[0], pk + P, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&cnt[1], pl + P, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&cnt[2], pr + P, sizeof(int), cudaMemcpyDeviceToHost, s));
+    read_status();
+    if (h_st->err_migrate != INT_MAX)
+      throw SimError(IMPM_ERR_DOMAIN, "particle " + std::to_string(h_st->err_migrate) +
+                                          " moved past the neighbouring slab in one step");
+    if (P == 0) cnt[0] = cnt[1] = cnt[2] = 0;
+    const int nk = cnt[0], nl = cnt[1], nrr = cnt[2];
+    // counts, then payloads (records of ND doubles + id)
+    slab_counts.ensure(4);
+    long long hc[4] = {nl, nrr, 0, 0};
+    CK(cudaMemcpyAsync(slab_counts.p, hc, sizeof(hc), cudaMemcpyHostToDevice, s));
+    {
+      std::vector<Comm::Msg> snd, rcv;
+      if (hl) {
+        snd.push_back({rk - 1, slab_counts.p + 0, sizeof(long long)});
+        rcv.push_back({rk - 1, slab_counts.p + 2, sizeof(long long)});
+      }
+      if (hr) {
+        snd.push_back({rk + 1, slab_counts.p + 1, sizeof(long long)});
+        rcv.push_back({rk + 1, slab_counts.p + 3, sizeof(long long)});
+      }
+      comm_call([&] { comm->exchange(snd, rcv, s); });
+    }
+    CK(cudaMemcpyAsync(hc, slab_counts.p, sizeof(hc), cudaMemcpyDeviceToHost, s));
+    sync();
+    const int cl = static_cast<int>(hc[2]), cr = static_cast<int>(hc[3]);
+    const int RW = ND + 1;
+    mig_send_l.ensure(static_cast<size_t>(std::max(nl, 1)) * RW);
+    mig_send_r.ensure(static_cast<size_t>(std::max(nrr, 1)) * RW);
+    mig_recv_l.ensure(static_cast<size_t>(std::max(cl, 1)) * RW);
+    mig_recv_r.ensure(static_cast<size_t>(std::max(cr, 1)) * RW);
+    if (P > 0) {
+      k_pack_records<<<blocks_for(P), kThreads, 0, s>>>(pd.p, cap, P, ND, orig.p, fl, pl, mig_send_l.p); ++g_launches;
+      k_pack_records<<<blocks_for(P), kThreads, 0, s>>>(pd.p, cap, P, ND, orig.p, fr, pr, mig_send_r.p); ++g_launches;
+      CKL();
+    }
+    {
+      std::vector<Comm::Msg> snd, rcv;
+      const size_t rb = sizeof(double) * RW;
+      if (hl) {
+        snd.push_back({rk - 1, mig_send_l.p, rb * nl});
+        rcv.push_back({rk - 1, mig_recv_l.p, rb * cl});
+      }
+      if (hr) {
+        snd.push_back({rk + 1, mig_send_r.p, rb * nrr});
+        rcv.push_back({rk + 1, mig_recv_r.p, rb * cr});
+      }
+      comm_call([&] { comm->exchange(snd, rcv, s); });
+    }
+    const int newP = cl + nk + cr;
+    // grow with headroom: every growth reallocates all per-particle buffers
+    const int64_t newcap = newP > cap ? newP + newP / 32 + 1 : cap;
+    pd_tmp.ensure(newcap * ND);
+    orig_tmp.ensure(newcap);
+    if (cl > 0) {
+      k_unpack_records<<<blocks_for(cl), kThreads, 0, s>>>(mig_recv_l.p, cl, ND, pd_tmp.p, newcap, 0, orig_tmp.p);
+      ++g_launches;
+    }
+    if (P > 0) {
+      k_keep_gather<<<blocks_for(P), kThreads, 0, s>>>(pd.p, cap, P, ND, orig.p, fk, pk, pd_tmp.p, newcap, cl,
+                                                       orig_tmp.p);
+      ++g_launches;
+    }
+    if (cr > 0) {
+      k_unpack_records<<<blocks_for(cr), kThreads, 0, s>>>(mig_recv_r.p, cr, ND, pd_tmp.p, newcap, cl + nk,
+                                                           orig_tmp.p);
+      ++g_launches;
+    }
+    CKL();
+    std::swap(pd.p, pd_tmp.p);
+    std::swap(pd.cap, pd_tmp.cap);
+    std::swap(orig.p, orig_tmp.p);
+    std::swap(orig.cap, orig_tmp.cap);
+    P = newP;
+    cap = newcap;
+    ensure_particle_buffers();
+    sync();
+    step_built = false;
+    matrix_valid = false;
+  }
+
   void set_particle_field(int field, const double* vals_h) {
+    if (slab) throw SimError(IMPM_ERR_UNSUPPORTED, "set_particle_field indexes the full particle set");
     if (field < 0 || field >= ND) throw SimError(IMPM_ERR_CONFIG, "bad particle field");
     DBuf<double> tmp;
     tmp.ensure(std::max(P, 1));
@@ -495,6 +732,7 @@ struct Sim {
         }
       });
     }
+    gmin_int(&st.p->err_domain, 3);  // err_domain, err_ood, err_cfg
     read_status();
     if (h_st->err_ood != INT_MAX) throw SimError(IMPM_ERR_OUT_OF_DOMAIN, ood_message(h_st->err_ood));
     if (h_st->err_cfg != INT_MAX)
@@ -546,6 +784,8 @@ struct Sim {
           k_bext<DD><<<blocks_for(P), kThreads, 0, s>>>(pd.p, cap, P, gravity[0], gravity[1], gravity[2], bext.p, st.p); ++g_launches;
           CKL();
         }
+        // activity cutoff 1e-12 * max particle mass over ALL particles
+        if (multi()) comm_call([&] { comm->allreduce(&st.p->max_mass, 1, RedType::F64, RedOp::Max, s); });
         if (coupled) {
           if constexpr (DD == 2)
             k_node_mass<2, 3, SH><<<blocks_for(N), kThreads, 0, s>>>(g, pd.p, cap, xs.p, bin_start.p, sup.p, fixed.p,
@@ -555,6 +795,11 @@ struct Sim {
                                                                       st.p, mass.p, act_flag.p, free_flag.p);
         } ++g_launches;
         CKL();
+        if (slab) {
+          k_mask_owned<<<blocks_for(N), kThreads, 0, s>>>(N, F, g.stride[0], own_lo, own_hi, act_flag.p, free_flag.p);
+          ++g_launches;
+          CKL();
+        }
       });
     }
     {
@@ -575,6 +820,26 @@ struct Sim {
     prof.flush();
     n_dofs = counts[0];
     n_act = counts[1];
+    // global DofMap = exclusive scan of the owned free-DOF counts in rank
+    // order (grid.hpp:69-86 numbers nodes in ascending flat order, axis 0
+    // slowest, so each slab's DOFs are one contiguous global range)
+    n_dofs_glob = n_dofs;
+    dof_offset = 0;
+    if (multi()) {
+      const int nr = comm->nranks;
+      slab_counts.ensure(std::max(nr, 4));
+      std::vector<long long> hcnt(nr, 0);
+      hcnt[comm->rank] = n_dofs;
+      CK(cudaMemcpyAsync(slab_counts.p, hcnt.data(), sizeof(long long) * nr, cudaMemcpyHostToDevice, s));
+      comm_call([&] { comm->allreduce(slab_counts.p, nr, RedType::I64, RedOp::Sum, s); });
+      CK(cudaMemcpyAsync(hcnt.data(), slab_counts.p, sizeof(long long) * nr, cudaMemcpyDeviceToHost, s));
+      sync();
+      n_dofs_glob = 0;
+      for (int q = 0; q < nr; ++q) {
+        if (q < comm->rank) dof_offset += hcnt[q];
+        n_dofs_glob += hcnt[q];
+      }
+    }
     const int S = ipow_c(5, D);
     row_len = row_len_for(S, F);
     vals.ensure(std::max<int64_t>(1, static_cast<int64_t>(n_act) * row_len));
@@ -612,6 +877,7 @@ struct Sim {
   double residual_dev(const double* ud, double load_scale, double* rd) {
     clear_errors_only();
     if (coupled) return residual_up(ud, load_scale, rd);
+    halo(ud);
     const MatParams mp = matp();
     dispatch([&](auto Dc, auto Sc) {
       constexpr int DD = decltype(Dc)::value, SH = decltype(Sc)::value;
@@ -629,7 +895,7 @@ struct Sim {
         for (int col = 0; col < nc; ++col) {
           int cc[3] = {0, 0, 0}, nb[3] = {1, 1, 1}, rr = col;
           for (int a = DD - 1; a >= 0; --a) {
-            cc[a] = rr % 3;
+            cc[a] = a == 0 ? colour0(rr % 3) : rr % 3;
             rr /= 3;
             nb[a] = std::max(0, (g.nodes[a] - cc[a] + 2) / 3);
           }
@@ -641,10 +907,12 @@ struct Sim {
         }
         k_mask_norm<<<kRedBlocks, kThreads, 0, s>>>(NF(), freem.p, rd, partials.p); ++g_launches;
         CKL();
+        gsum(partials.p, kRedBlocks);
         k_finalize_sum<1><<<1, 1024, 0, s>>>(partials.p, kRedBlocks, &st.p->norm2); ++g_launches;
         CKL();
       }
     });
+    gmin_int(&st.p->err_domain, 1);
     read_status();
     prof.flush();
     if (h_st->err_domain != INT_MAX)
@@ -655,6 +923,7 @@ struct Sim {
   // ------------------------------------------------------ Jacobian (K6)
   void jacobian_dev(const double* ud) {
     if (coupled) return jacobian_up(ud, up_dt);
+    halo(ud);
     const MatParams mp = matp();
     dispatch([&](auto Dc, auto Sc) {
       constexpr int DD = decltype(Dc)::value, SH = decltype(Sc)::value;
@@ -675,7 +944,7 @@ struct Sim {
         for (int col = 0; col < nc; ++col) {
           int cc[3] = {0, 0, 0}, nb[3] = {1, 1, 1}, r = col;
           for (int a = DD - 1; a >= 0; --a) {
-            cc[a] = r % 3;
+            cc[a] = a == 0 ? colour0(r % 3) : r % 3;
             r /= 3;
             nb[a] = std::max(0, (g.nodes[a] - cc[a] + 2) / 3);
           }
@@ -696,6 +965,7 @@ struct Sim {
 
   // ------------------------------------------------------- Krylov (K7)
   void spmv(const double* x, double* y, const double* dotv, double* parts) {
+    halo(x);  // columns of owned rows reach 2 planes into the neighbours
     Prof::Scope ps(&prof, kcSpmv);
     dispatch_df([&](auto Dc, auto Fc) {
       constexpr int DD = decltype(Dc)::value, FE = decltype(Fc)::value;
@@ -704,18 +974,20 @@ struct Sim {
                                                       row_nzb.p, x, freem.p, y, dotv, parts, dflag.p); ++g_launches;
       CKL();
     });
+    if (parts) gsum(parts, kSpmvBlocks);
   }
 
   template <int FF>
   int cg_solve(const double* b, double* x) {
     const int N = g.N;
-    const int max_it = opt.krylov_max_iter > 0 ? opt.krylov_max_iter : std::min(20000, std::max(100, 10 * n_dofs));
+    const int max_it = opt.krylov_max_iter > 0 ? opt.krylov_max_iter : std::min(20000, std::max(100, 10 * ndg()));
     const double rtol2 = cur_rtol * cur_rtol;
     CK(cudaMemsetAsync(dflag.p, 0, sizeof(int), s));
     {
       Prof::Scope ps(&prof, kcKrylov);
       k_cg_init<FF><<<kRedBlocks, kThreads, 0, s>>>(N, act_idx.p, dinv.p, b, x, kr.p, kz.p, kp.p, partials.p); ++g_launches;
       CKL();
+      gsum(partials.p, 2 * kRedBlocks);
       k_finalize_sum<2><<<1, 1024, 0, s>>>(partials.p, kRedBlocks, sums.p); ++g_launches;
       CKL();
       k_cg_start<<<1, 1, 0, s>>>(sums.p, sc.p, rtol2); ++g_launches;
@@ -725,7 +997,7 @@ struct Sim {
     CK(cudaMemcpyAsync(h_sc, sc.p, sizeof(double) * kNSlots, cudaMemcpyDeviceToHost, s));
     sync();
     if (h_sc[kDone] != 0.0) return 0;
-    const int batch = n_dofs < 20000 ? 16 : 4;
+    const int batch = ndg() < 20000 ? 16 : 4;
     int done = 0;
     double* partA = partials.p;
     double* partB = partials.p + kSpmvBlocks;
@@ -736,6 +1008,7 @@ struct Sim {
         Prof::Scope ps(&prof, kcKrylov);
         k_cg_update2<FF><<<kRedBlocks, kThreads, 0, s>>>(N, act_idx.p, dinv.p, sc.p, dflag.p, par, partA, kSpmvBlocks,
                                                          x, kr.p, kz.p, kp.p, kq.p, partB); ++g_launches;
+        gsum(partB, 2 * kRedBlocks);
         k_cg_p2<FF><<<kRedBlocks, kThreads, 0, s>>>(N, act_idx.p, sc.p, dflag.p, par, it, partB, kRedBlocks, rtol2,
                                                     max_it, kz.p, kp.p); ++g_launches;
         CKL();
@@ -759,6 +1032,7 @@ struct Sim {
   // host-scalar BiCGStab (right block-Jacobi preconditioning), nonsymmetric path
   double dot(const double* a, const double* b) {
     k_dot2<<<kRedBlocks, kThreads, 0, s>>>(NF(), a, b, nullptr, nullptr, partials.p); ++g_launches;
+    gsum(partials.p, 2 * kRedBlocks);
     k_finalize_sum<2><<<1, 1024, 0, s>>>(partials.p, kRedBlocks, sums.p); ++g_launches;
     CKL();
     double h[2];
@@ -793,8 +1067,8 @@ struct Sim {
     CK(cudaMemsetAsync(dflag.p, 0, sizeof(int), s));
     // the u-p saddle point (cond ~1e15) needs far more than n iterations
     const int max_it = opt.krylov_max_iter > 0 ? opt.krylov_max_iter
-                       : coupled              ? std::max(4000, 50 * n_dofs)
-                                              : std::min(20000, std::max(100, 10 * n_dofs));
+                       : coupled              ? std::max(4000, 50 * ndg())
+                                              : std::min(20000, std::max(100, 10 * ndg()));
     CK(cudaMemsetAsync(x, 0, sizeof(double) * NF(), s));
     CK(cudaMemcpyAsync(kr.p, b, sizeof(double) * NF(), cudaMemcpyDeviceToDevice, s));
     CK(cudaMemcpyAsync(khat.p, b, sizeof(double) * NF(), cudaMemcpyDeviceToDevice, s));
@@ -1124,7 +1398,7 @@ struct Sim {
   int cg_mg_solve(const double* b, double* x) {
     const int N = g.N;
     const int64_t n = NF();
-    const int max_it = opt.krylov_max_iter > 0 ? opt.krylov_max_iter : std::min(20000, std::max(100, 10 * n_dofs));
+    const int max_it = opt.krylov_max_iter > 0 ? opt.krylov_max_iter : std::min(20000, std::max(100, 10 * ndg()));
     const double rtol2 = cur_rtol * cur_rtol;
     {
       Prof::Scope ps(&prof, kcMgSetup);
@@ -1142,13 +1416,14 @@ struct Sim {
     const double* z = mg[0]->x;
     CK(cudaMemcpyAsync(kp.p, z, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
     k_dot2<<<kRedBlocks, kThreads, 0, s>>>(n, kr.p, z, b, b, partials.p); ++g_launches;
+    gsum(partials.p, 2 * kRedBlocks);
     k_finalize_sum<2><<<1, 1024, 0, s>>>(partials.p, kRedBlocks, sums.p); ++g_launches;
     k_cg_start<<<1, 1, 0, s>>>(sums.p, sc.p, rtol2); ++g_launches;
     CKL();
     CK(cudaMemcpyAsync(h_sc, sc.p, sizeof(double) * kNSlots, cudaMemcpyDeviceToHost, s));
     sync();
     if (h_sc[kDone] != 0.0) return 0;
-    const int batch = n_dofs < 20000 ? 8 : 4;
+    const int batch = ndg() < 20000 ? 8 : 4;
     int done = 0;
     for (int it = 0; !done;) {
       for (int i = 0; i < batch; ++i, ++it) {
@@ -1167,6 +1442,7 @@ struct Sim {
         z = mg[0]->x;
         Prof::Scope ps(&prof, kcKrylov);
         k_dot1<<<kRedBlocks, kThreads, 0, s>>>(n, dflag.p, kr.p, z, partB); ++g_launches;
+        gsum(partB, 2 * kRedBlocks);
         k_cg_p2<FE><<<kRedBlocks, kThreads, 0, s>>>(N, act_idx.p, sc.p, dflag.p, par, it, partB, kRedBlocks, rtol2,
                                                     max_it, z, kp.p); ++g_launches;
         CKL();
@@ -1195,6 +1471,7 @@ struct Sim {
   static constexpr int kGmBlocks = 148;
   double dot_sync(const double* a, const double* b) {
     k_dot2<<<kRedBlocks, kThreads, 0, s>>>(NF(), a, b, nullptr, nullptr, partials.p); ++g_launches;
+    gsum(partials.p, 2 * kRedBlocks);
     k_finalize_sum<2><<<1, 1024, 0, s>>>(partials.p, kRedBlocks, sums.p); ++g_launches;
     CKL();
     double hh[2];
@@ -1206,11 +1483,11 @@ struct Sim {
   template <int DD, int FE>
   int gmres_solve(const double* b, double* x, bool mgp) {
     const int64_t n = NF();
-    const int m = std::max(2, std::min(300, n_dofs));
+    const int m = std::max(2, std::min(300, ndg()));
     gm_part.ensure(static_cast<size_t>(m + 1) * kGmBlocks);
     gm_h.ensure(m + 1);
     std::vector<double> hbuf(m + 1);
-    const int max_it = opt.krylov_max_iter > 0 ? opt.krylov_max_iter : std::max(2000, 20 * n_dofs);
+    const int max_it = opt.krylov_max_iter > 0 ? opt.krylov_max_iter : std::max(2000, 20 * ndg());
     if (mgp) mg_setup<DD, FE>();
     CK(cudaMemsetAsync(dflag.p, 0, sizeof(int), s));
     gm_V.ensure(static_cast<size_t>(m + 1) * n);
@@ -1240,6 +1517,7 @@ struct Sim {
         for (int i = 0; i <= j; ++i) H[static_cast<size_t>(i) * m + j] = 0.0;
         for (int pass = 0; pass < 2; ++pass) {
           k_vdot<<<dim3(kGmBlocks, j + 1), kThreads, 0, s>>>(n, gm_V.p, n, w, gm_part.p); ++g_launches;
+          gsum(gm_part.p, static_cast<size_t>(j + 1) * kGmBlocks);
           k_finalize_rows<<<j + 1, 256, 0, s>>>(gm_part.p, kGmBlocks, gm_h.p); ++g_launches;
           k_vsub<<<kRedBlocks, kThreads, 0, s>>>(n, gm_V.p, n, j + 1, gm_h.p, w); ++g_launches;
           CKL();
@@ -1634,6 +1912,7 @@ struct Sim {
     clear_errors_only();
     const int big = INT_MAX;
     CK(cudaMemcpyAsync(&st.p->err_lp, &big, sizeof(int), cudaMemcpyHostToDevice, s));
+    halo(u.p);
     const MatParams mp = matp();
     dispatch([&](auto Dc, auto Sc) {
       constexpr int DD = decltype(Dc)::value, SH = decltype(Sc)::value;
@@ -1644,6 +1923,7 @@ struct Sim {
         CKL();
       }
     });
+    gmin_int(&st.p->err_domain, 5);  // err_domain .. err_lp
     read_status();
     prof.flush();
     if (h_st->err_domain != INT_MAX)
@@ -1712,6 +1992,11 @@ impm_status fail(Sim* sim, const SimError& e) {
 thread_local std::string g_create_error;
 
 }  // namespace
+
+// opaque communicator handle of the C ABI (include/impm_gpu.h)
+struct impm_comm {
+  std::shared_ptr<Comm> c;
+};
 
 // ================================================================ C ABI ===
 #define API_BEGIN(sim)        \
@@ -1956,6 +2241,7 @@ impm_status impm_sim_step(impm_sim* h, double load_scale, impm_step_record* rec)
   sim->begin_step();
   sim->newton_solve(load_scale, rec);
   sim->commit_step();
+  if (sim->slab) sim->migrate();  // particles follow their slab for the next step
   API_END(sim)
 }
 impm_status impm_coupled_initialize(impm_sim* h) {
@@ -2055,6 +2341,108 @@ impm_status impm_sim_matrix_info(impm_sim* h, int64_t* n_rows, int64_t* row_valu
     *row_values = static_cast<int64_t>(sim->h_nzb_total) * sim->F * sim->F;  // stored block values (all rows)
   }
   if (ref_nnz) *ref_nnz = sim->step_built ? sim->ref_nnz() : 0;
+  API_END(sim)
+}
+
+// ------------------------------------------------- slab decomposition (§8e)
+impm_status impm_comm_nccl_id(uint8_t* id, int32_t cap) {
+  if (!id || cap < static_cast<int32_t>(sizeof(ncclUniqueId))) return IMPM_ERR_CONFIG;
+  ncclUniqueId u;
+  const ncclResult_t r = ncclGetUniqueId(&u);
+  if (r != ncclSuccess) {
+    g_create_error = std::string("ncclGetUniqueId: ") + ncclGetErrorString(r);
+    return IMPM_ERR_NCCL;
+  }
+  std::memcpy(id, &u, sizeof(u));
+  return IMPM_OK;
+}
+impm_status impm_comm_nccl_create(const uint8_t* id, int32_t rank, int32_t nranks, int32_t device, impm_comm** out) {
+  if (!id || !out || nranks < 1 || rank < 0 || rank >= nranks) return IMPM_ERR_CONFIG;
+  try {
+    CK(cudaSetDevice(device));
+    ncclUniqueId u;
+    std::memcpy(&u, id, sizeof(u));
+    *out = new impm_comm{std::make_shared<NcclComm>(u, rank, nranks)};
+    return IMPM_OK;
+  } catch (const CommError& e) {
+    g_create_error = e.what();
+    return IMPM_ERR_NCCL;
+  } catch (const std::exception& e) {
+    g_create_error = e.what();
+    return IMPM_ERR_CUDA;
+  }
+}
+impm_status impm_comm_local_group(int32_t nranks, int32_t device, impm_comm** out) {
+  if (!out || nranks < 1) return IMPM_ERR_CONFIG;
+  try {
+    CK(cudaSetDevice(device));
+    auto grp = std::make_shared<LocalGroup>(nranks);
+    for (int r = 0; r < nranks; ++r) out[r] = new impm_comm{std::make_shared<LocalComm>(grp, r)};
+    return IMPM_OK;
+  } catch (const std::exception& e) {
+    g_create_error = e.what();
+    return IMPM_ERR_CUDA;
+  }
+}
+impm_status impm_comm_destroy(impm_comm* c) {
+  delete c;
+  return IMPM_OK;
+}
+impm_status impm_comm_info(impm_comm* c, int32_t* rank, int32_t* nranks, const char** kind) {
+  if (!c) return IMPM_ERR_CONFIG;
+  if (rank) *rank = c->c->rank;
+  if (nranks) *nranks = c->c->nranks;
+  if (kind) *kind = c->c->kind();
+  return IMPM_OK;
+}
+impm_status impm_sim_set_slab(impm_sim* h, impm_comm* c, int32_t global_n0, const int32_t* cuts) {
+  SIM;
+  API_BEGIN(sim)
+  if (!c || !cuts) throw SimError(IMPM_ERR_CONFIG, "set_slab needs a communicator and the ownership cuts");
+  sim->set_slab(c->c, global_n0, cuts);
+  API_END(sim)
+}
+impm_status impm_sim_set_particles_ids(impm_sim* h, const double* aos, const int64_t* ids, int64_t n, int64_t stride) {
+  SIM;
+  API_BEGIN(sim)
+  sim->set_particles_ids(aos, ids, n, stride);
+  API_END(sim)
+}
+impm_status impm_sim_get_particles_ids(impm_sim* h, double* aos, int64_t* ids, int64_t n, int64_t stride) {
+  SIM;
+  API_BEGIN(sim)
+  sim->get_particles_ids(aos, ids, n, stride);
+  API_END(sim)
+}
+impm_status impm_sim_migrate(impm_sim* h) {
+  SIM;
+  API_BEGIN(sim)
+  sim->migrate();
+  API_END(sim)
+}
+impm_status impm_sim_slab_info(impm_sim* h, int64_t* n_dofs_global, int64_t* dof_offset, int32_t* base0) {
+  SIM;
+  API_BEGIN(sim)
+  if (n_dofs_global) *n_dofs_global = sim->n_dofs_glob;
+  if (dof_offset) *dof_offset = sim->dof_offset;
+  if (base0) *base0 = sim->g.base0;
+  API_END(sim)
+}
+impm_status impm_sim_apply_jacobian(impm_sim* h, const double* uh, double load_scale, const double* x, double* y) {
+  SIM;
+  API_BEGIN(sim)
+  (void)load_scale;  // J does not depend on the load scale (external loads are constant in u)
+  if (!sim->step_built) throw SimError(IMPM_ERR_CONFIG, "apply_jacobian before begin_step");
+  if (sim->coupled) throw SimError(IMPM_ERR_UNSUPPORTED, "apply_jacobian: single-field simulations only");
+  sim->upload_dof_vec(uh, sim->tmp1.p);
+  sim->jacobian_dev(sim->tmp1.p);
+  const int64_t nf = sim->NF();
+  CK(cudaMemcpyAsync(sim->kx.p, x, sizeof(double) * nf, cudaMemcpyHostToDevice, sim->s));
+  CK(cudaMemsetAsync(sim->kq.p, 0, sizeof(double) * nf, sim->s));
+  sim->spmv(sim->kx.p, sim->kq.p, nullptr, nullptr);
+  CK(cudaMemcpyAsync(y, sim->kq.p, sizeof(double) * nf, cudaMemcpyDeviceToHost, sim->s));
+  sim->sync();
+  sim->prof.flush();
   API_END(sim)
 }
 

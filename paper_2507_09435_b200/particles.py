@@ -70,6 +70,47 @@ class GridSpec:
         return np.asarray(self.origin[: self.dim], dtype=np.float64) + idx * self.h
 
 
+def seed_box_rows(grid: GridSpec, lo, hi, ppc, density, rows):
+    """The particles of seed_box(grid, lo, hi, ppc, density) whose axis-0
+    lattice index is in `rows` (ascending), with their global ids (row index in
+    the full seed_box array), generated without the full array: axis 0 is the
+    slowest lattice index, so each row is a contiguous id range."""
+    D = grid.dim
+    cells = [int(np.floor((hi[a] - lo[a]) / grid.h + 0.5)) for a in range(D)]
+    spacing = grid.h / ppc
+    vol = 1.0
+    for _ in range(D):
+        vol *= spacing
+    sub = [c * ppc for c in cells]
+    rows = np.asarray(rows, dtype=np.int64)
+    inner = int(np.prod(sub[1:])) if D > 1 else 1
+    total = rows.size * inner
+    out = np.zeros((total, particle_doubles(D)), dtype=np.float64)
+    ids = (rows[:, None] * inner + np.arange(inner, dtype=np.int64)[None, :]).reshape(-1)
+    if total == 0:
+        return out, ids
+    pa = ParticleArray(out, D)
+    idx = [np.repeat(rows, inner)]
+    if D > 1:
+        rest = np.indices(sub[1:]).reshape(D - 1, -1)
+        for a in range(D - 1):
+            idx.append(np.tile(rest[a], rows.size))
+    for a in range(D):
+        X = lo[a] + (idx[a].astype(np.float64) + 0.5) * spacing
+        pa.X[:, a] = X
+        pa.x[:, a] = X
+        pa.lp0[:, a] = 0.5 * spacing
+        pa.lp[:, a] = 0.5 * spacing
+    pa.V0[:, 0] = vol
+    pa.V[:, 0] = vol
+    pa.m[:, 0] = density * vol
+    F = pa.F
+    for a in range(D):
+        F[:, a * D + a] = 1.0
+    pa.B_e[:, 0] = pa.B_e[:, 4] = pa.B_e[:, 8] = 1.0
+    return out, ids
+
+
 def seed_box(grid: GridSpec, lo, hi, ppc, density):
     """ppc^D equally spaced particles per cell in [lo, hi] (particle.hpp:33-69)."""
     D = grid.dim

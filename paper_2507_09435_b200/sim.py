@@ -285,6 +285,18 @@ class MpmSim:
                      ctypes.byref(it))
         return out[: self.n_dofs()], it.value
 
+    def apply_jacobian(self, u, load_scale, x_grid):
+        """y = J(u) x for a grid-layout vector x [N * D] (u = free-DOF vector);
+        on a slab the owned rows are valid and halo columns come from the
+        neighbours."""
+        u = _abi.f64(u)
+        x = np.ascontiguousarray(x_grid, dtype=np.float64).reshape(-1)
+        if x.size != self._N * self.D:
+            raise ValueError("x must be a grid vector [N_local * D]")
+        y = np.zeros_like(x)
+        self._h.call("impm_sim_apply_jacobian", _abi.ptr(u), float(load_scale), _abi.ptr(x), _abi.ptr(y))
+        return y
+
     def _record(self):
         buf = np.zeros(256)
         rec = _abi.StepRecordC()

@@ -200,3 +200,45 @@ def test_two_slab_decomposition_matches_single_process(case):
     while not errq.empty():
         errs.append(errq.get())
     assert all(p.exitcode == 0 for p in procs), "\n".join(errs)
+
+
+# ---------------------------------------------------------------- GPU-slab host logic
+def test_seed_box_rows_and_slab_seeding_match_global_seed_box():
+    """seed_box_rows / seed_box_slab generate exactly the rows (and global ids)
+    of seed_box that each rank holds, without the global array."""
+    from paper_2507_09435_b200 import distributed as dd
+    from paper_2507_09435_b200.particles import GridSpec, seed_box, seed_box_rows
+
+    for D, nodes, hi in [(1, (19,), (16.0,)), (2, (19, 7), (16.0, 4.0)), (3, (11, 11, 7), (8.0, 8.0, 4.0))]:
+        g = GridSpec(D, tuple([-1.0] * D), 1.0, nodes)
+        full = seed_box(g, (0.0,) * D, hi, 2, 2000.0)
+        p, ids = seed_box_rows(g, (0.0,) * D, hi, 2, 2000.0, np.arange(int(round(hi[0])) * 2))
+        assert np.array_equal(p, full) and np.array_equal(ids, np.arange(len(full)))
+        cuts = dd.slab_cuts(g, 2, full)
+        held = []
+        for r in range(2):
+            ps, ids = dd.seed_box_slab(g, (0.0,) * D, hi, 2, 2000.0, cuts, r)
+            assert np.array_equal(ids, dd.slab_member_ids(g, full, cuts, r))
+            assert np.array_equal(ps, full[ids])
+            held.append(ids)
+        from paper_2507_09435_b200 import slabs
+
+        first = slabs.support_first(g, full)
+        owned = np.concatenate([np.nonzero(dd.owned_mask(first, cuts, r))[0] for r in range(2)])
+        assert np.array_equal(np.sort(owned), np.arange(len(full)))  # every particle owned once
+
+
+def test_slab_cuts_respect_minimum_width_and_balance():
+    from paper_2507_09435_b200 import distributed as dd
+    from paper_2507_09435_b200.errors import ConfigError
+    from paper_2507_09435_b200.particles import GridSpec, seed_box
+
+    g = GridSpec(3, (-0.5, -0.5, -0.5), 0.5, (67, 11, 7))
+    parts = seed_box(g, (0.0, 0.0, 0.0), (32.0, 4.0, 2.0), 2, 2000.0)
+    for nr in (1, 2, 3, 4, 8):
+        cuts = dd.slab_cuts(g, nr, parts)
+        assert cuts[0] == 0 and cuts[-1] == 67 and len(cuts) == nr + 1
+        if nr > 1:
+            assert min(np.diff(cuts)) >= dd.MIN_PLANES
+    with pytest.raises(ConfigError):
+        dd.slab_cuts(GridSpec(2, (-1.0, -1.0), 1.0, (7, 7)), 2)
