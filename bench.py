@@ -140,13 +140,22 @@ def run_reference_sample(budget_s, replicas=1):
 
 
 # ------------------------------------------------------------- product ----
-def make_sim(prob, device, profile):
+def make_sim(prob, device, profile, comm=None):
+    """Single GPU: MpmSim on the whole problem. N > 1: this rank's SlabSim of
+    the cfg 5 problem (axis-0 slab decomposition over NCCL)."""
     import paper_2507_09435_b200 as impm
 
     opts = prob.options
     opts.profile = profile
-    sim = impm.MpmSim(prob.grid, prob.particles, prob.material, opts, device=device)
-    sim.fixed[:] = prob.fixed
+    if comm is None:
+        sim = impm.MpmSim(prob.grid, prob.particles, prob.material, opts, device=device)
+        sim.fixed[:] = prob.fixed
+    else:
+        from paper_2507_09435_b200.distributed import SlabSim
+
+        sim = SlabSim(prob.grid, comm, prob.meta["cuts"], prob.particles, prob.meta["ids"], prob.material, opts,
+                      device=device)
+        sim.set_fixed_global(prob.fixed)
     sim.gravity = prob.gravity
     return sim
 
@@ -212,12 +221,27 @@ def main():
 
     from paper_2507_09435_b200 import _abi, workloads
 
-    if args.config == "cfg4":
+    comm = None
+    if world > 1:
+        # cfg 5: one cfg 4 slab per GPU, stacked along axis 0, one NCCL
+        # communicator of the library (halos + dot partials on the sim stream)
+        from paper_2507_09435_b200.distributed import Communicator
+
+        def bcast(payload):
+            box = [payload]
+            dist.broadcast_object_list(box, src=0)
+            return box[0]
+
+        comm = Communicator.nccl(rank, world, device, broadcast=bcast)
+        if args.config != "cfg4":
+            raise SystemExit("multi-GPU runs use the cfg 5 slab workload (--config cfg4)")
+        prob = workloads.footing3d_slab(world, rank)
+    elif args.config == "cfg4":
         prob = workloads.footing3d()
     else:
         prob = workloads.column2d_nh()
     D = prob.grid.dim
-    sim = make_sim(prob, device, profile=False)
+    sim = make_sim(prob, device, profile=False, comm=comm)
     stream = torch.cuda.current_stream(device)
     sim.set_stream(stream.cuda_stream)
     n_total = prob.load_steps
@@ -288,17 +312,37 @@ def main():
     if args.e2e_steps > 0:
         host = torch.empty(prob.particles.shape, dtype=torch.float64, pin_memory=True).numpy()
         host[:] = prob.particles
-        back = torch.empty(prob.particles.shape, dtype=torch.float64, pin_memory=True).numpy()
-        sim2 = make_sim(prob, device, profile=False)
+        # migration can grow a slab's particle count: headroom for the download
+        rows = prob.particles.shape[0] if comm is None else int(prob.particles.shape[0] * 1.1) + 1024
+        back = torch.empty((rows, prob.particles.shape[1]), dtype=torch.float64, pin_memory=True).numpy()
+        d2h = [0]
+        sim2 = make_sim(prob, device, profile=False, comm=comm)
         sim2.set_stream(stream.cuda_stream)
         e_its = 0
-        sim2.set_particles(host)  # warm (allocations)
+        ids = prob.meta.get("ids") if comm is not None else None
+
+        def upload():  # H2D of this step's inputs (pinned host AoS)
+            if comm is None:
+                sim2.set_particles(host)
+            else:
+                sim2.set_particles(host, ids)
+
+        def download():  # D2H of the step's result (particle state)
+            n = sim2.n_particles if comm is not None else back.shape[0]
+            d2h[0] = n * back.strides[0]
+            if comm is None:
+                sim2._h.call("impm_sim_get_particles", _abi.ptr(back), n, back.strides[0])
+            else:
+                ids_out = np.empty(n, dtype=np.int64)
+                sim2._h.call("impm_sim_get_particles_ids", _abi.ptr(back), _abi.ptr(ids_out), n, back.strides[0])
+
+        upload()  # warm (allocations)
         torch.cuda.synchronize(device)
         t0 = time.perf_counter()
         for j in range(args.e2e_steps):
-            sim2.set_particles(host)  # H2D of this step's inputs
+            upload()
             e_its += sim2.step(scale(1)).iterations
-            sim2._h.call("impm_sim_get_particles", _abi.ptr(back), back.shape[0], back.strides[0])  # D2H
+            download()
         torch.cuda.synchronize(device)
         el = time.perf_counter() - t0
         e_t = torch.tensor([el], dtype=torch.float64, device=f"cuda:{device}")
@@ -307,7 +351,7 @@ def main():
             dist.all_reduce(e_t, op=dist.ReduceOp.MAX)
             dist.all_reduce(e_i, op=dist.ReduceOp.SUM)
         e2e = {"value": float(e_i.item()) / float(e_t.item()), "unit": UNIT,
-               "h2d_bytes_per_step": int(host.nbytes), "d2h_bytes_per_step": int(back.nbytes),
+               "h2d_bytes_per_step": int(host.nbytes), "d2h_bytes_per_step": int(d2h[0]),
                "newton_iterations": int(e_its), "seconds": float(e_t.item())}
         del sim2
 
@@ -338,7 +382,8 @@ def main():
                    "stored_blocks_per_row": info["row_values"] / max(info["rows"], 1) / D ** 2,
                    "free_dofs": int(sim.n_dofs()), "load_increments": n_total,
                    "parallelism": "1 slab per GPU" if world == 1 else
-                   f"{world} independent slabs (halo exchange not yet implemented: replicas)",
+                   (f"{world} axis-0 slabs of one (128*{world})x128x64-cell problem (cfg 5): NCCL 2-plane halos, "
+                    f"summed dot partials, rank-local MG (block Jacobi across slabs), particle migration"),
                    "l2": "inputs larger than L2 (particle state 3.3 GB, BSR 9.7 GB per slab)"},
         "newton_iterations": its, "krylov_iterations": kry,
         "nnz_per_s": nnz_rate, "nnz_assembled": nnz,

@@ -98,6 +98,11 @@ def slab_cuts(grid: GridSpec, nranks: int, particles=None, use_X=False):
     if particles is not None:
         first = slabs.support_first(grid, particles, 0, use_X)
         w = np.bincount(np.clip(first, 0, n0 - 1), minlength=n0)
+    return slab_cuts_from_weights(n0, nranks, w)
+
+
+def slab_cuts_from_weights(n0, nranks, w=None):
+    """Cuts balanced by per-plane weights `w` [n0] (None: by plane count)."""
     ranges = slabs.partition_nodes(n0, nranks, w)
     cuts = [r[0] for r in ranges] + [n0]
     if nranks > 1:  # every slab >= MIN_PLANES owned planes (2-plane halos, one-neighbour migration)

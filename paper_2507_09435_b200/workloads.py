@@ -110,6 +110,45 @@ def footing3d(cells=(128, 128, 64), ppc=2, h=0.5, steps=20, t_hat=100e3, frac=0.
                    meta={"strip_particles": n_strip})
 
 
+def footing3d_slab(nranks, rank, cells=(128, 128, 64), ppc=2, h=0.5, steps=20, t_hat=100e3, frac=0.125, E=10e6,
+                   nu=0.3, density=2000.0):
+    """cfg 5 (weak scaling): cfg 4 per GPU stacked along axis 0, i.e. the
+    footing3d problem on (cells[0] * nranks) x cells[1] x cells[2] cells, of
+    which only rank `rank`'s slab (owned + ghost particles) is generated. The
+    strip-traction magnitude uses the GLOBAL strip particle count (computed
+    from the lattice), so nranks = 1 reproduces footing3d() exactly. Returns a
+    Problem whose meta holds the global ids, cuts and global grid."""
+    from .distributed import keep_mask, slab_cuts_from_weights, seed_box_slab
+
+    D = 3
+    gcells = (cells[0] * nranks, cells[1], cells[2])
+    grid = GridSpec(3, (-h, -h, -h), h, tuple(c + 3 for c in gcells))
+    ext = tuple(c * h for c in gcells)
+    spacing = h / ppc
+    sub = [c * ppc for c in gcells]
+    x0 = 0.0 + (np.arange(sub[0], dtype=np.float64) + 0.5) * spacing
+    lp = np.full(sub[0], 0.5 * spacing)
+    first = np.floor((x0 - grid.origin[0] - (grid.h + lp)) / grid.h).astype(np.int64) + 1
+    n0 = int(grid.nodes[0])
+    w = np.bincount(np.clip(first, 0, n0 - 1), minlength=n0).astype(float) * (sub[1] * sub[2])
+    cuts = slab_cuts_from_weights(n0, nranks, w)
+    parts, ids = seed_box_slab(grid, (0.0, 0.0, 0.0), ext, ppc, density, cuts, rank)
+    # strip traction on the top layer under the centred strip (as _strip_traction)
+    lo, hi = 0.5 * ext[0] * (1 - frac), 0.5 * ext[0] * (1 + frac)
+    n_strip = int(((x0 >= lo) & (x0 <= hi)).sum()) * sub[1]
+    area = ext[0] * frac * ext[1]
+    pa = ParticleArray(parts, D)
+    top = 0.0 + (sub[2] - 1 + 0.5) * spacing
+    sel = (pa.X[:, 2] >= top - 1e-9) & (pa.X[:, 0] >= lo) & (pa.X[:, 0] <= hi)
+    pa.traction_force[sel, 2] = -t_hat * area / max(n_strip, 1)
+    mat = MaterialSpec("neo_hookean", ElasticParams(E, nu))
+    return Problem(f"cfg5_footing3d_nh_slab{rank}of{nranks}", grid, parts, mat, SolverOptions(tol=1e-10),
+                   _column_fixed(grid, ext), np.array([0.0, 0.0, -9.81]), steps,
+                   note="cfg4 per GPU stacked along axis 0; neo-Hookean substitute for modified Cam-Clay (unpinned)",
+                   meta={"ids": ids, "cuts": cuts, "strip_particles": n_strip, "rank": rank, "nranks": nranks,
+                         "global_particles": int(np.prod(sub))})
+
+
 def by_name(name, **kw):
     table = {"cfg1": column2d_nh, "cfg2": slope2d, "cfg4": footing3d, "cfg5": footing3d}
     return table[name](**kw)

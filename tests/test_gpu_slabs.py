@@ -210,3 +210,35 @@ def test_slab_rejects_bad_geometry():
     comms = Communicator.local_group(3)
     with pytest.raises(ConfigError):  # 8 planes cannot give 3 slabs of >= 4
         SlabSim.from_global(g, comms[0], [0, 3, 5, 8], parts, m, o)
+
+
+def test_cfg5_slab_workload_matches_single_gpu():
+    """The bench's multi-GPU workload (workloads.footing3d_slab: cfg 4 per GPU
+    stacked along axis 0, generated per rank) on 2 in-process ranks vs the same
+    problem on one GPU: identical Newton counts, particle state within 1e-7."""
+    from paper_2507_09435_b200 import workloads
+    from paper_2507_09435_b200.distributed import SlabSim, gather_owned, run_local_ranks
+    import paper_2507_09435_b200 as impm
+
+    cells = (12, 8, 6)
+    whole = workloads.footing3d(cells=(24, 8, 6), steps=3)
+    single = impm.MpmSim(whole.grid, whole.particles, whole.material, whole.options)
+    single.fixed[:] = whole.fixed
+    single.gravity = whole.gravity
+    ref_iters = [single.step(k / 3).iterations for k in range(1, 4)]
+    ref = single.particles.data
+
+    def body(rank, comm):
+        p = workloads.footing3d_slab(2, rank, cells=cells, steps=3)
+        assert np.array_equal(p.particles, whole.particles[p.meta["ids"]])
+        sim = SlabSim(p.grid, comm, p.meta["cuts"], p.particles, p.meta["ids"], p.material, p.options)
+        sim.set_fixed_global(p.fixed)
+        sim.gravity = p.gravity
+        its = [sim.step(k / 3).iterations for k in range(1, 4)]
+        return its, sim.owned_particles()
+
+    res = run_local_ranks(2, body)
+    assert res[0][0] == ref_iters and res[1][0] == ref_iters
+    owned, ids = gather_owned([r[1] for r in res], 3)
+    np.testing.assert_array_equal(ids, np.arange(len(ref)))
+    _assert_state_close(owned.data, ref, 3, whole.grid.h)
