@@ -338,11 +338,19 @@ def main():
 
         upload()  # warm (allocations)
         torch.cuda.synchronize(device)
+        phase = {"upload": 0.0, "step": 0.0, "download": 0.0}
         t0 = time.perf_counter()
         for j in range(args.e2e_steps):
+            ta = time.perf_counter()
             upload()
+            tb = time.perf_counter()
             e_its += sim2.step(scale(1)).iterations
+            tc = time.perf_counter()
             download()
+            td = time.perf_counter()
+            phase["upload"] += tb - ta
+            phase["step"] += tc - tb
+            phase["download"] += td - tc
         torch.cuda.synchronize(device)
         el = time.perf_counter() - t0
         e_t = torch.tensor([el], dtype=torch.float64, device=f"cuda:{device}")
@@ -352,7 +360,8 @@ def main():
             dist.all_reduce(e_i, op=dist.ReduceOp.SUM)
         e2e = {"value": float(e_i.item()) / float(e_t.item()), "unit": UNIT,
                "h2d_bytes_per_step": int(host.nbytes), "d2h_bytes_per_step": int(d2h[0]),
-               "newton_iterations": int(e_its), "seconds": float(e_t.item())}
+               "newton_iterations": int(e_its), "seconds": float(e_t.item()),
+               "phase_seconds": {k_: round(v_, 4) for k_, v_ in phase.items()}}
         del sim2
 
     if rank != 0:

@@ -1272,7 +1272,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
   constexpr int S = ipow_c(5, D);
   constexpr int FF = F * F;
   constexpr int XS = cpad(S, F);
-  constexpr int NB = 6;  // double2 per lane buffered ahead of the x gathers
+  // double2 per lane buffered ahead of the x gathers (the Jacobi sweep keeps
+  // its Dinv row and rhs in registers too: smaller head under the 64-reg cap)
+  constexpr int NB = MODE == kSpmvJacobi ? 4 : 6;
   __shared__ int offt[S];
   __shared__ __align__(16) double xs_all[WARPS][XS];
   for (int sl = threadIdx.x; sl < S; sl += blockDim.x) {
@@ -1299,6 +1301,27 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
       const int nzb = row_nzb[row];
       const int cp = cpad(nzb, F);
       const int h = cp >> 1, tot2 = F * h;
+      const int64_t base = static_cast<int64_t>(k) * F;
+      // 0. epilogue operands go in flight first: lane c < F holds component
+      //    c's free mask, its dot / rhs operand, its own x and row c of Dinv
+      bool fm = false;
+      double e0 = 0.0, e1 = 0.0;
+      double di[F];
+#pragma unroll
+      for (int d = 0; d < F; ++d) di[d] = 0.0;
+      if (lane < F) {
+        fm = freem[base + lane] != 0;
+        if constexpr (MODE == kSpmvY) {
+          if (dotv) e0 = dotv[base + lane];
+        } else {
+          e0 = b[base + lane];
+          if constexpr (MODE == kSpmvJacobi) {
+            e1 = x[base + lane];
+#pragma unroll
+            for (int d = 0; d < F; ++d) di[d] = dinv[static_cast<int64_t>(row) * FF + lane * F + d];
+          }
+        }
+      }
       // 1. the first NB double2 per lane of the row (independent of x) go in
       //    flight before the x gathers
       const double2* rv = reinterpret_cast<const double2*>(vals + static_cast<int64_t>(row) * row_len);
@@ -1335,35 +1358,31 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
       }
 #pragma unroll 4
       for (int j2 = lane + 32 * NB; j2 < tot2; j2 += 32) consume(j2, __ldcs(rv + j2));
+      // butterfly: every lane holds the row sums; lane c < F finishes component c
 #pragma unroll
       for (int c = 0; c < F; ++c)
-        for (int o = 16; o > 0; o >>= 1) acc[c] += __shfl_down_sync(0xffffffffu, acc[c], o);
-      if (lane == 0) {
-        const int64_t base = static_cast<int64_t>(k) * F;
-        if constexpr (MODE == kSpmvY) {
+        for (int o = 16; o > 0; o >>= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
+      double mine = acc[0];
+      if (F > 1 && lane == 1) mine = acc[1];
+      if (F > 2 && lane == 2) mine = acc[2];
+      if constexpr (MODE == kSpmvY) {
+        if (lane < F) {
+          const double v = fm ? mine : 0.0;
+          y[base + lane] = v;
+          if (dotv) part[0] += v * e0;
+        }
+      } else if constexpr (MODE == kSpmvResid) {
+        if (lane < F) y[base + lane] = fm ? e0 - mine : 0.0;
+      } else {
+        const double rown = (lane < F && fm) ? e0 - mine : 0.0;
+        double rr[F];
 #pragma unroll
-          for (int c = 0; c < F; ++c) {
-            const double v = freem[base + c] ? acc[c] : 0.0;
-            y[base + c] = v;
-            if (dotv) part[0] += v * dotv[base + c];
-          }
-        } else {
-          double rr[F];
+        for (int d = 0; d < F; ++d) rr[d] = __shfl_sync(0xffffffffu, rown, d);
+        if (lane < F) {
+          double sacc = 0.0;
 #pragma unroll
-          for (int c = 0; c < F; ++c) rr[c] = freem[base + c] ? b[base + c] - acc[c] : 0.0;
-          if constexpr (MODE == kSpmvResid) {
-#pragma unroll
-            for (int c = 0; c < F; ++c) y[base + c] = rr[c];
-          } else {
-            const double* Di = dinv + static_cast<int64_t>(row) * FF;
-#pragma unroll
-            for (int c = 0; c < F; ++c) {
-              double sacc = 0.0;
-#pragma unroll
-              for (int d = 0; d < F; ++d) sacc += Di[c * F + d] * rr[d];
-              y[base + c] = freem[base + c] ? x[base + c] + omega * sacc : 0.0;
-            }
-          }
+          for (int d = 0; d < F; ++d) sacc += di[d] * rr[d];
+          y[base + lane] = fm ? e1 + omega * sacc : 0.0;
         }
       }
       __syncwarp();

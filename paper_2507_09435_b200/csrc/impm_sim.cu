@@ -11,6 +11,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -70,7 +71,8 @@ struct DBuf {
 
 constexpr int kThreads = 256;
 constexpr int kRedBlocks = 148 * 4;    // fixed partial count for deterministic reductions
-constexpr int kSpmvBlocks = 148 * 12;  // SpMV grid (4-warp CTAs, 8 resident per SM)
+constexpr int kSpmvBlocks = 148 * 8;   // SpMV grid: 4-warp CTAs, 8 resident per SM -> exactly one wave
+constexpr int kSpmvMaxBlocks = 148 * 32;
 inline unsigned blocks_for(int64_t n, int t = kThreads) { return static_cast<unsigned>(std::max<int64_t>(1, (n + t - 1) / t)); }
 
 template <int V>
@@ -215,6 +217,7 @@ struct Sim {
   double up_dt = 0.0, up_time = 0.0, up_rscale = 0.0;
   DBuf<double> uty;  // accumulated vertical displacement per particle (sorted order)
 
+  int spmv_blocks = kSpmvBlocks;
   // relative Krylov tolerance of the current solve (see newton_attempt)
   double cur_rtol = 1e-12;
 
@@ -363,7 +366,9 @@ struct Sim {
     st.ensure(1);
     dflag.ensure(4);
     sc.ensure(kNSlots);
-    partials.ensure(8 * kRedBlocks + kSpmvBlocks);
+    partials.ensure(8 * kRedBlocks + kSpmvMaxBlocks);
+    if (const char* e = std::getenv("IMPM_SPMV_BLOCKS"))  // tuning experiments only
+      spmv_blocks = std::max(1, std::min(kSpmvMaxBlocks, std::atoi(e)));
     sums.ensure(8);
     CK(cudaMallocHost(&h_st, sizeof(DevStatus)));
     CK(cudaMallocHost(&h_sc, sizeof(double) * kNSlots));
@@ -970,11 +975,11 @@ struct Sim {
     dispatch_df([&](auto Dc, auto Fc) {
       constexpr int DD = decltype(Dc)::value, FE = decltype(Fc)::value;
       constexpr int W = 4;
-      k_spmv<DD, FE, W><<<kSpmvBlocks, W * 32, 0, s>>>(g, act_list.p, n_act, vals.p, row_len, row_slots.p,
+      k_spmv<DD, FE, W><<<spmv_blocks, W * 32, 0, s>>>(g, act_list.p, n_act, vals.p, row_len, row_slots.p,
                                                       row_nzb.p, x, freem.p, y, dotv, parts, dflag.p); ++g_launches;
       CKL();
     });
-    if (parts) gsum(parts, kSpmvBlocks);
+    if (parts) gsum(parts, spmv_blocks);
   }
 
   template <int FF>
@@ -1000,13 +1005,13 @@ struct Sim {
     const int batch = ndg() < 20000 ? 16 : 4;
     int done = 0;
     double* partA = partials.p;
-    double* partB = partials.p + kSpmvBlocks;
+    double* partB = partials.p + spmv_blocks;
     for (int it = 0; !done;) {
       for (int i = 0; i < batch; ++i, ++it) {
         const int par = it & 1;
         spmv(kp.p, kq.p, kp.p, partA);
         Prof::Scope ps(&prof, kcKrylov);
-        k_cg_update2<FF><<<kRedBlocks, kThreads, 0, s>>>(N, act_idx.p, dinv.p, sc.p, dflag.p, par, partA, kSpmvBlocks,
+        k_cg_update2<FF><<<kRedBlocks, kThreads, 0, s>>>(N, act_idx.p, dinv.p, sc.p, dflag.p, par, partA, spmv_blocks,
                                                          x, kr.p, kz.p, kp.p, kq.p, partB); ++g_launches;
         gsum(partB, 2 * kRedBlocks);
         k_cg_p2<FF><<<kRedBlocks, kThreads, 0, s>>>(N, act_idx.p, sc.p, dflag.p, par, it, partB, kRedBlocks, rtol2,
@@ -1116,7 +1121,7 @@ struct Sim {
   void level_spmv(MgLevel& L, const double* x, double* y, const double* b, double omega, const double* dotv,
                   double* parts) {
     constexpr int W = 4;
-    k_spmv<DD, FE, W, MODE><<<kSpmvBlocks, W * 32, 0, s>>>(L.g, L.act_list, L.n_act, L.vals, L.row_len, L.row_slots,
+    k_spmv<DD, FE, W, MODE><<<spmv_blocks, W * 32, 0, s>>>(L.g, L.act_list, L.n_act, L.vals, L.row_len, L.row_slots,
                                                           L.row_nzb, x, L.freem, y, dotv, parts, dflag.p, b, L.dinv,
                                                           omega); ++g_launches;
     CKL();
@@ -1406,7 +1411,7 @@ struct Sim {
     }
     CK(cudaMemsetAsync(dflag.p, 0, sizeof(int), s));
     double* partA = partials.p;
-    double* partB = partials.p + kSpmvBlocks;
+    double* partB = partials.p + spmv_blocks;
     CK(cudaMemsetAsync(x, 0, sizeof(double) * n, s));
     CK(cudaMemcpyAsync(kr.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
     {
@@ -1431,7 +1436,7 @@ struct Sim {
         spmv(kp.p, kq.p, kp.p, partA);
         {
           Prof::Scope ps(&prof, kcKrylov);
-          k_cg_update_mg<FE><<<kRedBlocks, kThreads, 0, s>>>(N, act_idx.p, sc.p, dflag.p, par, partA, kSpmvBlocks, x,
+          k_cg_update_mg<FE><<<kRedBlocks, kThreads, 0, s>>>(N, act_idx.p, sc.p, dflag.p, par, partA, spmv_blocks, x,
                                                              kr.p, kp.p, kq.p, partB + kRedBlocks); ++g_launches;
           CKL();
         }
