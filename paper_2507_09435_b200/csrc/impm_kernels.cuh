@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "impm_math.cuh"
 
@@ -1259,9 +1260,22 @@ struct SpmvTab {
 // y = x + omega Dinv (b - A x); MODE 2: residual y = b - A x.
 enum SpmvMode { kSpmvY = 0, kSpmvJacobi = 1, kSpmvResid = 2 };
 
-template <int D, int F, int WARPS, int MODE = kSpmvY>
+// per-component chunk length of a compacted row: fp64 rows pad to 2 values
+// (double2 loads), fp32 rows to 4 (float4 loads); both 16-byte aligned
+template <class VT>
+__host__ __device__ constexpr int chunk_len(int nzb, int F) {
+  return sizeof(VT) == 8 ? cpad(nzb, F) : ((nzb * F + 3) & ~3);
+}
+template <class VT>
+__host__ __device__ constexpr int64_t row_len_of(int S, int F) {
+  return sizeof(VT) == 8 ? row_len_for(S, F) : static_cast<int64_t>(F) * chunk_len<VT>(S, F);
+}
+
+// VT = double: the Jacobian itself; VT = float: the preconditioner's copy of
+// a level matrix (values rounded once, vectors and sums stay fp64)
+template <int D, int F, int WARPS, int MODE = kSpmvY, class VT = double>
 __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC g, const int* __restrict__ act_list, int n_act,
-                                                     const double* __restrict__ vals, int64_t row_len,
+                                                     const VT* __restrict__ vals, int64_t row_len,
                                                      const uint8_t* __restrict__ row_slots,
                                                      const int* __restrict__ row_nzb,
                                                      const double* __restrict__ x, const uint8_t* __restrict__ freem,
@@ -1271,12 +1285,18 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
                                                      const double* __restrict__ dinv = nullptr, double omega = 0.0) {
   constexpr int S = ipow_c(5, D);
   constexpr int FF = F * F;
-  constexpr int XS = cpad(S, F);
+  constexpr int XS = chunk_len<VT>(S, F);
+  constexpr int VW = 16 / sizeof(VT);  // values per 16-byte load
+  constexpr int TAIL_UNROLL = sizeof(VT) == 8 ? 4 : 2;
+  using V16 = typename std::conditional<sizeof(VT) == 8, double2, float4>::type;
   // double2 per lane buffered ahead of the x gathers (the Jacobi sweep keeps
   // its Dinv row and rhs in registers too: smaller head under the 64-reg cap)
-  constexpr int NB = MODE == kSpmvJacobi ? 4 : 6;
+  // fp32 rows carry half the bytes (~5 float4 per lane at 73 blocks/row)
+  constexpr int NB = sizeof(VT) == 8 ? (MODE == kSpmvJacobi ? 4 : 6) : (MODE == kSpmvJacobi ? 4 : 6);
   __shared__ int offt[S];
-  __shared__ __align__(16) double xs_all[WARPS][XS];
+  // x neighbourhood staged in the matrix precision (fp32 copies: products in
+  // fp32, each 4-term partial added to the fp64 row sum)
+  __shared__ __align__(16) VT xs_all[WARPS][XS];
   for (int sl = threadIdx.x; sl < S; sl += blockDim.x) {
     int rs = sl, off = 0;
 #pragma unroll
@@ -1290,7 +1310,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
   double part[1] = {0.0};
   if (done == nullptr || *done == 0) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    double* xs = xs_all[warp];
+    VT* xs = xs_all[warp];
     // contiguous row chunks per CTA: consecutive rows share 4/5 of their x
     // neighbourhood, so the x gathers of a chunk hit in this SM's L1
     constexpr int CH = 16 * WARPS;
@@ -1299,8 +1319,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
     for (int row = ci * CH + warp; row < min(n_act, (ci + 1) * CH); row += WARPS) {
       const int k = act_list[row];
       const int nzb = row_nzb[row];
-      const int cp = cpad(nzb, F);
-      const int h = cp >> 1, tot2 = F * h;
+      const int cp = chunk_len<VT>(nzb, F);
+      const int h = cp / VW, tot2 = F * h;
       const int64_t base = static_cast<int64_t>(k) * F;
       // 0. epilogue operands go in flight first: lane c < F holds component
       //    c's free mask, its dot / rhs operand, its own x and row c of Dinv
@@ -1324,29 +1344,34 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
       }
       // 1. the first NB double2 per lane of the row (independent of x) go in
       //    flight before the x gathers
-      const double2* rv = reinterpret_cast<const double2*>(vals + static_cast<int64_t>(row) * row_len);
-      double2 buf[NB];
+      const V16* rv = reinterpret_cast<const V16*>(vals + static_cast<int64_t>(row) * row_len);
+      V16 buf[NB];
 #pragma unroll
       for (int t = 0; t < NB; ++t) {
         const int j2 = lane + 32 * t;
-        buf[t] = j2 < tot2 ? __ldcs(rv + j2) : make_double2(0.0, 0.0);  // streamed once: evict-first
+        buf[t] = j2 < tot2 ? __ldcs(rv + j2) : V16{};  // streamed once: evict-first
       }
       // 2. stage the x records of the stored neighbours
       const uint8_t* rsl = row_slots + static_cast<int64_t>(row) * S;
       for (int pos = lane; pos < nzb; pos += 32) {
         const int64_t nb = static_cast<int64_t>(k + offt[rsl[pos]]) * F;
 #pragma unroll
-        for (int d = 0; d < F; ++d) xs[pos * F + d] = __ldg(x + nb + d);
+        for (int d = 0; d < F; ++d) xs[pos * F + d] = static_cast<VT>(__ldg(x + nb + d));
       }
-      if (lane == 0 && cp != nzb * F) xs[nzb * F] = 0.0;
+      if (lane < cp - nzb * F) xs[nzb * F + lane] = VT(0);
       __syncwarp();
       // 3. component-major dot products (buffered head, streamed tail)
       double acc[3] = {0.0, 0.0, 0.0};
-      const double2* xv = reinterpret_cast<const double2*>(xs);
-      auto consume = [&](int j2, const double2 v) {
+      const V16* xv = reinterpret_cast<const V16*>(xs);
+      auto consume = [&](int j2, const V16 v) {
         const int c = F == 1 ? 0 : (F == 2 ? (j2 >= h) : (j2 >= h) + (j2 >= 2 * h));
-        const double2 xx = xv[j2 - c * h];
-        const double p = fma(v.x, xx.x, v.y * xx.y);
+        double p;
+        const V16 xx = xv[j2 - c * h];
+        if constexpr (sizeof(VT) == 8) {
+          p = fma(v.x, xx.x, v.y * xx.y);
+        } else {
+          p = static_cast<double>(fmaf(v.x, xx.x, fmaf(v.y, xx.y, fmaf(v.z, xx.z, v.w * xx.w))));
+        }
         acc[0] += c == 0 ? p : 0.0;
         if (F > 1) acc[1] += c == 1 ? p : 0.0;
         if (F > 2) acc[2] += c == 2 ? p : 0.0;
@@ -1356,7 +1381,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
         const int j2 = lane + 32 * t;
         if (j2 < tot2) consume(j2, buf[t]);
       }
-#pragma unroll 4
+#pragma unroll TAIL_UNROLL
       for (int j2 = lane + 32 * NB; j2 < tot2; j2 += 32) consume(j2, __ldcs(rv + j2));
       // butterfly: every lane holds the row sums; lane c < F finishes component c
 #pragma unroll
@@ -1389,6 +1414,23 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
     }
   }
   if (partials) block_sum_store<1>(part, partials);
+}
+
+// fp32 copy of a compacted level matrix for the preconditioner (one pass per
+// assembly / Galerkin product: read 8 B + write 4 B per stored value)
+template <int F>
+__global__ void k_vals_to_f32(int n_act, const int* __restrict__ row_nzb, const double* __restrict__ vals,
+                              int64_t row_len, float* __restrict__ v32, int64_t row_len32) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int row = warp; row < n_act; row += nw) {
+    const int nzb = row_nzb[row];
+    const int cp = chunk_len<double>(nzb, F), cq = chunk_len<float>(nzb, F);
+    const double* src = vals + static_cast<int64_t>(row) * row_len;
+    float* dst = v32 + static_cast<int64_t>(row) * row_len32;
+    for (int c = 0; c < F; ++c)
+      for (int j = lane; j < cq; j += 32) dst[c * cq + j] = j < nzb * F ? static_cast<float>(src[c * cp + j]) : 0.0f;
+  }
 }
 
 // ------------------------------------------------------- K7 PCG vectors --

@@ -146,6 +146,7 @@ struct MgLevel {
   DBuf<int> act_flag_b, act_scan_b, act_idx_b, act_list_b, row_nzb_b;
   DBuf<uint8_t> freem_b, row_slots_b;
   DBuf<double> vals_b, dinv_b;
+  DBuf<float> vals32_b;          // fp32 copy for the smoother / residual SpMVs
   DBuf<double> xa, xb, r, bvec;  // level vectors (grid layout)
   // views
   const int* act_idx = nullptr;
@@ -154,6 +155,8 @@ struct MgLevel {
   const uint8_t* freem = nullptr;
   const uint8_t* row_slots = nullptr;
   const double* vals = nullptr;
+  const float* vals32 = nullptr;
+  int64_t row_len32 = 0;
   const double* dinv = nullptr;
   double* x = nullptr;  // current iterate (ping-pong between xa / xb)
   double* t = nullptr;
@@ -218,6 +221,10 @@ struct Sim {
   DBuf<double> uty;  // accumulated vertical displacement per particle (sorted order)
 
   int spmv_blocks = kSpmvBlocks;
+  // the MG preconditioner streams fp32 copies of its level matrices (the
+  // outer Krylov SpMV stays fp64, so the solve tolerance is unaffected)
+  bool mg_f32 = true;
+  DBuf<float> vals32;
   // relative Krylov tolerance of the current solve (see newton_attempt)
   double cur_rtol = 1e-12;
 
@@ -367,6 +374,7 @@ struct Sim {
     dflag.ensure(4);
     sc.ensure(kNSlots);
     partials.ensure(8 * kRedBlocks + kSpmvMaxBlocks);
+    if (const char* e = std::getenv("IMPM_MG_F64")) mg_f32 = std::atoi(e) == 0;  // A/B experiments only
     if (const char* e = std::getenv("IMPM_SPMV_BLOCKS"))  // tuning experiments only
       spmv_blocks = std::max(1, std::min(kSpmvMaxBlocks, std::atoi(e)));
     sums.ensure(8);
@@ -1121,9 +1129,15 @@ struct Sim {
   void level_spmv(MgLevel& L, const double* x, double* y, const double* b, double omega, const double* dotv,
                   double* parts) {
     constexpr int W = 4;
-    k_spmv<DD, FE, W, MODE><<<spmv_blocks, W * 32, 0, s>>>(L.g, L.act_list, L.n_act, L.vals, L.row_len, L.row_slots,
-                                                          L.row_nzb, x, L.freem, y, dotv, parts, dflag.p, b, L.dinv,
-                                                          omega); ++g_launches;
+    if (mg_f32)
+      k_spmv<DD, FE, W, MODE, float><<<spmv_blocks, W * 32, 0, s>>>(L.g, L.act_list, L.n_act, L.vals32, L.row_len32,
+                                                                   L.row_slots, L.row_nzb, x, L.freem, y, dotv, parts,
+                                                                   dflag.p, b, L.dinv, omega);
+    else
+      k_spmv<DD, FE, W, MODE><<<spmv_blocks, W * 32, 0, s>>>(L.g, L.act_list, L.n_act, L.vals, L.row_len, L.row_slots,
+                                                            L.row_nzb, x, L.freem, y, dotv, parts, dflag.p, b, L.dinv,
+                                                            omega);
+    ++g_launches;
     CKL();
   }
 
@@ -1152,6 +1166,16 @@ struct Sim {
     L0->row_slots = row_slots.p;
     L0->vals = vals.p;
     L0->dinv = dinv.p;
+    if (mg_f32) {
+      L0->row_len32 = row_len_of<float>(S, FE);
+      vals32.ensure(std::max<int64_t>(1, static_cast<int64_t>(n_act) * L0->row_len32));
+      L0->vals32 = vals32.p;
+      if (n_act > 0) {
+        k_vals_to_f32<FE><<<kSpmvBlocks, 128, 0, s>>>(n_act, row_nzb.p, vals.p, row_len, vals32.p, L0->row_len32);
+        ++g_launches;
+        CKL();
+      }
+    }
     mg.push_back(std::move(L0));
     mg_stored_blocks = 0;
     const int coarsest_max = 200;  // unknowns solved densely at the bottom
@@ -1216,6 +1240,17 @@ struct Sim {
               C->row_nzb_b.p, C->freem_b.p, C->dinv_b.p, mg_nzb.p);
           ++g_launches;
           CKL();
+        }
+        if (mg_f32) {
+          C->row_len32 = row_len_of<float>(S, FE);
+          C->vals32_b.ensure(std::max<int64_t>(1, static_cast<int64_t>(na) * C->row_len32));
+          C->vals32 = C->vals32_b.p;
+          if (na > 0) {
+            k_vals_to_f32<FE><<<kSpmvBlocks, 128, 0, s>>>(na, C->row_nzb_b.p, C->vals_b.p, C->row_len,
+                                                          C->vals32_b.p, C->row_len32);
+            ++g_launches;
+            CKL();
+          }
         }
       }
       mg.push_back(std::move(C));
