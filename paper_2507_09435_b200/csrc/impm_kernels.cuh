@@ -1035,7 +1035,11 @@ __global__ void __launch_bounds__(WARPS * 32) k_assemble_bins(
 // are staged in shared memory with all loads in flight at once, so the
 // per-particle loop (H_k = g^k . A_p, then the lane-owned block pairs) runs
 // from shared memory only.
-template <int D, int SHAPE, int PPL, int WARPS, int PCH>
+//
+// SYM: the single-field J is symmetric (hyperelastic / associative J2: the
+// per-particle tangent has major symmetry), so only blocks with l >= k are
+// computed and the transpose is mirrored into row l: ~45% fewer task rounds.
+template <int D, int SHAPE, int PPL, int WARPS, int PCH, bool SYM = false>
 __global__ void __launch_bounds__(WARPS * 32) k_assemble_bins_staged(
     GridC g, const double* __restrict__ pd, int64_t cap, const double* __restrict__ xs,
     const int* __restrict__ bin_start, const uint8_t* __restrict__ bflag, const double* __restrict__ A,
@@ -1067,15 +1071,36 @@ __global__ void __launch_bounds__(WARPS * 32) k_assemble_bins_staged(
 #pragma unroll
     for (int a = 0; a < D; ++a) cn[a] = 2 + ((fl >> a) & 1);
     const int nk = cn[0] * cn[1] * cn[2];
-    // lane task = (row node k, run of PPL column nodes l0..l0+PPL-1)
+    // lane task = (row node k, run of PPL column nodes l0..l0+PPL-1); SYM:
+    // runs start at l = k (row k has ceil((nk - k) / PPL) runs)
     const int nchunk = (nk + PPL - 1) / PPL;
-    const int ntasks = nk * nchunk;
+    int ntasks = nk * nchunk;
+    if constexpr (SYM) {
+      ntasks = 0;
+      for (int k = 0; k < nk; ++k) ntasks += (nk - k + PPL - 1) / PPL;
+    }
+    // (row, first column) of task t
+    auto task_of = [&](int t, int& k_out, int& l_out) {
+      if constexpr (SYM) {
+        int k = 0, n = (nk + PPL - 1) / PPL;
+        while (t >= n) {
+          t -= n;
+          ++k;
+          n = (nk - k + PPL - 1) / PPL;
+        }
+        k_out = k;
+        l_out = k + t * PPL;
+      } else {
+        k_out = t / nchunk;
+        l_out = (t - k_out * nchunk) * PPL;
+      }
+    };
     const int p0 = bin_start[b], p1 = bin_start[b + 1];
     for (int r0 = 0; r0 < ntasks; r0 += 32) {
       const int task = r0 + lane;
       const bool has_task = task < ntasks;
-      const int tk = has_task ? task / nchunk : 0;
-      const int tl0 = has_task ? (task - tk * nchunk) * PPL : nk;
+      int tk = 0, tl0 = nk;
+      if (has_task) task_of(task, tk, tl0);
       double acc[PPL][DD];
 #pragma unroll
       for (int t = 0; t < PPL; ++t)
@@ -1120,9 +1145,14 @@ __global__ void __launch_bounds__(WARPS * 32) k_assemble_bins_staged(
           for (int a = 0; a < D; ++a) Gs[warp][pl][k][a] = gk[a];
         }
         __syncwarp();
+        // this round's lanes use row nodes [k_lo, k_hi] only (~5 of 27)
+        int k_lo, k_hi, dummy;
+        task_of(r0, k_lo, dummy);
+        task_of(min(r0 + 31, ntasks - 1), k_hi, dummy);
+        const int nh = (k_hi - k_lo + 1) * D3;
         for (int pl = 0; pl < np; ++pl) {
           const double* Ap = &As[warp][pl * NA];
-          for (int e = lane; e < nk * D3; e += 32) {
+          for (int e = k_lo * D3 + lane; e < k_lo * D3 + nh; e += 32) {
             const int k = e / D3, cdf = e - k * D3, c = cdf / DD, df = cdf - c * DD;
             double sacc = 0.0;
 #pragma unroll
@@ -1182,6 +1212,34 @@ __global__ void __launch_bounds__(WARPS * 32) k_assemble_bins_staged(
             for (int c = 0; c < D; ++c)
 #pragma unroll
               for (int d = 0; d < D; ++d) rv[c * cp + d] += acc[t][c * D + d];
+          }
+        }
+        if constexpr (SYM) {
+          // mirrored blocks: row l, column k, K_lk = K_kl^T
+#pragma unroll
+          for (int t = 0; t < PPL; ++t) {
+            const int l = tl0 + t;
+            if (l >= nk || l == tk) continue;
+            int ll[3] = {0, 0, 0}, rl = l, nodel = 0, sl = 0;
+#pragma unroll
+            for (int a = D - 1; a >= 0; --a) {
+              ll[a] = rl % cn[a];
+              rl /= cn[a];
+            }
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+              nodel += (bidx[a] + ll[a]) * g.stride[a];
+              sl = sl * 5 + (lk[a] - ll[a] + 2);
+            }
+            const int rowl = act_idx[nodel];
+            if (rowl < 0) continue;
+            const unsigned* ml = row_mask + static_cast<int64_t>(rowl) * 4;
+            const int cpl = cpad(row_nzb[rowl], D);
+            double* rv = vals + static_cast<int64_t>(rowl) * row_len + mask_pos(ml, sl) * D;
+#pragma unroll
+            for (int c = 0; c < D; ++c)
+#pragma unroll
+              for (int d = 0; d < D; ++d) rv[c * cpl + d] += acc[t][d * D + c];
           }
         }
       }

@@ -964,9 +964,17 @@ struct Sim {
           const int nbins = nb[0] * nb[1] * nb[2];
           if (nbins == 0) continue;
           constexpr int WS = 4;
-          k_assemble_bins_staged<DD, SH, (DD == 3 ? 3 : PPL), WS, 4><<<std::min<unsigned>(blocks_for(nbins, WS), 148 * 32), WS * 32, 0, s>>>(
-              g, pd.p, cap, xs.p, bin_start.p, bflag.p, Atan.p, act_idx.p, row_mask.p, row_nzb.p, vals.p, row_len,
-              cc[0], cc[1], cc[2], nb[0], nb[1], nb[2]); ++g_launches;
+          const unsigned grid = std::min<unsigned>(blocks_for(nbins, WS), 148 * 32);
+          // J is symmetric except under non-associative Drucker-Prager flow
+          if (mat.kind != kDruckerPrager)
+            k_assemble_bins_staged<DD, SH, (DD == 3 ? 3 : PPL), WS, 4, true><<<grid, WS * 32, 0, s>>>(
+                g, pd.p, cap, xs.p, bin_start.p, bflag.p, Atan.p, act_idx.p, row_mask.p, row_nzb.p, vals.p, row_len,
+                cc[0], cc[1], cc[2], nb[0], nb[1], nb[2]);
+          else
+            k_assemble_bins_staged<DD, SH, (DD == 3 ? 3 : PPL), WS, 4, false><<<grid, WS * 32, 0, s>>>(
+                g, pd.p, cap, xs.p, bin_start.p, bflag.p, Atan.p, act_idx.p, row_mask.p, row_nzb.p, vals.p, row_len,
+                cc[0], cc[1], cc[2], nb[0], nb[1], nb[2]);
+          ++g_launches;
         }
         k_diag_inverse<DD><<<blocks_for(n_act), kThreads, 0, s>>>(n_act, act_list.p, freem.p, row_mask.p, row_nzb.p,
                                                                    vals.p, row_len, dinv.p); ++g_launches;
