@@ -179,6 +179,7 @@ struct Sim {
   int64_t cap = 0;
   int ND = 0;
   DBuf<double> pd, pd_tmp, xs, bext, Pst, Atan;
+  DBuf<double> io_staging;  // AoS staging of particle upload / download
   DBuf<int> orig, orig_tmp, key, sup, rank, perm, bin_count, bin_start;
   // grid / dofs
   DBuf<uint8_t> fixed, freem;
@@ -446,7 +447,7 @@ struct Sim {
     orig.ensure(cap);
     ensure_particle_buffers();
     CK(cudaMemsetAsync(uty.p, 0, sizeof(double) * cap, s));
-    DBuf<double> staging;
+    DBuf<double>& staging = io_staging;  // persistent: no 3 GB malloc/free per call
     staging.ensure(std::max<int64_t>(1, n * (stride / 8)));
     if (n > 0) {
       CK(cudaMemcpyAsync(staging.p, aos, n * stride, cudaMemcpyHostToDevice, s));
@@ -476,7 +477,7 @@ struct Sim {
     if (n != P) throw SimError(IMPM_ERR_CONFIG, "particle count mismatch");
     if (stride % 8 != 0 || stride < ND * 8) throw SimError(IMPM_ERR_CONFIG, "bad particle stride");
     if (n == 0) return;
-    DBuf<double> staging;
+    DBuf<double>& staging = io_staging;
     staging.ensure(n * (stride / 8));
     if (stride != ND * 8) CK(cudaMemcpyAsync(staging.p, aos, n * stride, cudaMemcpyHostToDevice, s));
     k_soa_to_aos<<<blocks_for(n), kThreads, 0, s>>>(pd.p, cap, P, ND, orig.p, staging.p, stride / 8); ++g_launches;
@@ -502,7 +503,7 @@ struct Sim {
     if (n != P) throw SimError(IMPM_ERR_CONFIG, "particle count mismatch");
     if (stride % 8 != 0 || stride < ND * 8) throw SimError(IMPM_ERR_CONFIG, "bad particle stride");
     if (n == 0) return;
-    DBuf<double> staging;
+    DBuf<double>& staging = io_staging;
     DBuf<long long> dids;
     staging.ensure(n * (stride / 8));
     dids.ensure(n);
