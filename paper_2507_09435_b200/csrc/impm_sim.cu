@@ -226,6 +226,12 @@ struct Sim {
   // outer Krylov SpMV stays fp64, so the solve tolerance is unaffected)
   bool mg_f32 = true;
   DBuf<float> vals32;
+  // coarse levels (Galerkin products, dense coarsest inverse) are kept for
+  // the later Newton iterations of a load step: the row structure is fixed
+  // within a step and J moves little, while the fine level always smooths
+  // with the current J
+  bool mg_reuse = true;
+  int mg_setup_step = -1;
   // relative Krylov tolerance of the current solve (see newton_attempt)
   double cur_rtol = 1e-12;
 
@@ -376,6 +382,7 @@ struct Sim {
     sc.ensure(kNSlots);
     partials.ensure(8 * kRedBlocks + kSpmvMaxBlocks);
     if (const char* e = std::getenv("IMPM_MG_F64")) mg_f32 = std::atoi(e) == 0;  // A/B experiments only
+    if (const char* e = std::getenv("IMPM_MG_REUSE")) mg_reuse = std::atoi(e) != 0;
     if (const char* e = std::getenv("IMPM_SPMV_BLOCKS"))  // tuning experiments only
       spmv_blocks = std::max(1, std::min(kSpmvMaxBlocks, std::atoi(e)));
     sums.ensure(8);
@@ -883,6 +890,7 @@ struct Sim {
     if (coupled) CK(cudaMemsetAsync(prev.p, 0, sizeof(double) * NF(), s));  // p_nodes_ = 0 (porous.cpp:70)
     matrix_valid = false;
     step_built = true;
+    mg_setup_step = -1;  // new row structure: rebuild the MG hierarchy
     sync();
   }
 
@@ -1154,6 +1162,16 @@ struct Sim {
   void mg_setup() {
     constexpr int S = ipow_c(5, DD);
     constexpr int FF = FE * FE;
+    if (mg_reuse && mg_setup_step == step_counter && !mg.empty() && mg[0]->n_act == n_act &&
+        mg[0]->vals == vals.p) {
+      if (mg_f32 && n_act > 0) {  // fine level: fp32 copy of the current J
+        k_vals_to_f32<FE><<<kSpmvBlocks, 128, 0, s>>>(n_act, row_nzb.p, vals.p, row_len, vals32.p, mg[0]->row_len32);
+        ++g_launches;
+        CKL();
+      }
+      return;
+    }
+    mg_setup_step = step_counter;
     // level objects (and their device buffers) persist across setups; only
     // growth reallocates
     std::vector<std::unique_ptr<MgLevel>> pool;
