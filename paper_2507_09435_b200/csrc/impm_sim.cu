@@ -81,11 +81,12 @@ using IC = std::integral_constant<int, V>;
 // ---------------------------------------------------------- profiling ---
 enum KClass {
   kcSort = 0, kcMass, kcDof, kcResP, kcResN, kcTangent, kcAssemble, kcSpmv, kcKrylov, kcCommit, kcMgSetup, kcVcycle,
-  kcGalerkin, kcMgPower, kcMgCoarsest, kcCount
+  kcGalerkin, kcMgPower, kcMgCoarsest, kcVcL0, kcVcL1, kcVcCoarse, kcCount
 };
 const char* kClassNames[kcCount] = {"support_sort", "node_mass", "dof_map", "residual_particles", "residual_nodes",
                                     "tangent",      "assemble",  "spmv",    "krylov_vector",      "commit",
-                                    "mg_setup",     "vcycle",    "galerkin", "mg_power",           "mg_coarsest"};
+                                    "mg_setup",     "vcycle",    "galerkin", "mg_power",           "mg_coarsest",
+                                    "vcycle_level0", "vcycle_level1", "vcycle_coarse"};
 
 struct Prof {
   bool on = false;
@@ -1300,7 +1301,10 @@ struct Sim {
     CK(cudaMemsetAsync(dflag.p, 0, sizeof(int), s));
     // lambda_max(Dinv A) moves little between the Newton iterations of one
     // load step: estimate it on the first setup of the step, then reuse
-    const bool need_power = mg_power_step != step_counter || mg_lam_host.size() != mg.size();
+    // ... and it moves little between load steps too: omega * lambda_est =
+    // 4 / 3.3 leaves a wide margin below the divergence limit 2, so the
+    // estimate is refreshed every 5 load steps (or when the depth changes)
+    const bool need_power = mg_power_step < 0 || step_counter - mg_power_step >= 5 || mg_lam_host.size() != mg.size();
     mg_lam.ensure(std::max<size_t>(mg.size(), 1));
     if (need_power) {
       Prof::Scope psp(&prof, kcMgPower);
@@ -1428,8 +1432,10 @@ struct Sim {
   template <int DD, int FE>
   void vcycle(size_t l, const double* b) {
     MgLevel& L = *mg[l];
+    const int lcls = l == 0 ? kcVcL0 : (l == 1 ? kcVcL1 : kcVcCoarse);  // nested sub-classes of "vcycle"
     if (l + 1 == mg.size()) {
       if (mg_dense_n > 0) {
+        Prof::Scope ps(&prof, kcVcCoarse);
         k_dense_apply<<<std::min<unsigned>(blocks_for(mg_dense_n, 128), 148), 128, 0, s>>>(
             mg_dense_n, FE, dflag.p, L.act_list, mg_dense.p, b, L.x); ++g_launches;
         CKL();
@@ -1437,20 +1443,24 @@ struct Sim {
       return;
     }
     const int nu = opt.mg_smooth > 0 ? opt.mg_smooth : 1;
-    // pre-smoothing from x = 0
-    k_jacobi0<FE><<<kRedBlocks, kThreads, 0, s>>>(L.n_act, dflag.p, L.act_list, L.dinv, L.freem, L.omega, b, L.x);
-    ++g_launches;
-    CKL();
-    for (int i = 1; i < nu; ++i) {
-      level_spmv<DD, FE, kSpmvJacobi>(L, L.x, L.t, b, L.omega, nullptr, nullptr);
-      std::swap(L.x, L.t);
-    }
-    level_spmv<DD, FE, kSpmvResid>(L, L.x, L.r.p, b, 0.0, nullptr, nullptr);
     MgLevel& C = *mg[l + 1];
-    k_restrict<DD, FE><<<blocks_for(C.g.N), kThreads, 0, s>>>(L.g, C.g, dflag.p, L.r.p, C.freem, C.bvec.p);
-    ++g_launches;
-    CKL();
+    {
+      Prof::Scope ps(&prof, lcls);
+      // pre-smoothing from x = 0
+      k_jacobi0<FE><<<kRedBlocks, kThreads, 0, s>>>(L.n_act, dflag.p, L.act_list, L.dinv, L.freem, L.omega, b, L.x);
+      ++g_launches;
+      CKL();
+      for (int i = 1; i < nu; ++i) {
+        level_spmv<DD, FE, kSpmvJacobi>(L, L.x, L.t, b, L.omega, nullptr, nullptr);
+        std::swap(L.x, L.t);
+      }
+      level_spmv<DD, FE, kSpmvResid>(L, L.x, L.r.p, b, 0.0, nullptr, nullptr);
+      k_restrict<DD, FE><<<blocks_for(C.g.N), kThreads, 0, s>>>(L.g, C.g, dflag.p, L.r.p, C.freem, C.bvec.p);
+      ++g_launches;
+      CKL();
+    }
     vcycle<DD, FE>(l + 1, C.bvec.p);
+    Prof::Scope ps(&prof, lcls);
     k_prolong_add<DD, FE><<<blocks_for(L.g.N), kThreads, 0, s>>>(L.g, C.g, dflag.p, C.x, L.freem, L.x);
     ++g_launches;
     CKL();
@@ -1459,6 +1469,7 @@ struct Sim {
       std::swap(L.x, L.t);
     }
   }
+
 
   // MG-preconditioned CG (device-resident scalars, batched host checks)
   template <int DD, int FE>
