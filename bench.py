@@ -160,6 +160,17 @@ def make_sim(prob, device, profile, comm=None):
     return sim
 
 
+def ncu_traffic(name):
+    """DRAM bytes per launch of a kernel from the committed ncu --set full
+    capture (scripts/ncu_steady.sh -> profiles/r01/ncu_steady/traffic.json)."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01", "ncu_steady", "traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)[name]["traffic_bytes"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def spmv_bytes(info, D):
     """algorithmic bytes of one compacted box-BSR SpMV launch: the stored
     (structurally nonzero) block values + their slot ids, per-row act_list and
@@ -417,7 +428,9 @@ def main():
         "nnz_per_s": nnz_rate, "nnz_assembled": nnz,
         "roofline": {"bound": "hbm", "kernel": "k_spmv (compacted box-BSR, fine level of the MG-PCG solve)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak if achieved else None, "traffic": None,
+                     "frac": achieved / peak if achieved else None, "traffic": ncu_traffic("cg"),
+                     "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum per launch, ncu --set full of "
+                                       "the same kernel at cfg4 load step 2 (profiles/r01/ncu_steady/)",
                      "bytes_per_launch": byt, "avg_launch_ms": spmv_avg, "launches": spmv_n,
                      "peak_source": peak_kind},
         "profiled_step": {"newton_iterations": prof_rec.iterations, "krylov_iterations": prof_rec.krylov_iterations,
