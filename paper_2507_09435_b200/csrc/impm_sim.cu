@@ -235,6 +235,9 @@ struct Sim {
   int mg_setup_step = -1;
   // relative Krylov tolerance of the current solve (see newton_attempt)
   double cur_rtol = 1e-12;
+  // |r1| / r0 of the last converged load step (first-iteration forcing term)
+  double newton_ratio1 = -1.0;
+  double newton_eta_factor = 0.01;
 
   // slab decomposition along axis 0; comm == nullptr or a
   // single rank -> the plain single-GPU path
@@ -384,6 +387,7 @@ struct Sim {
     partials.ensure(8 * kRedBlocks + kSpmvMaxBlocks);
     if (const char* e = std::getenv("IMPM_MG_F64")) mg_f32 = std::atoi(e) == 0;  // A/B experiments only
     if (const char* e = std::getenv("IMPM_MG_REUSE")) mg_reuse = std::atoi(e) != 0;
+    if (const char* e = std::getenv("IMPM_ETA0_FACTOR")) newton_eta_factor = std::atof(e);  // A/B experiments
     if (const char* e = std::getenv("IMPM_SPMV_BLOCKS"))  // tuning experiments only
       spmv_blocks = std::max(1, std::min(kSpmvMaxBlocks, std::atoi(e)));
     sums.ensure(8);
@@ -1715,7 +1719,7 @@ struct Sim {
   void newton_attempt(double load_scale, impm_step_record* rec) {
     std::vector<double> rels;
     const auto t0 = std::chrono::steady_clock::now();
-    double diff_s = 0.0, solve_s = 0.0, res_s = 0.0, rnorm_prev = 0.0;
+    double diff_s = 0.0, solve_s = 0.0, res_s = 0.0, rnorm_prev = 0.0, ratio1_now = -1.0;
     int kry = 0, iters = 0;
     auto tres = std::chrono::steady_clock::now();
     const double r0 = residual_dev(u.p, load_scale, r.p);
@@ -1750,8 +1754,15 @@ struct Sim {
       // outcome; floor = krylov_rtol (1e-12).
       auto ts = std::chrono::steady_clock::now();
       axpbypcz(-1.0, r.p, 0.0, tmp2.p);
-      const double rcur = it == 1 ? r0 : rnorm_prev;
-      cur_rtol = std::min(1e-6, std::max(opt.krylov_rtol, 0.01 * opt.tol * r0 / std::max(rcur, 1e-300)));
+      if (it == 1) {
+        // first iteration: its linear error lands in r1 as <= eta r0, so eta =
+        // 1% of the contraction |r1| / r0 seen at the previous load step keeps
+        // r1 within ~1% of the exact-solve value (no history: 1% of tol)
+        const double ref = newton_ratio1 > 0.0 ? std::max(newton_ratio1, opt.tol) : opt.tol;
+        cur_rtol = std::min(1e-6, std::max(opt.krylov_rtol, newton_eta_factor * ref));
+      } else {
+        cur_rtol = std::min(1e-6, std::max(opt.krylov_rtol, 0.01 * opt.tol * r0 / std::max(rnorm_prev, 1e-300)));
+      }
       kry += solve_dev(tmp2.p, delta.p);
       cur_rtol = opt.krylov_rtol;
       solve_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - ts).count();
@@ -1769,6 +1780,7 @@ struct Sim {
           std::swap(r.p, rtry.p);
           rnorm_prev = rnorm;
           accepted = true;
+          if (it == 1) ratio1_now = rnorm / r0;
         } catch (const SimError& e) {
           if (e.code != IMPM_ERR_DOMAIN) throw;
         }
@@ -1781,6 +1793,7 @@ struct Sim {
       rels.push_back(rel);
       iters = it;
       if (rel <= opt.tol) {
+        newton_ratio1 = ratio1_now;
         if (opt.total_lagrangian) {
           have_uwarm = true;
           CK(cudaMemcpyAsync(prev.p, u.p, sizeof(double) * NF(), cudaMemcpyDeviceToDevice, s));
