@@ -238,6 +238,7 @@ struct Sim {
   // |r1| / r0 of the last converged load step (first-iteration forcing term)
   double newton_ratio1 = -1.0;
   double newton_eta_factor = 0.01;
+  int mg_smooth_env = 0;
 
   // slab decomposition along axis 0; comm == nullptr or a
   // single rank -> the plain single-GPU path
@@ -388,6 +389,7 @@ struct Sim {
     if (const char* e = std::getenv("IMPM_MG_F64")) mg_f32 = std::atoi(e) == 0;  // A/B experiments only
     if (const char* e = std::getenv("IMPM_MG_REUSE")) mg_reuse = std::atoi(e) != 0;
     if (const char* e = std::getenv("IMPM_ETA0_FACTOR")) newton_eta_factor = std::atof(e);  // A/B experiments
+    if (const char* e = std::getenv("IMPM_MG_SMOOTH")) mg_smooth_env = std::atoi(e);
     if (const char* e = std::getenv("IMPM_SPMV_BLOCKS"))  // tuning experiments only
       spmv_blocks = std::max(1, std::min(kSpmvMaxBlocks, std::atoi(e)));
     sums.ensure(8);
@@ -1446,7 +1448,7 @@ struct Sim {
       }
       return;
     }
-    const int nu = opt.mg_smooth > 0 ? opt.mg_smooth : 1;
+    const int nu = mg_smooth_env > 0 ? mg_smooth_env : (opt.mg_smooth > 0 ? opt.mg_smooth : 1);
     MgLevel& C = *mg[l + 1];
     {
       Prof::Scope ps(&prof, lcls);
