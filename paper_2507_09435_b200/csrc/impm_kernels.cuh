@@ -1331,7 +1331,8 @@ __host__ __device__ constexpr int64_t row_len_of(int S, int F) {
 
 // VT = double: the Jacobian itself; VT = float: the preconditioner's copy of
 // a level matrix (values rounded once, vectors and sums stay fp64)
-template <int D, int F, int WARPS, int MODE = kSpmvY, class VT = double>
+// RPW: rows per warp and chunk (0: the runtime rows_per_warp argument)
+template <int D, int F, int WARPS, int MODE = kSpmvY, class VT = double, int RPW = 16>
 __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC g, const int* __restrict__ act_list, int n_act,
                                                      const VT* __restrict__ vals, int64_t row_len,
                                                      const uint8_t* __restrict__ row_slots,
@@ -1340,7 +1341,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
                                                      double* __restrict__ y, const double* __restrict__ dotv,
                                                      double* __restrict__ partials, const int* __restrict__ done,
                                                      const double* __restrict__ b = nullptr,
-                                                     const double* __restrict__ dinv = nullptr, double omega = 0.0) {
+                                                     const double* __restrict__ dinv = nullptr, double omega = 0.0,
+                                                     int rows_per_warp = 16) {
   constexpr int S = ipow_c(5, D);
   constexpr int FF = F * F;
   constexpr int XS = chunk_len<VT>(S, F);
@@ -1370,8 +1372,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     VT* xs = xs_all[warp];
     // contiguous row chunks per CTA: consecutive rows share 4/5 of their x
-    // neighbourhood, so the x gathers of a chunk hit in this SM's L1
-    constexpr int CH = 16 * WARPS;
+    // neighbourhood, so the x gathers of a chunk hit in this SM's L1 (small
+    // coarse levels use short chunks so that every warp gets a row)
+    const int CH = (RPW > 0 ? RPW : rows_per_warp) * WARPS;
     const int nchunks = (n_act + CH - 1) / CH;
     for (int ci = blockIdx.x; ci < nchunks; ci += gridDim.x)
     for (int row = ci * CH + warp; row < min(n_act, (ci + 1) * CH); row += WARPS) {

@@ -1153,14 +1153,21 @@ struct Sim {
   void level_spmv(MgLevel& L, const double* x, double* y, const double* b, double omega, const double* dotv,
                   double* parts) {
     constexpr int W = 4;
+    // rows go out in 64-row chunks: small coarse levels need few CTAs (a
+    // caller asking for dot partials keeps the full, fixed-size grid)
+    // rows per warp: 16 on big levels (L1 reuse of x), fewer on small ones so
+    // that all 148 x 32 warps get work instead of a few walking long chunks
+    const int rpw = std::max(1, std::min(16, (L.n_act + spmv_blocks * W - 1) / (spmv_blocks * W)));
+    const unsigned grid = parts ? spmv_blocks
+                                : static_cast<unsigned>(std::max(1, std::min(spmv_blocks, (L.n_act + rpw * W - 1) / (rpw * W))));
     if (mg_f32)
-      k_spmv<DD, FE, W, MODE, float><<<spmv_blocks, W * 32, 0, s>>>(L.g, L.act_list, L.n_act, L.vals32, L.row_len32,
+      k_spmv<DD, FE, W, MODE, float, 0><<<grid, W * 32, 0, s>>>(L.g, L.act_list, L.n_act, L.vals32, L.row_len32,
                                                                    L.row_slots, L.row_nzb, x, L.freem, y, dotv, parts,
-                                                                   dflag.p, b, L.dinv, omega);
+                                                                   dflag.p, b, L.dinv, omega, rpw);
     else
-      k_spmv<DD, FE, W, MODE><<<spmv_blocks, W * 32, 0, s>>>(L.g, L.act_list, L.n_act, L.vals, L.row_len, L.row_slots,
+      k_spmv<DD, FE, W, MODE, double, 0><<<grid, W * 32, 0, s>>>(L.g, L.act_list, L.n_act, L.vals, L.row_len, L.row_slots,
                                                             L.row_nzb, x, L.freem, y, dotv, parts, dflag.p, b, L.dinv,
-                                                            omega);
+                                                            omega, rpw);
     ++g_launches;
     CKL();
   }
