@@ -1489,8 +1489,17 @@ __global__ void k_vals_to_f32(int n_act, const int* __restrict__ row_nzb, const 
     const int cp = chunk_len<double>(nzb, F), cq = chunk_len<float>(nzb, F);
     const double* src = vals + static_cast<int64_t>(row) * row_len;
     float* dst = v32 + static_cast<int64_t>(row) * row_len32;
-    for (int c = 0; c < F; ++c)
-      for (int j = lane; j < cq; j += 32) dst[c * cq + j] = j < nzb * F ? static_cast<float>(src[c * cp + j]) : 0.0f;
+    // pairs: both chunk starts are 16-byte aligned (cp even, cq % 4 == 0)
+    const int h2 = cq >> 1;  // float2 per fp32 chunk
+    for (int e = lane; e < F * h2; e += 32) {
+      const int c = e / h2, j2 = e - c * h2;
+      float2 o = make_float2(0.0f, 0.0f);
+      if (2 * j2 < nzb * F) {  // pads (fp64 or fp32) become exact zeros
+        const double2 v = __ldcs(reinterpret_cast<const double2*>(src + c * cp) + j2);
+        o = make_float2(static_cast<float>(v.x), 2 * j2 + 1 < nzb * F ? static_cast<float>(v.y) : 0.0f);
+      }
+      reinterpret_cast<float2*>(dst + c * cq)[j2] = o;
+    }
   }
 }
 
