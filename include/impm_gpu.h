@@ -255,6 +255,32 @@ impm_status impm_sim_slab_info(impm_sim* sim, int64_t* n_dofs_global, int64_t* d
  * neighbours). */
 impm_status impm_sim_apply_jacobian(impm_sim* sim, const double* u, double load_scale, const double* x, double* y);
 
+/* ---------------------------------------------------------------------------
+ * Link-level seam: general CSR matrices (impm::CsrMatrix, sparse.hpp:11-31;
+ * n x n, int64 row_ptr[n+1], int32 column indices sorted and unique per row).
+ * Host arrays in and out; the work runs on `device`.
+ * ------------------------------------------------------------------------- */
+/* impm::sparse_lu_solve (sparse.hpp:43, src/linear_solver.cpp:11-88): x = A^-1 b
+ * with the reference's row equilibration, <= 2 refinement sweeps while the
+ * normwise backward error exceeds 1e-14, and IMPM_ERR_LINEAR_SOLVER with the
+ * reference's message texts ("empty matrix row i", "singular factorization: ...",
+ * "solution backward error ... exceeds 1e-10; ...", "right-hand side size does
+ * not match the matrix dimension"). Dense device LU for n <= 2048, Jacobi-
+ * right-preconditioned GMRES above (*iterations = its Krylov count, may be NULL). */
+impm_status impm_sparse_lu_solve(int32_t n, const int64_t* row_ptr, const int32_t* cols, const double* vals,
+                                 const double* b, int64_t b_len, double* x /*[n]*/, int32_t device,
+                                 int32_t* iterations);
+/* CsrMatrix::multiply (src/sparse.cpp:44-53): y = A x, bitwise the reference's
+ * in-order row sums. */
+impm_status impm_csr_multiply(int32_t n, const int64_t* row_ptr, const int32_t* cols, const double* vals,
+                              const double* x, double* y /*[n]*/, int32_t device);
+/* CsrMatrix::transposed (src/sparse.cpp:55-70): same nnz, columns sorted. */
+impm_status impm_csr_transposed(int32_t n, const int64_t* row_ptr, const int32_t* cols, const double* vals,
+                                int64_t* t_row_ptr /*[n+1]*/, int32_t* t_cols /*[nnz]*/, double* t_vals /*[nnz]*/,
+                                int32_t device);
+/* message of the last failed impm_sparse_lu_solve / impm_csr_* call on this thread */
+const char* impm_csr_last_error(void);
+
 #ifdef __cplusplus
 }
 #endif

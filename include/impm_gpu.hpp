@@ -30,7 +30,9 @@
 #include "impm/errors.hpp"
 #include "impm/grid.hpp"
 #include "impm/particle.hpp"
+#include "impm/sparse.hpp"
 #endif
+#include <span>
 
 namespace impm_gpu {
 
@@ -43,6 +45,7 @@ using impm::NonConvergenceError;
 using impm::OutOfDomainError;
 using impm::SeedingFault;
 using impm::UnsupportedOperation;
+using impm::CsrMatrix;
 template <int D>
 using Particle = impm::Particle<D>;
 #else
@@ -142,6 +145,14 @@ struct StepRecord {  // mpm_solver.hpp:38-46
   int krylov_iterations = 0;
 };
 
+#ifndef IMPM_GPU_REFERENCE_TYPES
+struct CsrMatrix {  // sparse.hpp:11-31 (fields only)
+  int n = 0;
+  std::vector<std::int64_t> row_ptr;
+  std::vector<std::int32_t> cols;
+  std::vector<double> vals;
+};
+#endif
 struct DofMap {  // grid.hpp:66-93
   int n_fields = 0, n_dofs = 0;
   std::vector<std::int32_t> dof_of, node_of, field_of;
@@ -320,5 +331,42 @@ class MpmSim {
   impm_sim* h_ = nullptr;
   std::vector<char> shadow_;
 };
+
+// ---- link-level seam (sparse.hpp:43): drop-in for impm::sparse_lu_solve ----
+namespace detail {
+inline void check_csr(impm_status st) {
+  if (st == IMPM_OK) return;
+  const std::string msg = impm_csr_last_error();
+  if (st == IMPM_ERR_LINEAR_SOLVER) throw LinearSolverError(msg);
+  if (st == IMPM_ERR_CONFIG) throw ConfigError(msg);
+  throw Error(msg);
+}
+}  // namespace detail
+
+// impm::sparse_lu_solve (src/linear_solver.cpp:11-88) on the GPU.
+inline std::vector<double> sparse_lu_solve(const CsrMatrix& A, std::span<const double> b, int device = 0) {
+  std::vector<double> x(static_cast<std::size_t>(A.n));
+  if (A.n == 0) return x;
+  detail::check_csr(impm_sparse_lu_solve(A.n, A.row_ptr.data(), A.cols.data(), A.vals.data(), b.data(),
+                                         static_cast<std::int64_t>(b.size()), x.data(), device, nullptr));
+  return x;
+}
+// CsrMatrix::multiply (src/sparse.cpp:44-53) on the GPU, bitwise the reference's sums.
+inline std::vector<double> csr_multiply(const CsrMatrix& A, std::span<const double> x, int device = 0) {
+  std::vector<double> y(static_cast<std::size_t>(A.n));
+  detail::check_csr(impm_csr_multiply(A.n, A.row_ptr.data(), A.cols.data(), A.vals.data(), x.data(), y.data(), device));
+  return y;
+}
+// CsrMatrix::transposed (src/sparse.cpp:55-70) on the GPU.
+inline CsrMatrix csr_transposed(const CsrMatrix& A, int device = 0) {
+  CsrMatrix t;
+  t.n = A.n;
+  t.row_ptr.assign(static_cast<std::size_t>(A.n) + 1, 0);
+  t.cols.resize(A.cols.size());
+  t.vals.resize(A.vals.size());
+  detail::check_csr(impm_csr_transposed(A.n, A.row_ptr.data(), A.cols.data(), A.vals.data(), t.row_ptr.data(),
+                                        t.cols.data(), t.vals.data(), device));
+  return t;
+}
 
 }  // namespace impm_gpu

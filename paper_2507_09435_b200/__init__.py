@@ -11,6 +11,7 @@ include/impm_gpu.h.
 from .errors import (ConfigError, CudaError, DomainError, Error, LinearSolverError, NonConvergenceError,
                      OutOfDomainError, SeedingFault, UnsupportedOperation)
 from .particles import GridSpec, ParticleArray, particle_doubles, particle_fields, seed_box
+from .sparse import CsrMatrix, sparse_lu_solve
 from .sim import CoupledSim, DofMap, ElasticParams, MaterialSpec, MpmSim, PoroParams, SolverOptions, StepRecord
 
 __all__ = [
@@ -18,7 +19,7 @@ __all__ = [
     "OutOfDomainError", "SeedingFault", "UnsupportedOperation", "GridSpec", "ParticleArray", "particle_doubles",
     "particle_fields", "seed_box", "DofMap", "ElasticParams", "MaterialSpec", "MpmSim", "SolverOptions",
     "StepRecord", "gimp_weight_1d", "block_size", "CoupledSim", "PoroParams", "Config", "run_scenario",
-    "run_scenario_text", "bench_scenario",
+    "run_scenario_text", "bench_scenario", "CsrMatrix", "sparse_lu_solve",
 ]
 
 

@@ -120,6 +120,12 @@ _SIGNATURES = {
     "impm_sim_migrate": (c_int32, [c_void_p]),
     "impm_sim_slab_info": (c_int32, [c_void_p, _P(c_int64), _P(c_int64), _P(c_int32)]),
     "impm_sim_apply_jacobian": (c_int32, [c_void_p, c_void_p, c_double, c_void_p, c_void_p]),
+    # link-level seam: general CSR (sparse.hpp:11-43)
+    "impm_sparse_lu_solve": (c_int32, [c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_int32,
+                                       _P(c_int32)]),
+    "impm_csr_multiply": (c_int32, [c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int32]),
+    "impm_csr_transposed": (c_int32, [c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int32]),
+    "impm_csr_last_error": (ctypes.c_char_p, []),
 }
 
 # every symbol include/impm_gpu.h declares (checked by tests without a GPU)

@@ -2109,6 +2109,34 @@ thread_local std::string g_create_error;
 
 }  // namespace
 
+#include "impm_csr.cuh"
+
+namespace {
+thread_local std::string g_csr_error;
+
+// Runs one CSR call on `device` on a private stream; errors -> g_csr_error.
+template <class F>
+impm_status csr_call(int32_t device, F&& f) {
+  cudaStream_t s = nullptr;
+  try {
+    CK(cudaSetDevice(device));
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    f(s);
+    cudaStreamDestroy(s);
+    g_csr_error.clear();
+    return IMPM_OK;
+  } catch (const SimError& e) {
+    if (s) cudaStreamDestroy(s);
+    g_csr_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    if (s) cudaStreamDestroy(s);
+    g_csr_error = e.what();
+    return IMPM_ERR_CUDA;
+  }
+}
+}  // namespace
+
 // opaque communicator handle of the C ABI (include/impm_gpu.h)
 struct impm_comm {
   std::shared_ptr<Comm> c;
@@ -2561,5 +2589,53 @@ impm_status impm_sim_apply_jacobian(impm_sim* h, const double* uh, double load_s
   sim->prof.flush();
   API_END(sim)
 }
+
+// ---- link-level seam: impm::sparse_lu_solve / CsrMatrix (impm_csr.cuh) ----
+impm_status impm_sparse_lu_solve(int32_t n, const int64_t* row_ptr, const int32_t* cols, const double* vals,
+                                 const double* b, int64_t b_len, double* x, int32_t device, int32_t* iterations) {
+  if (n == 0) return IMPM_OK;  // linear_solver.cpp:12
+  if (b_len != n) {            // :13-14
+    g_csr_error = "right-hand side size does not match the matrix dimension";
+    return IMPM_ERR_LINEAR_SOLVER;
+  }
+  if (!row_ptr || !cols || !vals || !b || !x) {
+    g_csr_error = "null pointer argument";
+    return IMPM_ERR_CONFIG;
+  }
+  return csr_call(device, [&](cudaStream_t s) {
+    csr::LuSolver lu;
+    lu.A.upload(n, row_ptr, cols, vals, s);
+    lu.solve(b, x);
+    if (iterations) *iterations = lu.A.n <= csr::kDenseMax ? 0 : lu.krylov_iterations;
+  });
+}
+impm_status impm_csr_multiply(int32_t n, const int64_t* row_ptr, const int32_t* cols, const double* vals,
+                              const double* x, double* y, int32_t device) {
+  if (n == 0) return IMPM_OK;
+  return csr_call(device, [&](cudaStream_t s) {
+    csr::DevCsr A;
+    A.upload(n, row_ptr, cols, vals, s);
+    DBuf<double> dx, dy;
+    dx.ensure(n);
+    dy.ensure(n);
+    CK(cudaMemcpyAsync(dx.get(), x, n * sizeof(double), cudaMemcpyHostToDevice, s));
+    A.spmv<0>(dx.get(), dy.get());
+    CK(cudaMemcpyAsync(y, dy.get(), n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  });
+}
+impm_status impm_csr_transposed(int32_t n, const int64_t* row_ptr, const int32_t* cols, const double* vals,
+                                int64_t* t_row_ptr, int32_t* t_cols, double* t_vals, int32_t device) {
+  if (n == 0) {
+    if (t_row_ptr) t_row_ptr[0] = 0;
+    return IMPM_OK;
+  }
+  return csr_call(device, [&](cudaStream_t s) {
+    csr::DevCsr A;
+    A.upload(n, row_ptr, cols, vals, s);
+    csr::transposed(A, t_row_ptr, t_cols, t_vals);
+  });
+}
+const char* impm_csr_last_error(void) { return g_csr_error.c_str(); }
 
 }  // extern "C"

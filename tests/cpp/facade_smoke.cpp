@@ -35,7 +35,23 @@ int main() {
   sim.gravity = {0.0, 0.0, -9.81};
   try {
     const StepRecord rec = sim.step(1.0);
-    std::printf("%d %d\n", sim.n_dofs(), rec.iterations);
+    // link-level seam: the 2x2 hand solve of test_linear_solver.cpp:60-65, and
+    // the singular matrix of :92-97 -> LinearSolverError
+    CsrMatrix A;
+    A.n = 2;
+    A.row_ptr = {0, 2, 4};
+    A.cols = {0, 1, 0, 1};
+    A.vals = {2.0, 1.0, 1.0, 2.0};
+    const std::vector<double> b{3.0, 3.0};
+    const std::vector<double> x = sparse_lu_solve(A, b);
+    A.vals = {1.0, 2.0, 2.0, 4.0};
+    bool threw = false;
+    try {
+      (void)sparse_lu_solve(A, std::vector<double>{1.0, 2.0});
+    } catch (const LinearSolverError&) {
+      threw = true;
+    }
+    std::printf("%d %d %.17g %.17g %d\n", sim.n_dofs(), rec.iterations, x[0], x[1], threw ? 1 : 0);
   } catch (const Error& e) {
     std::printf("error: %s\n", e.what());
     return 1;

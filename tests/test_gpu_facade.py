@@ -18,3 +18,6 @@ def test_cpp_facade_smoke3d_matches_reference(tmp_path):
     ref = np.load(gu.GOLDEN + "/reference_out.npz")["smoke3d__summary"]
     assert int(out[0]) == int(ref[0, 0]) == 300
     assert int(out[1]) == int(ref[0, 1]) == 3
+    # sparse_lu_solve seam through the C++ facade (test_linear_solver.cpp:60-65, :92-97)
+    assert abs(float(out[2]) - 1.0) <= 1e-14 and abs(float(out[3]) - 1.0) <= 1e-14
+    assert int(out[4]) == 1
