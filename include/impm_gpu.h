@@ -53,7 +53,8 @@ typedef enum impm_material_kind {
   IMPM_HENCKY = 0,
   IMPM_HENCKY_J2 = 1,
   IMPM_NEO_HOOKEAN = 2,
-  IMPM_DRUCKER_PRAGER = 3  /* extension, parity unpinned (D <= 2) */
+  IMPM_DRUCKER_PRAGER = 3, /* extension, parity unpinned */
+  IMPM_CAM_CLAY = 4        /* modified Cam-Clay, extension, parity unpinned */
 } impm_material_kind;
 
 /* impm::MaterialSpec (mpm_solver.hpp:21-25) */
@@ -62,8 +63,10 @@ typedef struct impm_material {
   int32_t pad_;
   double E, nu;       /* ElasticParams (materials.hpp:12-23) */
   double kappa;       /* J2 yield strength */
-  double friction_deg;  /* Drucker-Prager friction angle [deg] */
-  double cohesion;      /* Drucker-Prager cohesion [Pa] (apex shift) */
+  double friction_deg;  /* Drucker-Prager friction angle / Cam-Clay critical-state angle [deg] */
+  double cohesion;      /* Drucker-Prager cohesion [Pa] (apex shift) / Cam-Clay tensile intercept p_t [Pa] */
+  double pc0;           /* Cam-Clay initial preconsolidation pressure [Pa] */
+  double hardening;     /* Cam-Clay hardening exponent theta = (1 + e0) / (lambda - kappa) */
 } impm_material;
 
 /* Transfer functions: impm::ShapeFunctionKind (gimp.hpp:11). */

@@ -25,7 +25,7 @@ class Grid(ctypes.Structure):
 
 class Material(ctypes.Structure):
     _fields_ = [("kind", c_int32), ("pad_", c_int32), ("E", c_double), ("nu", c_double), ("kappa", c_double),
-                ("friction_deg", c_double), ("cohesion", c_double)]
+                ("friction_deg", c_double), ("cohesion", c_double), ("pc0", c_double), ("hardening", c_double)]
 
 
 class Options(ctypes.Structure):

@@ -484,29 +484,39 @@ struct MatParams {
   double lam, mu, kappa;
   double dp_alpha;  // Drucker-Prager sqrt(2/3) 2 sin(phi) / (3 - sin(phi))
   double dp_ec;     // apex strain shift 3 c / (3 lam + 2 mu)
+  double mcc_M;     // Cam-Clay critical-state slope 6 sin(phi) / (3 - sin(phi))
+  double mcc_pc0;   // initial preconsolidation pressure
+  double mcc_theta; // hardening exponent (1 + e0) / (lambda - kappa)
+  double mcc_pt;    // tensile intercept
 };
 
-__host__ __device__ __forceinline__ bool has_history(int kind) { return kind == kHenckyJ2 || kind == kDruckerPrager; }
+__host__ __device__ __forceinline__ bool has_history(int kind) {
+  return kind == kHenckyJ2 || kind == kDruckerPrager || kind == kCamClay;
+}
 
-// update_stress (mpm_solver.hpp:445-454) over scalar T
-template <class T, int D>
+// update_stress (mpm_solver.hpp:445-454) over scalar T. NHO: the kind is
+// known to be neo-Hookean at compile time (keeps the 3D tangent lean).
+template <class T, int D, bool NHO = false>
 __device__ __forceinline__ StressOut<T> update_stress(const MatParams& mp, const Mat<T, D>& F_new,
                                                       const Mat<T, D>& f_inc, const double* Be_n,
                                                       double* Be_out = nullptr, double* dg_out = nullptr) {
   const T lam = T(mp.lam), mu = T(mp.mu);
+  if constexpr (NHO) return neo_hookean_update<T, D>(F_new, lam, mu);
   if (mp.kind == kNeoHookean) return neo_hookean_update<T, D>(F_new, lam, mu);
-  if constexpr (D <= 2) {
-    if (mp.kind == kHencky) return hencky_update<T, D>(F_new, lam, mu);
-    if (mp.kind == kDruckerPrager) return dp_update<T, D>(F_new, f_inc, Be_n, lam, mu, mp.dp_alpha, mp.dp_ec, Be_out, dg_out);
-    return j2_update<T, D>(f_inc, Be_n, lam, mu, mp.kappa, Be_out, dg_out);
-  }
-  return neo_hookean_update<T, D>(F_new, lam, mu);
+  // D = 3 Hencky / J2 / Drucker-Prager / Cam-Clay take the 3x3 spectral
+  // log/exp (extensions; the reference stops at D <= 2, mpm_solver.hpp:448-453)
+  if (mp.kind == kHencky) return hencky_update<T, D>(F_new, lam, mu);
+  if (mp.kind == kDruckerPrager) return dp_update<T, D>(F_new, f_inc, Be_n, lam, mu, mp.dp_alpha, mp.dp_ec, Be_out, dg_out);
+  if (mp.kind == kCamClay)
+    return mcc_update<T, D>(F_new, f_inc, Be_n, mp.lam + 2.0 * mp.mu / 3.0, mp.mu, mp.mcc_M, mp.mcc_pc0, mp.mcc_theta,
+                            mp.mcc_pt, Be_out, dg_out);
+  return j2_update<T, D>(f_inc, Be_n, lam, mu, mp.kappa, Be_out, dg_out);
 }
 
 // Residual phase A (particles): G, f_inc, F_new, det check, sigma, V and the
 // nominal stress P = V sigma f_inc^{-T} so that the node-side gather is
 // r_{k,c} = sum_b grad_{k,b} P_{cb} - w_k b_c s  (mpm_solver.hpp:164-208).
-template <int D, int SHAPE>
+template <int D, int SHAPE, bool NHO>
 __global__ void k_residual_particles(GridC g, const double* __restrict__ pd, int64_t cap, int P,
                                      const double* __restrict__ xs, const int* __restrict__ key,
                                      const int* __restrict__ sup, const int* __restrict__ orig,
@@ -545,11 +555,12 @@ __global__ void k_residual_particles(GridC g, const double* __restrict__ pd, int
     for (int i = 0; i < D * D; ++i) out[i] = 0.0;
     return;
   }
-  double Be_n[9];
+  double Be_n[10];
   if (has_history(mp.kind))
 #pragma unroll
     for (int i = 0; i < 9; ++i) Be_n[i] = pd[(PF<D>::Be + i) * cap + p];
-  const StressOut<double> su = update_stress<double, D>(mp, F_new, f_inc, Be_n);
+  if (mp.kind == kCamClay) Be_n[9] = pd[PF<D>::alpha * cap + p];
+  const StressOut<double> su = update_stress<double, D, NHO>(mp, F_new, f_inc, Be_n);
   const double V = su.J * pd[PF<D>::V0 * cap + p];
   const Mat<double, D> fi = inverse(f_inc);
 #pragma unroll
@@ -713,7 +724,7 @@ __global__ void k_mask_norm(int64_t n, const uint8_t* __restrict__ freem, double
 // dP/dG per particle by forward-mode duals over the same expression graph as
 // the residual (hand-written AD replacing the tape, tape.hpp:107-122):
 // A[p][(c*D+b)*D*D + (d*D+f)] = dP_cb / dG_df.
-template <int D, int SHAPE, int K>
+template <int D, int SHAPE, int K, bool NHO>
 __global__ void k_tangent(GridC g, const double* __restrict__ pd, int64_t cap, int P,
                           const double* __restrict__ xs, const int* __restrict__ key,
                           const int* __restrict__ sup, const double* __restrict__ u, MatParams mp, int tl,
@@ -737,10 +748,11 @@ __global__ void k_tangent(GridC g, const double* __restrict__ pd, int64_t cap, i
   double Fn[DD];
 #pragma unroll
   for (int i = 0; i < DD; ++i) Fn[i] = pd[(PF<D>::F + i) * cap + p];
-  double Be_n[9];
+  double Be_n[10];
   if (has_history(mp.kind))
 #pragma unroll
     for (int i = 0; i < 9; ++i) Be_n[i] = pd[(PF<D>::Be + i) * cap + p];
+  if (mp.kind == kCamClay) Be_n[9] = pd[PF<D>::alpha * cap + p];
   const double V0 = pd[PF<D>::V0 * cap + p];
   double* out = A + static_cast<int64_t>(p) * DD * DD;
 #pragma unroll 1
@@ -768,7 +780,7 @@ __global__ void k_tangent(GridC g, const double* __restrict__ pd, int64_t cap, i
       for (int i = 0; i < DD * DD; ++i) out[i] = 0.0;
       return;
     }
-    const StressOut<T> su = update_stress<T, D>(mp, F_new, f_inc, Be_n);
+    const StressOut<T> su = update_stress<T, D, NHO>(mp, F_new, f_inc, Be_n);
     const T V = su.J * V0;
     const Mat<T, D> fi = inverse(f_inc);
 #pragma unroll
@@ -2228,7 +2240,7 @@ __global__ void k_dot1(int64_t n, const int* __restrict__ done, const double* __
 }
 
 // --------------------------------------------------------------- K9 G2P --
-template <int D, int SHAPE>
+template <int D, int SHAPE, bool NHO>
 __global__ void k_commit(GridC g, double* __restrict__ pd, int64_t cap, int P, const double* __restrict__ xs,
                          const int* __restrict__ key, const int* __restrict__ sup, const int* __restrict__ orig,
                          const double* __restrict__ u, MatParams mp, int tl, DevStatus* st) {
@@ -2264,11 +2276,12 @@ __global__ void k_commit(GridC g, double* __restrict__ pd, int64_t cap, int P, c
     for (int i = 0; i < D * D; ++i) Fn.e[i] = pd[(PF<D>::F + i) * cap + p];
     F_new = matmul(f_inc, Fn);
   }
-  double Be_n[9], Be_new[9], dg = 0.0;
+  double Be_n[10], Be_new[9], dg = 0.0;
   if (has_history(mp.kind))
 #pragma unroll
     for (int i = 0; i < 9; ++i) Be_n[i] = pd[(PF<D>::Be + i) * cap + p];
-  const StressOut<double> su = update_stress<double, D>(mp, F_new, f_inc, Be_n, Be_new, &dg);
+  if (mp.kind == kCamClay) Be_n[9] = pd[PF<D>::alpha * cap + p];
+  const StressOut<double> su = update_stress<double, D, NHO>(mp, F_new, f_inc, Be_n, Be_new, &dg);
 #pragma unroll
   for (int a = 0; a < D; ++a) {
     if (tl)

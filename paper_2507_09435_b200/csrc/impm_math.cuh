@@ -327,7 +327,7 @@ __device__ __forceinline__ void gimp_support_1d(double x, double lp, double orig
 }
 
 // ---------------------------------------------------------- constitutive --
-enum MaterialKind : int { kHencky = 0, kHenckyJ2 = 1, kNeoHookean = 2, kDruckerPrager = 3 };
+enum MaterialKind : int { kHencky = 0, kHenckyJ2 = 1, kNeoHookean = 2, kDruckerPrager = 3, kCamClay = 4 };
 
 template <class T>
 struct StressOut {
@@ -397,9 +397,158 @@ IMPM_HD Mat<T, 2> sym_exp_2x2(const Mat<T, 2>& a) {
   return out;
 }
 
-// embedded_sym_log / embedded_sym_exp (materials.hpp:61-105), D <= 2
+
+// ------------------------------------------------- 3x3 spectral functions --
+// Extension beyond the reference, whose embedded closed forms stop at D <= 2
+// (materials.hpp:61-62 static_assert "use the 3x3 spectral path"): f(B) for a
+// symmetric 3x3 B with f = log (Hencky strain) or exp (B_e from strain).
+// Values: cyclic Jacobi eigen-decomposition B = Q diag(l) Q^T (orthogonal Q to
+// roundoff, no branch on eigenvalue multiplicity), f(B) = Q diag(f(l)) Q^T.
+// Tangents (T = Dual<K>): the Daleckii-Krein formula
+//   df(B)[dB] = Q (F o (Q^T dB Q)) Q^T,  F_ij = f[l_i, l_j],
+// with first divided differences in cancellation-free forms that tend to
+// f'(l) as l_i -> l_j, so repeated eigenvalues (B = I at rest) are exact.
+IMPM_HD void sym_eig3(const double Bin[9], double l[3], double Q[9]) {
+  double a[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) a[i * 3 + j] = 0.5 * (Bin[i * 3 + j] + Bin[j * 3 + i]);
+#pragma unroll
+  for (int i = 0; i < 9; ++i) Q[i] = (i % 4 == 0) ? 1.0 : 0.0;
+  for (int sweep = 0; sweep < 12; ++sweep) {
+    const double off = a[1] * a[1] + a[2] * a[2] + a[5] * a[5];
+    const double dia = a[0] * a[0] + a[4] * a[4] + a[8] * a[8];
+    if (!(off > 1e-34 * dia)) break;
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const int p = r == 2 ? 1 : 0, q = r == 0 ? 1 : 2;
+      const double apq = a[p * 3 + q];
+      if (apq == 0.0) continue;
+      const double theta = (a[q * 3 + q] - a[p * 3 + p]) / (2.0 * apq);
+      const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+      const double c = 1.0 / sqrt(t * t + 1.0), sn = t * c;
+      // A <- J^T A J with J = rotation in the (p, q) plane
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const double akp = a[k * 3 + p], akq = a[k * 3 + q];
+        a[k * 3 + p] = c * akp - sn * akq;
+        a[k * 3 + q] = sn * akp + c * akq;
+      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const double apk = a[p * 3 + k], aqk = a[q * 3 + k];
+        a[p * 3 + k] = c * apk - sn * aqk;
+        a[q * 3 + k] = sn * apk + c * aqk;
+      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const double qkp = Q[k * 3 + p], qkq = Q[k * 3 + q];
+        Q[k * 3 + p] = c * qkp - sn * qkq;
+        Q[k * 3 + q] = sn * qkp + c * qkq;
+      }
+    }
+  }
+  l[0] = a[0];
+  l[1] = a[4];
+  l[2] = a[8];
+}
+
+enum SymFn : int { kSymLog = 0, kSymExp = 1 };
+
+IMPM_HD double sym_fn(int fn, double x) { return fn == kSymLog ? log(x) : exp(x); }
+
+// first divided difference f[a, b] (f'(a) at a == b)
+IMPM_HD double sym_fn_dd(int fn, double a, double b) {
+  if (fn == kSymLog) {
+    const double r = (a - b) / (a + b);  // log(a/b) = 2 atanh(r)
+    if (fabs(r) < 1e-3) {
+      const double r2 = r * r;
+      return 2.0 / (a + b) * (1.0 + r2 * (1.0 / 3.0 + r2 * (1.0 / 5.0 + r2 * (1.0 / 7.0))));
+    }
+    return (log(a) - log(b)) / (a - b);
+  }
+  const double d = a - b;  // exp[a, b] = exp(b) expm1(d) / d
+  if (fabs(d) < 1e-3) return exp(b) * (1.0 + d * (0.5 + d * (1.0 / 6.0 + d * (1.0 / 24.0 + d * (1.0 / 120.0)))));
+  return exp(b) * expm1(d) / d;
+}
+
+IMPM_HD Mat<double, 3> sym_fun3(const Mat<double, 3>& B, int fn) {
+  double l[3], Q[9];
+  sym_eig3(B.e, l, Q);
+  const double f[3] = {sym_fn(fn, l[0]), sym_fn(fn, l[1]), sym_fn(fn, l[2])};
+  Mat<double, 3> out;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      out(i, j) = Q[i * 3 + 0] * f[0] * Q[j * 3 + 0] + Q[i * 3 + 1] * f[1] * Q[j * 3 + 1] +
+                  Q[i * 3 + 2] * f[2] * Q[j * 3 + 2];
+  return out;
+}
+
+template <int K>
+IMPM_HD Mat<Dual<K>, 3> sym_fun3(const Mat<Dual<K>, 3>& B, int fn) {
+  Mat<double, 3> Bv;
+#pragma unroll
+  for (int i = 0; i < 9; ++i) Bv.e[i] = B.e[i].v;
+  double l[3], Q[9];
+  sym_eig3(Bv.e, l, Q);
+  double f[3], dd[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) f[i] = sym_fn(fn, l[i]);
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) dd[i][j] = j < i ? dd[j][i] : sym_fn_dd(fn, l[i], l[j]);
+  Mat<Dual<K>, 3> out;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      out(i, j).v = Q[i * 3 + 0] * f[0] * Q[j * 3 + 0] + Q[i * 3 + 1] * f[1] * Q[j * 3 + 1] +
+                    Q[i * 3 + 2] * f[2] * Q[j * 3 + 2];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double dB[9], M[9], T1[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) dB[i * 3 + j] = 0.5 * (B(i, j).d[k] + B(j, i).d[k]);
+    // M = Q^T dB Q, scaled by the divided differences
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        T1[i * 3 + j] = dB[i * 3 + 0] * Q[0 * 3 + j] + dB[i * 3 + 1] * Q[1 * 3 + j] + dB[i * 3 + 2] * Q[2 * 3 + j];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        M[i * 3 + j] = dd[i][j] * (Q[0 * 3 + i] * T1[0 * 3 + j] + Q[1 * 3 + i] * T1[1 * 3 + j] +
+                                   Q[2 * 3 + i] * T1[2 * 3 + j]);
+    // out.d = Q M Q^T
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        T1[i * 3 + j] = Q[i * 3 + 0] * M[0 * 3 + j] + Q[i * 3 + 1] * M[1 * 3 + j] + Q[i * 3 + 2] * M[2 * 3 + j];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        out(i, j).d[k] = T1[i * 3 + 0] * Q[j * 3 + 0] + T1[i * 3 + 1] * Q[j * 3 + 1] + T1[i * 3 + 2] * Q[j * 3 + 2];
+  }
+  return out;
+}
+
+// embedded_sym_log / embedded_sym_exp (materials.hpp:61-105); D = 3 takes the
+// spectral path above (extension, parity unpinned)
 template <class T, int D>
 IMPM_HD Mat<T, 3> embedded_sym_log(const Mat<T, 3>& b) {
+  if constexpr (D == 3) {
+    return sym_fun3(b, kSymLog);
+  } else {
   Mat<T, 3> out = Mat<T, 3>::zero();
   if constexpr (D == 1) {
     out(0, 0) = dlog(b(0, 0));
@@ -418,10 +567,14 @@ IMPM_HD Mat<T, 3> embedded_sym_log(const Mat<T, 3>& b) {
 #pragma unroll
   for (int i = D; i < 3; ++i) out(i, i) = dlog(b(i, i));
   return out;
+  }
 }
 
 template <class T, int D>
 IMPM_HD Mat<T, 3> embedded_sym_exp(const Mat<T, 3>& eps) {
+  if constexpr (D == 3) {
+    return sym_fun3(eps, kSymExp);
+  } else {
   Mat<T, 3> out = Mat<T, 3>::zero();
   if constexpr (D == 1) {
     out(0, 0) = dexp(eps(0, 0));
@@ -440,6 +593,7 @@ IMPM_HD Mat<T, 3> embedded_sym_exp(const Mat<T, 3>& eps) {
 #pragma unroll
   for (int i = D; i < 3; ++i) out(i, i) = dexp(eps(i, i));
   return out;
+  }
 }
 
 template <class T>
@@ -626,6 +780,103 @@ IMPM_HD StressOut<T> dp_update(const Mat<T, D>& F_new, const Mat<T, D>& f_incr, 
 #pragma unroll
     for (int i = 0; i < 9; ++i) Be_out[i] = Be.e[i];
     *dgamma_out = dg;
+  }
+  return out;
+}
+
+// Modified Cam-Clay on Hencky strain (extension, parity unpinned: no
+// critical-state model in /root/reference). Linear isotropic elasticity in
+// Hencky strain (K, G), compression-positive invariants
+//   P = -K tr(eps_e),  q = sqrt(3/2) |2 G dev(eps_e)|,
+// yield f = q^2/M^2 + (P + p_t)(P - p_c) (ellipse from -p_t to p_c; p_t > 0
+// keeps the stress-free state strictly elastic), associative flow, and
+// exponential hardening p_c = p_c0 exp(theta a), a = accumulated plastic
+// compaction (the particle's alpha). Return map: radial in the deviatoric
+// plane (coaxial with the trial strain), Newton on (x = plastic compaction
+// increment, g = plastic multiplier):
+//   r1 = x - g (2P + p_t - p_c) = 0,   r2 = (q^2/M^2 + (P + p_t)(P - p_c)) / p_c,n^2 = 0,
+//   P = P_tr - K x,  p_c = p_c,n exp(theta x),  q = q_tr / (1 + 6 G g / M^2).
+// Run in T = Dual<K>, one extra Newton step after the values converge makes
+// the dual parts the exact implicit derivative (the consistent tangent).
+// Be_n[9] carries alpha_n. Outputs B_e = exp(2 eps_e) and x (added to alpha).
+template <class T, int D>
+IMPM_HD StressOut<T> mcc_update(const Mat<T, D>& F_new, const Mat<T, D>& f_incr, const double* Be_n, double K,
+                                double G, double M, double pc0, double theta, double pt, double* Be_out = nullptr,
+                                double* dgamma_out = nullptr) {
+  const Mat<T, 3> f3 = embed_F<T, D>(f_incr);
+  Mat<T, 3> Ben;
+#pragma unroll
+  for (int i = 0; i < 9; ++i) Ben.e[i] = T(Be_n[i]);
+  const Mat<T, 3> b_tr = matmul(matmul(f3, Ben), transpose(f3));
+  const Mat<T, 3> eps_tr = scale3(0.5, embedded_sym_log<T, D>(b_tr));
+  const T tr = trace(eps_tr);
+  Mat<T, 3> dev = eps_tr;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) dev(i, i) -= tr * (1.0 / 3.0);
+  T s2 = T(0.0);
+#pragma unroll
+  for (int i = 0; i < 9; ++i) s2 += dev.e[i] * dev.e[i];
+  const T dn = dsqrt(s2 + 1e-300);
+  const T P_tr = (-K) * tr;
+  const T q_tr = (2.449489742783178 * G) * dn;  // sqrt(6) G |dev|
+  const double pcn = pc0 * exp(theta * Be_n[9]);
+  const double M2 = M * M;
+  const T f_tr = q_tr * q_tr / M2 + (P_tr + pt) * (P_tr - pcn);
+  T P = P_tr, scale_q = T(1.0);
+  double xv = 0.0;
+  if (value_of(f_tr) > 1e-12 * pcn * pcn) {
+    T x = T(0.0), g = T(0.0);
+    const double inv_pc2 = 1.0 / (pcn * pcn);
+    int extra = -1;
+    for (int it = 0; it < 60; ++it) {
+      const T pc = pcn * dexp(theta * x);
+      const T Pk = P_tr - K * x;
+      const T den = 1.0 + (6.0 * G / M2) * g;
+      const T q = q_tr / den;
+      const T r1 = x - g * (2.0 * Pk + pt - pc);
+      const T r2 = (q * q / M2 + (Pk + pt) * (Pk - pc)) * inv_pc2;
+      const double rn = fabs(value_of(r1)) + fabs(value_of(r2));
+      if (extra < 0 && rn <= 1e-14) extra = 0;
+      if (extra >= 0 && extra++ >= 2) break;
+      const T a11 = 1.0 + g * (2.0 * K + theta * pc);
+      const T a12 = -(2.0 * Pk + pt - pc);
+      const T a21 = ((-K) * (Pk - pc) + (Pk + pt) * ((-K) - theta * pc)) * inv_pc2;
+      const T a22 = (2.0 * q / M2) * ((-6.0 * G / M2) * q / den) * inv_pc2;
+      const T dt = a11 * a22 - a12 * a21;
+      T dx = (a22 * r1 - a12 * r2) / dt;
+      T dg = (a11 * r2 - a21 * r1) / dt;
+      // keep the multiplier non-negative (den > 0) with a damped step
+      double lam_s = 1.0;
+      while (value_of(g) - lam_s * value_of(dg) < 0.0 && lam_s > 1e-6) lam_s *= 0.5;
+      x = x - lam_s * dx;
+      g = g - lam_s * dg;
+    }
+    P = P_tr - K * x;
+    scale_q = 1.0 / (1.0 + (6.0 * G / M2) * g);
+    xv = value_of(x);
+  }
+  const T J = det(F_new);
+  StressOut<T> out;
+  out.J = J;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      T tau = (2.0 * G) * scale_q * dev(i, j);
+      if (i == j) tau -= P;
+      out.sigma(i, j) = tau / J;
+    }
+  if (Be_out) {
+    Mat<double, 3> e2;
+    const double ev = -value_of(P) / K;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) e2(i, j) = 2.0 * (value_of(scale_q) * value_of(dev(i, j)) + (i == j ? ev / 3.0 : 0.0));
+    const Mat<double, 3> Be = embedded_sym_exp<double, D>(e2);
+#pragma unroll
+    for (int i = 0; i < 9; ++i) Be_out[i] = Be.e[i];
+    *dgamma_out = xv;
   }
   return out;
 }

@@ -343,6 +343,10 @@ struct Sim {
     const double sphi = std::sin(mat.friction_deg * M_PI / 180.0);
     m.dp_alpha = std::sqrt(2.0 / 3.0) * 2.0 * sphi / (3.0 - sphi);
     m.dp_ec = 3.0 * mat.cohesion / (3.0 * m.lam + 2.0 * m.mu);
+    m.mcc_M = 6.0 * sphi / (3.0 - sphi);
+    m.mcc_pc0 = mat.pc0;
+    m.mcc_theta = mat.hardening;
+    m.mcc_pt = mat.cohesion;
     return m;
   }
 
@@ -412,12 +416,20 @@ struct Sim {
     mat = *m;
     if (!(mat.E > 0.0)) throw SimError(IMPM_ERR_CONFIG, "Young's modulus must be positive");
     if (!(mat.nu > -1.0 && mat.nu < 0.5)) throw SimError(IMPM_ERR_CONFIG, "Poisson's ratio must lie in (-1, 0.5)");
-    if (mat.kind != kHencky && mat.kind != kHenckyJ2 && mat.kind != kNeoHookean && mat.kind != kDruckerPrager)
+    if (mat.kind != kHencky && mat.kind != kHenckyJ2 && mat.kind != kNeoHookean && mat.kind != kDruckerPrager &&
+        mat.kind != kCamClay)
       throw SimError(IMPM_ERR_CONFIG, "unknown material kind");
     if (mat.kind == kDruckerPrager && !(mat.friction_deg > 0.0 && mat.friction_deg < 90.0))
       throw SimError(IMPM_ERR_CONFIG, "Drucker-Prager friction angle must lie in (0, 90) degrees");
-    if (D == 3 && mat.kind != kNeoHookean)  // mpm_solver.hpp:448-453
-      throw SimError(IMPM_ERR_CONFIG, "material kind not available in 3D");
+    if (mat.kind == kCamClay) {
+      if (!(mat.friction_deg > 0.0 && mat.friction_deg < 90.0))
+        throw SimError(IMPM_ERR_CONFIG, "Cam-Clay critical-state friction angle must lie in (0, 90) degrees");
+      if (!(mat.pc0 > 0.0)) throw SimError(IMPM_ERR_CONFIG, "Cam-Clay preconsolidation pressure must be positive");
+      if (!(mat.hardening >= 0.0)) throw SimError(IMPM_ERR_CONFIG, "Cam-Clay hardening must be non-negative");
+      if (!(mat.cohesion > 0.0)) throw SimError(IMPM_ERR_CONFIG, "Cam-Clay tensile intercept must be positive");
+    }
+    // the reference has Hencky / J2 only for D <= 2 (mpm_solver.hpp:448-453);
+    // here every kind runs in 3D through the spectral log/exp (extension)
     if (mat.kind == kHenckyJ2 && !(mat.kappa > 0.0)) throw SimError(IMPM_ERR_CONFIG, "yield strength must be positive");
   }
   void set_options(const impm_options* o) {
@@ -916,8 +928,13 @@ struct Sim {
       constexpr int DD = decltype(Dc)::value, SH = decltype(Sc)::value;
       if (P > 0) {
         Prof::Scope ps(&prof, kcResP);
-        k_residual_particles<DD, SH><<<blocks_for(P), kThreads, 0, s>>>(g, pd.p, cap, P, xs.p, key.p, sup.p, orig.p,
-                                                                        ud, mp, opt.total_lagrangian, Pst.p, st.p); ++g_launches;
+        if (mp.kind == kNeoHookean)
+          k_residual_particles<DD, SH, true><<<blocks_for(P), kThreads, 0, s>>>(
+              g, pd.p, cap, P, xs.p, key.p, sup.p, orig.p, ud, mp, opt.total_lagrangian, Pst.p, st.p);
+        else
+          k_residual_particles<DD, SH, false><<<blocks_for(P), kThreads, 0, s>>>(
+              g, pd.p, cap, P, xs.p, key.p, sup.p, orig.p, ud, mp, opt.total_lagrangian, Pst.p, st.p);
+        ++g_launches;
         CKL();
       }
       {
@@ -963,12 +980,17 @@ struct Sim {
       if (P > 0) {
         Prof::Scope ps(&prof, kcTangent);
         constexpr int K = DD == 3 ? 3 : DD * DD;
-        if (DD == 3 && tangent_k1)
-          k_tangent<DD, SH, 1><<<blocks_for(P, 128), 128, 0, s>>>(g, pd.p, cap, P, xs.p, key.p, sup.p, ud, mp,
-                                                                  opt.total_lagrangian, Atan.p);
+        // plastic kinds (one return map per pass) take K = 3 directions per pass in 3D
+        const bool nho = mp.kind == kNeoHookean;
+        if (DD == 3 && tangent_k1 && nho)
+          k_tangent<DD, SH, 1, true><<<blocks_for(P, 128), 128, 0, s>>>(g, pd.p, cap, P, xs.p, key.p, sup.p, ud, mp,
+                                                                        opt.total_lagrangian, Atan.p);
+        else if (nho)
+          k_tangent<DD, SH, K, true><<<blocks_for(P, 128), 128, 0, s>>>(g, pd.p, cap, P, xs.p, key.p, sup.p, ud, mp,
+                                                                        opt.total_lagrangian, Atan.p);
         else
-          k_tangent<DD, SH, K><<<blocks_for(P, 128), 128, 0, s>>>(g, pd.p, cap, P, xs.p, key.p, sup.p, ud, mp,
-                                                                  opt.total_lagrangian, Atan.p);
+          k_tangent<DD, SH, K, false><<<blocks_for(P, 128), 128, 0, s>>>(g, pd.p, cap, P, xs.p, key.p, sup.p, ud, mp,
+                                                                         opt.total_lagrangian, Atan.p);
         ++g_launches;
         CKL();
       }
@@ -990,8 +1012,10 @@ struct Sim {
           if (nbins == 0) continue;
           constexpr int WS = 4;
           const unsigned grid = std::min<unsigned>(blocks_for(nbins, WS), 148 * 32);
-          // J is symmetric except under non-associative Drucker-Prager flow
-          if (mat.kind != kDruckerPrager)
+          // J is symmetric except under non-associative Drucker-Prager flow and
+          // Cam-Clay (associative, but its compaction hardening breaks major
+          // symmetry of dP/dG: ~2% in tests/test_math_cpu.py terms)
+          if (mat.kind != kDruckerPrager && mat.kind != kCamClay)
             k_assemble_bins_staged<DD, SH, (DD == 3 ? 3 : PPL), WS, 4, true><<<grid, WS * 32, 0, s>>>(
                 g, pd.p, cap, xs.p, bin_start.p, bflag.p, Atan.p, act_idx.p, row_mask.p, row_nzb.p, vals.p, row_len,
                 cc[0], cc[1], cc[2], nb[0], nb[1], nb[2]);
@@ -1679,7 +1703,7 @@ struct Sim {
       constexpr int DD = decltype(Dc)::value, FE = decltype(Fc)::value;
       // non-associative Drucker-Prager flow gives a nonsymmetric J -> GMRES;
       // MG right-preconditions GMRES for DP; the u-p saddle point uses block Jacobi
-      const bool nonsym = coupled || mat.kind == kDruckerPrager;
+      const bool nonsym = coupled || mat.kind == kDruckerPrager || mat.kind == kCamClay;
       const bool mgp = opt.precond == IMPM_PRECOND_MG && !coupled;
       if (!nonsym && opt.krylov != IMPM_KRYLOV_BICGSTAB && opt.krylov != IMPM_KRYLOV_GMRES) {
         const int it = mgp ? cg_mg_solve<DD, FE>(rhs, x) : cg_solve<FE>(rhs, x);
@@ -2034,8 +2058,13 @@ struct Sim {
       constexpr int DD = decltype(Dc)::value, SH = decltype(Sc)::value;
       if (P > 0) {
         Prof::Scope ps(&prof, kcCommit);
-        k_commit<DD, SH><<<blocks_for(P), kThreads, 0, s>>>(g, pd.p, cap, P, xs.p, key.p, sup.p, orig.p, u.p, mp,
-                                                            opt.total_lagrangian, st.p); ++g_launches;
+        if (mp.kind == kNeoHookean)
+          k_commit<DD, SH, true><<<blocks_for(P), kThreads, 0, s>>>(g, pd.p, cap, P, xs.p, key.p, sup.p, orig.p, u.p,
+                                                                    mp, opt.total_lagrangian, st.p);
+        else
+          k_commit<DD, SH, false><<<blocks_for(P), kThreads, 0, s>>>(g, pd.p, cap, P, xs.p, key.p, sup.p, orig.p, u.p,
+                                                                     mp, opt.total_lagrangian, st.p);
+        ++g_launches;
         CKL();
       }
     });

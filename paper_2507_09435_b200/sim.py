@@ -15,7 +15,7 @@ from . import _abi
 from .errors import raise_for
 from .particles import GridSpec, ParticleArray, particle_doubles
 
-MATERIAL_KINDS = {"hencky": 0, "hencky_j2": 1, "neo_hookean": 2, "drucker_prager": 3}
+MATERIAL_KINDS = {"hencky": 0, "hencky_j2": 1, "neo_hookean": 2, "drucker_prager": 3, "cam_clay": 4}
 SHAPES = {"gimp": 1, "quadratic-bspline": 2, "quadratic_bspline": 2}
 KRYLOV = {"auto": 0, "cg": 1, "bicgstab": 2, "gmres": 3}
 PRECOND = {"mg": 0, "multigrid": 0, "block_jacobi": 1, "jacobi": 1}
@@ -40,8 +40,10 @@ class MaterialSpec:
     kind: str = "hencky"
     elastic: ElasticParams = field(default_factory=lambda: ElasticParams(1.0, 0.0))
     kappa: float = 0.0
-    friction_deg: float = 30.0  # Drucker-Prager (extension)
-    cohesion: float = 0.0
+    friction_deg: float = 30.0  # Drucker-Prager friction / Cam-Clay critical-state angle (extensions)
+    cohesion: float = 0.0  # Drucker-Prager cohesion / Cam-Clay tensile intercept p_t
+    pc0: float = 0.0  # Cam-Clay initial preconsolidation pressure
+    hardening: float = 0.0  # Cam-Clay theta = (1 + e0) / (lambda - kappa)
 
 
 @dataclass
@@ -107,7 +109,7 @@ class _Handle:
             g.origin[a] = float(grid.origin[a]) if a < grid.dim else 0.0
         g.h = float(grid.h)
         m = _abi.Material(MATERIAL_KINDS[material.kind], 0, material.elastic.E, material.elastic.nu, material.kappa,
-                          material.friction_deg, material.cohesion)
+                          material.friction_deg, material.cohesion, material.pc0, material.hardening)
         o = options.to_c()
         h = ctypes.c_void_p()
         st = L.impm_sim_create(ctypes.byref(g), ctypes.byref(m), ctypes.byref(o), device, ctypes.byref(h))

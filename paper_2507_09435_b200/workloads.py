@@ -93,21 +93,34 @@ def slope2d(cells=(256, 128), ppc=4, h=0.5, steps=20, friction_deg=30.0, E=10e6,
                          else "hencky_j2 pinned substitute for Drucker-Prager"))
 
 
-def footing3d(cells=(128, 128, 64), ppc=2, h=0.5, steps=20, t_hat=100e3, frac=0.125, E=10e6, nu=0.3):
+# cfg 4 clay (modified Cam-Clay, extension): critical-state angle 30 deg
+# (M = 1.2), preconsolidation 600 kPa (lightly overconsolidated over the 32 m
+# depth: mean overburden reaches ~400 kPa), theta = (1 + e0)/(lambda - kappa)
+# = 10, tensile intercept 5 kPa
+CAM_CLAY = {"friction_deg": 30.0, "cohesion": 5e3, "pc0": 600e3, "hardening": 10.0}
+
+
+def footing3d(cells=(128, 128, 64), ppc=2, h=0.5, steps=20, t_hat=100e3, frac=0.125, E=10e6, nu=0.3,
+              material="neo_hookean"):
     """cfg 4 / cfg 5 slab: 3D strip footing, 128x128x64 cells, ppc 2 (8,388,608
     particles). Modified Cam-Clay is absent from the reference: the pinned
-    substitute is neo-Hookean; the rigid footing is a strip
+    substitute is neo-Hookean; material="cam_clay" runs the
+    (unpinned) modified Cam-Clay extension. The rigid footing is a strip
     traction on the top layer (the reference has no contact)."""
     D = 3
     grid = GridSpec(3, (-h, -h, -h), h, tuple(c + 3 for c in cells))
     ext = tuple(c * h for c in cells)
     parts = seed_box(grid, (0.0, 0.0, 0.0), ext, ppc, 2000.0)
     n_strip = _strip_traction(parts, D, ext, frac, t_hat, axes=[0])
-    mat = MaterialSpec("neo_hookean", ElasticParams(E, nu))
-    return Problem("cfg4_footing3d_nh", grid, parts, mat, SolverOptions(tol=1e-10), _column_fixed(grid, ext),
-                   np.array([0.0, 0.0, -9.81]), steps,
-                   note="neo-Hookean substitute for modified Cam-Clay (unpinned); strip traction footing",
-                   meta={"strip_particles": n_strip})
+    if material == "cam_clay":
+        mat = MaterialSpec("cam_clay", ElasticParams(E, nu), **CAM_CLAY)
+        name, note = "cfg4_footing3d_mcc", "modified Cam-Clay (extension, parity unpinned); strip traction footing"
+    else:
+        mat = MaterialSpec(material, ElasticParams(E, nu))
+        name = "cfg4_footing3d_nh" if material == "neo_hookean" else f"cfg4_footing3d_{material}"
+        note = "neo-Hookean substitute for modified Cam-Clay (unpinned); strip traction footing"
+    return Problem(name, grid, parts, mat, SolverOptions(tol=1e-10), _column_fixed(grid, ext),
+                   np.array([0.0, 0.0, -9.81]), steps, note=note, meta={"strip_particles": n_strip})
 
 
 def footing3d_slab(nranks, rank, cells=(128, 128, 64), ppc=2, h=0.5, steps=20, t_hat=100e3, frac=0.125, E=10e6,
