@@ -187,6 +187,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="product", choices=["product", "reference"])
     ap.add_argument("--config", default="cfg4", choices=["cfg4", "cfg1"])
+    ap.add_argument("--material", default="neo_hookean", choices=["neo_hookean", "cam_clay", "hencky_j2", "hencky"],
+                    help="cfg4/cfg5 material: neo-Hookean (pinned substitute, default) or an unpinned extension")
     ap.add_argument("--e2e-steps", type=int, default=None, help="timed end-to-end load steps (default: --steps)")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
@@ -248,9 +250,9 @@ def main():
         comm = Communicator.nccl(rank, world, device, broadcast=bcast)
         if args.config != "cfg4":
             raise SystemExit("multi-GPU runs use the cfg 5 slab workload (--config cfg4)")
-        prob = workloads.footing3d_slab(world, rank)
+        prob = workloads.footing3d_slab(world, rank, material=args.material)
     elif args.config == "cfg4":
-        prob = workloads.footing3d()
+        prob = workloads.footing3d(material=args.material)
     else:
         prob = workloads.column2d_nh()
     D = prob.grid.dim

@@ -242,6 +242,7 @@ struct Sim {
   // 3D tangent: one dual direction per pass (160 registers, 9 passes) beats
   // three per pass (255 registers, 12% occupancy): 13.7 -> 10.3 ms per step
   bool tangent_k1 = true;
+  bool krylov_debug = std::getenv("IMPM_DEBUG_KRYLOV") != nullptr;
 
   // slab decomposition along axis 0; comm == nullptr or a
   // single rank -> the plain single-GPU path
@@ -1611,7 +1612,9 @@ struct Sim {
     gm_part.ensure(static_cast<size_t>(m + 1) * kGmBlocks);
     gm_h.ensure(m + 1);
     std::vector<double> hbuf(m + 1);
-    const int max_it = opt.krylov_max_iter > 0 ? opt.krylov_max_iter : std::max(2000, 20 * ndg());
+    const int max_it = opt.krylov_max_iter > 0 ? opt.krylov_max_iter
+                       : mgp                   ? 5000
+                                               : std::max(2000, 20 * ndg());
     if (mgp) mg_setup<DD, FE>();
     CK(cudaMemsetAsync(dflag.p, 0, sizeof(int), s));
     gm_V.ensure(static_cast<size_t>(m + 1) * n);
@@ -1625,7 +1628,7 @@ struct Sim {
     std::vector<double> H(static_cast<size_t>(m + 1) * m), cs(m), sn(m), gv(m + 1), y(m);
     int total = 0;
     CK(cudaMemcpyAsync(kr.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));  // r = b (x = 0)
-    double beta = bnorm;
+    double beta = bnorm, prev_beta = INFINITY;
     while (total < max_it) {
       double* V0 = gm_V.p;
       axpbypcz(1.0 / beta, kr.p, 0.0, V0);
@@ -1686,8 +1689,16 @@ struct Sim {
       CK(cudaMemcpyAsync(kr.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
       axpbypcz(-1.0, kq.p, 1.0, kr.p);
       beta = std::sqrt(dot_sync(kr.p, kr.p));
+      if (krylov_debug)
+        std::fprintf(stderr, "[gmres] it %d true rel %.3e target %.3e (arnoldi est %.3e)\n", total, beta / bnorm,
+                     tol / bnorm, std::abs(gv[j]) / bnorm);
       if (!(beta == beta)) throw SimError(IMPM_ERR_LINEAR_SOLVER, "GMRES breakdown: NaN residual");
       if (beta <= tol) return total;
+      // attainable accuracy: the Arnoldi estimate met the target but the true
+      // residual did not move over a restart (rounding in b - Jx at cond ~1e15
+      // with a tiny warm-started rhs). The Newton test decides from here.
+      if (std::abs(gv[j]) <= tol && beta > 0.5 * prev_beta && beta <= 1e-3 * bnorm) return total;
+      prev_beta = beta;
     }
     const double rel = beta / bnorm;
     if (!(rel <= 1e-6)) throw SimError(IMPM_ERR_LINEAR_SOLVER, "GMRES did not converge: relative residual " +
@@ -1704,7 +1715,10 @@ struct Sim {
       // non-associative Drucker-Prager flow gives a nonsymmetric J -> GMRES;
       // MG right-preconditions GMRES for DP; the u-p saddle point uses block Jacobi
       const bool nonsym = coupled || mat.kind == kDruckerPrager || mat.kind == kCamClay;
-      const bool mgp = opt.precond == IMPM_PRECOND_MG && !coupled;
+      // u-p: GMRES right-preconditioned by the same geometric MG on the 3x3
+      // node blocks (u_x, u_y, p): the block-Jacobi smoother inverts each
+      // node's u-p coupling, Galerkin coarse levels keep it
+      const bool mgp = opt.precond == IMPM_PRECOND_MG;
       if (!nonsym && opt.krylov != IMPM_KRYLOV_BICGSTAB && opt.krylov != IMPM_KRYLOV_GMRES) {
         const int it = mgp ? cg_mg_solve<DD, FE>(rhs, x) : cg_solve<FE>(rhs, x);
         if (it >= 0) {
@@ -2003,9 +2017,14 @@ struct Sim {
       diff_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - tj).count();
       auto ts = std::chrono::steady_clock::now();
       axpbypcz(-1.0, r.p, 0.0, tmp2.p);
-      // strict tolerance here: the u-p saddle point (cond ~1e15) does not let
-      // the residual bound the state, so no relaxed forcing term
+      // forcing term against the reference's convergence scale (porous.cpp:
+      // 105-110, 135): |J d + r| <= 1% of tol * r_scale adds at most 1% of the
+      // Newton tolerance to the next residual. Warm-started steps begin with
+      // |r| << r_scale, where a relative 1e-12 of |r| is below the attainable
+      // accuracy of the saddle point (cond ~1e15); floor = krylov_rtol.
+      cur_rtol = std::min(1e-6, std::max(opt.krylov_rtol, 0.01 * opt.tol * denom / std::max(rn, 1e-300)));
       kry += solve_dev(tmp2.p, delta.p);
+      cur_rtol = opt.krylov_rtol;
       solve_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - ts).count();
       axpbypcz(1.0, delta.p, 1.0, u.p);
       rn = residual_up(u.p, dt, r.p);

@@ -124,7 +124,7 @@ def footing3d(cells=(128, 128, 64), ppc=2, h=0.5, steps=20, t_hat=100e3, frac=0.
 
 
 def footing3d_slab(nranks, rank, cells=(128, 128, 64), ppc=2, h=0.5, steps=20, t_hat=100e3, frac=0.125, E=10e6,
-                   nu=0.3, density=2000.0):
+                   nu=0.3, density=2000.0, material="neo_hookean"):
     """cfg 5 (weak scaling): cfg 4 per GPU stacked along axis 0, i.e. the
     footing3d problem on (cells[0] * nranks) x cells[1] x cells[2] cells, of
     which only rank `rank`'s slab (owned + ghost particles) is generated. The
@@ -154,12 +154,43 @@ def footing3d_slab(nranks, rank, cells=(128, 128, 64), ppc=2, h=0.5, steps=20, t
     top = 0.0 + (sub[2] - 1 + 0.5) * spacing
     sel = (pa.X[:, 2] >= top - 1e-9) & (pa.X[:, 0] >= lo) & (pa.X[:, 0] <= hi)
     pa.traction_force[sel, 2] = -t_hat * area / max(n_strip, 1)
-    mat = MaterialSpec("neo_hookean", ElasticParams(E, nu))
-    return Problem(f"cfg5_footing3d_nh_slab{rank}of{nranks}", grid, parts, mat, SolverOptions(tol=1e-10),
+    if material == "cam_clay":
+        mat = MaterialSpec("cam_clay", ElasticParams(E, nu), **CAM_CLAY)
+    else:
+        mat = MaterialSpec(material, ElasticParams(E, nu))
+    tag = "nh" if material == "neo_hookean" else ("mcc" if material == "cam_clay" else material)
+    return Problem(f"cfg5_footing3d_{tag}_slab{rank}of{nranks}", grid, parts, mat, SolverOptions(tol=1e-10),
                    _column_fixed(grid, ext), np.array([0.0, 0.0, -9.81]), steps,
                    note="cfg4 per GPU stacked along axis 0; neo-Hookean substitute for modified Cam-Clay (unpinned)",
                    meta={"ids": ids, "cuts": cuts, "strip_particles": n_strip, "rank": rank, "nranks": nranks,
                          "global_particles": int(np.prod(sub))})
+
+
+def terzaghi2d(cells=(512, 512), ppc=2, height=10.0, t_hat=1e3, tol=1e-10):
+    """cfg 3: 2D Terzaghi consolidation with coupled u-p (CoupledSim, 3x3 BSR
+    blocks), 512x512 cells, ppc 2 (1,048,576 particles). The reference's
+    consolidation scenario (configs/consolidation.cfg, src/scenarios.cpp:387-418:
+    lambda = mu = 600 kPa, k = 1e-12 m^2, mu_f = 0.1 Pa s, drained top, base
+    fixed, lateral rollers, 1 kPa surface traction) widened from one column to
+    a square block. Returns a ready CoupledSim and its parameters."""
+    from .sim import CoupledSim, PoroParams
+
+    nx, ny = cells
+    h = height / ny
+    grid = GridSpec(2, (-h, -h), h, (nx + 3, ny + 3))
+    parts = seed_box(grid, (0.0, 0.0), (nx * h, height), ppc, 2000.0)
+    pa = ParticleArray(parts, 2)
+    top = pa.X[:, 1] >= pa.X[:, 1].max() - 1e-9
+    pa.traction_force[top, 1] = -t_hat * (nx * h) / top.sum()
+    pp = PoroParams(600e3, 600e3, 1e-12, 0.1, 1000.0)
+    sim = CoupledSim(grid, parts, pp, SolverOptions(tol=tol))
+    width = nx * h
+    sim.fix_displacement(lambda x: (x[:, 0] <= 1e-12) | (x[:, 0] >= width - 1e-9), 0)
+    sim.fix_displacement(lambda x: x[:, 1] <= 1e-12)
+    sim.fix_pressure(lambda x: x[:, 1] >= height - 1e-9)
+    sim.initialize()
+    return sim, {"height": height, "t_hat": t_hat, "c_v": 1e-12 * (600e3 + 2 * 600e3) / 0.1, "h": h,
+                 "particles": parts.shape[0]}
 
 
 def by_name(name, **kw):

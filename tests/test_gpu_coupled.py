@@ -56,3 +56,36 @@ def test_coupled_steps_counts_settlement_pressure():
     scale = np.maximum(np.abs(ref).max(axis=0), 1e-300)
     err = np.abs(got - ref).max(axis=0) / scale
     assert err[np.abs(ref).max(axis=0) > 1e-12].max() <= 1e-7
+
+
+def test_cfg3_terzaghi_full_size_matches_series_solution():
+    """BASELINE cfg 3 at full size: 2D Terzaghi consolidation, 512x512 cells,
+    1,048,576 particles, coupled u-p (3x3 blocks, ~790k DOFs). Size-independent
+    check: the pressure profile against the series solution (porous.cpp:8-15)
+    within the reference's own acceptance bound (L2 <= 0.02,
+    src/scenarios.cpp consolidation.terzaghi_L2_Tv_*), drained-top
+    dissipation monotone, and the Newton count the reference needs on the
+    column (2 per step)."""
+    from paper_2507_09435_b200 import workloads
+    from paper_2507_09435_b200.scenarios import terzaghi_pressure_ratio
+
+    sim, prm = workloads.terzaghi2d(cells=(512, 512))
+    assert prm["particles"] == 1_048_576
+    H, cv, t_hat = prm["height"], prm["c_v"], prm["t_hat"]
+    Tv = 0.05
+    n = 10
+    dt = Tv * H * H / cv / n
+    pmax_prev = np.inf
+    for _ in range(n):
+        rec = sim.step(dt)
+        assert rec.iterations <= 3
+        prof = sim.pressure_profile(256, H)
+        pmax = max(p for _, p in prof)
+        assert pmax <= pmax_prev * (1 + 1e-9)
+        pmax_prev = pmax
+    num = den = 0.0
+    for depth, p in prof:
+        pa = t_hat * terzaghi_pressure_ratio(depth / H, Tv)
+        num += (p - pa) ** 2
+        den += pa * pa
+    assert np.sqrt(num / den) <= 0.02
