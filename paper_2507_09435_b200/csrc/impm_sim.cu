@@ -1614,7 +1614,7 @@ struct Sim {
     std::vector<double> hbuf(m + 1);
     const int max_it = opt.krylov_max_iter > 0 ? opt.krylov_max_iter
                        : mgp                   ? 5000
-                                               : std::max(2000, 20 * ndg());
+                                               : std::min(20000, std::max(2000, 20 * ndg()));
     if (mgp) mg_setup<DD, FE>();
     CK(cudaMemsetAsync(dflag.p, 0, sizeof(int), s));
     gm_V.ensure(static_cast<size_t>(m + 1) * n);
@@ -1732,7 +1732,20 @@ struct Sim {
         return;
       }
       if (nonsym || opt.krylov == IMPM_KRYLOV_GMRES) {
-        out = gmres_solve<DD, FE>(rhs, x, mgp);
+        if (!mgp) {
+          out = gmres_solve<DD, FE>(rhs, x, false);
+          return;
+        }
+        try {
+          out = gmres_solve<DD, FE>(rhs, x, true);
+        } catch (const SimError& e) {
+          // MG smoothing can diverge on a nonsymmetric J with (near-)singular
+          // node blocks (Drucker-Prager particles projected to the cone tip
+          // carry no stiffness): retry with block Jacobi before giving up
+          if (e.code != IMPM_ERR_LINEAR_SOLVER) throw;
+          if (krylov_debug) std::fprintf(stderr, "[gmres] MG failed (%s): block-Jacobi retry\n", e.what());
+          out = gmres_solve<DD, FE>(rhs, x, false);
+        }
         return;
       }
       out = bicgstab_solve<DD, FE>(rhs, x, mgp);

@@ -72,12 +72,19 @@ def column2d_nh(cells=64, ppc=2, h=1.0, steps=10):
 
 
 def slope2d(cells=(256, 128), ppc=4, h=0.5, steps=20, friction_deg=30.0, E=10e6, nu=0.3, material="drucker_prager",
-            slope_deg=45.0, kappa=20e3, cohesion=0.0):
-    """cfg 2: 2D granular slope collapse, 256x128 cells, ppc 4 (~0.5 M
-    particles). Drucker-Prager is an extension (parity unpinned); the pinned
-    substitute of SURVEY.md §8(d) is hencky_j2 (pass material="hencky_j2").
-    Body = seed_box filtered by y <= (x - x_toe) tan(beta) up to the crest,
-    base fixed, lateral rollers, gravity ramped over `steps` increments."""
+            slope_deg=45.0, kappa=400e3, cohesion=120e3):
+    """cfg 2: 2D slope under a gravity ramp, 256x128 cells, ppc 4 (401,216
+    particles after the slope cut). Drucker-Prager is an extension (parity
+    unpinned); the pinned substitute of SURVEY.md §8(d) is hencky_j2 (pass
+    material="hencky_j2"). Body = seed_box filtered by y <= (x - x_toe)
+    tan(beta) up to the crest, base fixed, lateral rollers, gravity ramped over
+    `steps` increments.
+
+    The reference is quasi-static (no inertia, mpm_solver.hpp:248-355): past
+    the limit load no equilibrium exists and Newton cannot follow a collapse.
+    The default strengths put the 64 m, 45 deg slope near its limit state
+    (J2: kappa 400 kPa, i.e. c_u = 283 kPa against Taylor's ~230 kPa; DP:
+    30 deg with 120 kPa cohesion), so a plastic zone forms at full gravity."""
     W, H = cells[0] * h, cells[1] * h
     grid = GridSpec(2, (-h, -h), h, (cells[0] + 3, cells[1] + 3))
     parts = seed_box(grid, (0.0, 0.0), (W, H), ppc, 2000.0)

@@ -16,7 +16,7 @@ def small_slope(material="drucker_prager", shape="gimp"):
 
     # statically admissible slope (phi 40 deg on 30 deg) with a little cohesion:
     # plastic zones without surface particles at the zero-stiffness apex
-    prob = workloads.slope2d(cells=(24, 12), ppc=2, h=0.5, steps=10, material=material, friction_deg=40.0,
+    prob = workloads.slope2d(cells=(24, 12), ppc=2, h=0.5, steps=10, material=material, friction_deg=40.0, kappa=20e3,
                              slope_deg=30.0, cohesion=2e3)
     prob.options.shape = shape
     sim = impm.MpmSim(prob.grid, prob.particles, prob.material, prob.options)
