@@ -707,6 +707,107 @@ __global__ void __launch_bounds__(WARPS * 32) k_residual_bins(
   }
 }
 
+// Staged variant of k_residual_bins: the bin's particles are processed in
+// chunks of PCH with every global load of the chunk in flight at once
+// (positions, lp, nominal stress P, external-force density) into shared
+// memory, the 1D weights of all chunk particles computed in parallel, then the
+// node lanes sum from shared memory in the same fixed particle order (bitwise
+// the values of k_residual_bins). Removes the per-particle load->sync->FMA
+// latency chain of the unstaged loop.
+template <int D, int SHAPE, int WARPS, int PCH>
+__global__ void __launch_bounds__(WARPS * 32) k_residual_bins_staged(
+    GridC g, const double* __restrict__ pd, int64_t cap, const double* __restrict__ xs,
+    const int* __restrict__ bin_start, const uint8_t* __restrict__ bflag, const double* __restrict__ Pst,
+    const double* __restrict__ bext, double load_scale, double* __restrict__ r, int c0, int c1, int c2, int nb0,
+    int nb1, int nb2) {
+  constexpr int DD = D * D;
+  __shared__ double Ps[WARPS][PCH * DD];
+  __shared__ double Bs[WARPS][PCH][D];
+  __shared__ double W1[WARPS][PCH][D][3][2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nbins = nb0 * nb1 * nb2;
+  const int col[3] = {c0, c1, c2};
+  const int nbv[3] = {nb0, nb1, nb2};
+  for (int bi = blockIdx.x * WARPS + warp; bi < nbins; bi += gridDim.x * WARPS) {
+    int bidx[3] = {0, 0, 0}, rr = bi, b = 0;
+#pragma unroll
+    for (int a = D - 1; a >= 0; --a) {
+      bidx[a] = 3 * (rr % nbv[a]) + col[a];
+      rr /= nbv[a];
+      b += bidx[a] * g.stride[a];
+    }
+    const int fl = bflag[b];
+    if (!(fl & 0x80)) continue;
+    int cn[3] = {1, 1, 1};
+#pragma unroll
+    for (int a = 0; a < D; ++a) cn[a] = 2 + ((fl >> a) & 1);
+    const int nk = cn[0] * cn[1] * cn[2];
+    int li[3] = {0, 0, 0};
+    {
+      int rk = lane;
+#pragma unroll
+      for (int a = D - 1; a >= 0; --a) {
+        li[a] = rk % cn[a];
+        rk /= cn[a];
+      }
+    }
+    double acc[3] = {0.0, 0.0, 0.0};
+    const int p0 = bin_start[b], p1 = bin_start[b + 1];
+    for (int pc = p0; pc < p1; pc += PCH) {
+      const int np = min(PCH, p1 - pc);
+      __syncwarp();
+      // P of the chunk is contiguous (particle-major, D*D per particle)
+      const double* Pb = Pst + static_cast<int64_t>(pc) * DD;
+      for (int e = lane; e < np * DD; e += 32) Ps[warp][e] = __ldg(Pb + e);
+      for (int e = lane; e < np * D; e += 32) {
+        const int pl = e / D, c = e - pl * D;
+        Bs[warp][pl][c] = __ldg(bext + c * cap + pc + pl);
+      }
+      for (int e = lane; e < np * D * 3; e += 32) {
+        const int pl = e / (D * 3), rem = e - pl * D * 3, a = rem / 3, i = rem - a * 3;
+        double w = 0.0, dw = 0.0;
+        if (i < cn[a]) {
+          const int p = pc + pl;
+          const WeightValue wv = weight_1d<SHAPE>(__ldg(xs + a * cap + p) - node_coord(g, a, bidx[a] + i),
+                                                  __ldg(pd + (PF<D>::lp + a) * cap + p), g.h);
+          w = wv.w;
+          dw = wv.dw;
+        }
+        W1[warp][pl][a][i][0] = w;
+        W1[warp][pl][a][i][1] = dw;
+      }
+      __syncwarp();
+      if (lane < nk) {
+        for (int pl = 0; pl < np; ++pl) {
+          double w[3], dw[3], W, gr[3];
+#pragma unroll
+          for (int a = 0; a < D; ++a) {
+            w[a] = W1[warp][pl][a][li[a]][0];
+            dw[a] = W1[warp][pl][a][li[a]][1];
+          }
+          tensor_weight<D>(w, dw, W, gr);
+          const double* Pp = &Ps[warp][pl * DD];
+#pragma unroll
+          for (int c = 0; c < D; ++c) {
+            double fint = gr[0] * Pp[c * D];
+#pragma unroll
+            for (int bb = 1; bb < D; ++bb) fint += gr[bb] * Pp[c * D + bb];
+            const double fext = W * Bs[warp][pl][c] * load_scale;  // same association as k_residual_bins
+            acc[c] += fint - fext;
+          }
+        }
+      }
+    }
+    if (lane < nk) {
+      int node = 0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) node += (bidx[a] + li[a]) * g.stride[a];
+#pragma unroll
+      for (int c = 0; c < D; ++c) r[static_cast<int64_t>(node) * D + c] += acc[c];
+    }
+  }
+}
+
 // r <- r at free DOFs, 0 elsewhere; partial sums of r.r
 __global__ void k_mask_norm(int64_t n, const uint8_t* __restrict__ freem, double* __restrict__ r,
                             double* __restrict__ partials) {

@@ -243,6 +243,7 @@ struct Sim {
   // three per pass (255 registers, 12% occupancy): 13.7 -> 10.3 ms per step
   bool tangent_k1 = true;
   bool krylov_debug = std::getenv("IMPM_DEBUG_KRYLOV") != nullptr;
+  bool res_staged = !(std::getenv("IMPM_RES_UNSTAGED") && std::atoi(std::getenv("IMPM_RES_UNSTAGED")) != 0);
 
   // slab decomposition along axis 0; comm == nullptr or a
   // single rank -> the plain single-GPU path
@@ -952,9 +953,15 @@ struct Sim {
           }
           const int nbins = nb[0] * nb[1] * nb[2];
           if (nbins == 0) continue;
-          k_residual_bins<DD, SH, W><<<std::min<unsigned>(blocks_for(nbins, W), 148 * 16), W * 32, 0, s>>>(
-              g, pd.p, cap, xs.p, bin_start.p, bflag.p, Pst.p, bext.p, load_scale, rd, cc[0], cc[1], cc[2], nb[0],
-              nb[1], nb[2]); ++g_launches;
+          if (res_staged)
+            k_residual_bins_staged<DD, SH, W, 16><<<std::min<unsigned>(blocks_for(nbins, W), 148 * 16), W * 32, 0, s>>>(
+                g, pd.p, cap, xs.p, bin_start.p, bflag.p, Pst.p, bext.p, load_scale, rd, cc[0], cc[1], cc[2], nb[0],
+                nb[1], nb[2]);
+          else
+            k_residual_bins<DD, SH, W><<<std::min<unsigned>(blocks_for(nbins, W), 148 * 16), W * 32, 0, s>>>(
+                g, pd.p, cap, xs.p, bin_start.p, bflag.p, Pst.p, bext.p, load_scale, rd, cc[0], cc[1], cc[2], nb[0],
+                nb[1], nb[2]);
+          ++g_launches;
         }
         k_mask_norm<<<kRedBlocks, kThreads, 0, s>>>(NF(), freem.p, rd, partials.p); ++g_launches;
         CKL();
