@@ -803,7 +803,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_residual_bins_staged(
 #pragma unroll
       for (int a = 0; a < D; ++a) node += (bidx[a] + li[a]) * g.stride[a];
 #pragma unroll
-      for (int c = 0; c < D; ++c) r[static_cast<int64_t>(node) * D + c] += acc[c];
+      for (int c = 0; c < D; ++c) atomicAdd(r + static_cast<int64_t>(node) * D + c, acc[c]);  // RED, one writer per colour
     }
   }
 }
@@ -990,6 +990,20 @@ __device__ __forceinline__ int mask_pos(const unsigned* m, int sl) {
   return pos + __popc(m[w] & ((1u << (sl & 31)) - 1u));
 }
 
+__device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+
+// mask_pos over a register copy of the row's 128-bit slot mask (no dynamic
+// indexing, so the words stay in registers)
+__device__ __forceinline__ int mask_pos_r(const unsigned (&m)[4], int sl) {
+  const int w = sl >> 5;
+  int pos = 0;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+    if (i < w) pos += __popc(m[i]);
+  const unsigned mw = w == 0 ? m[0] : (w == 1 ? m[1] : (w == 2 ? m[2] : m[3]));
+  return pos + __popc(mw & ((1u << (sl & 31)) - 1u));
+}
+
 // zero the stored part of every row (component chunks incl. padding)
 __global__ void k_zero_rows(int n_act, int F, const int* __restrict__ row_nzb, double* __restrict__ vals,
                             int64_t row_len) {
@@ -1165,6 +1179,10 @@ __global__ void __launch_bounds__(WARPS * 32) k_assemble_bins_staged(
   __shared__ double As[WARPS][PCH * NA];
   __shared__ double Gs[WARPS][PCH][NK][D];
   __shared__ double Hs[WARPS][NK * D3];
+  // row metadata of the bin's box nodes: row index, slot mask, component pitch
+  __shared__ int Rrow[WARPS][NK];
+  __shared__ int Rcp[WARPS][NK];
+  __shared__ uint4 Rmask[WARPS][NK];
   __shared__ double W1[WARPS][PCH][D][3][2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nbins = nb0 * nb1 * nb2;
@@ -1208,6 +1226,27 @@ __global__ void __launch_bounds__(WARPS * 32) k_assemble_bins_staged(
         l_out = (t - k_out * nchunk) * PPL;
       }
     };
+    // stage the box nodes' row metadata once per bin (all lanes in parallel)
+    // so that the per-task block lookups read shared memory only
+    __syncwarp();
+    if (lane < nk) {
+      int rk = lane, node = 0;
+      int li[3] = {0, 0, 0};
+#pragma unroll
+      for (int a = D - 1; a >= 0; --a) {
+        li[a] = rk % cn[a];
+        rk /= cn[a];
+      }
+#pragma unroll
+      for (int a = 0; a < D; ++a) node += (bidx[a] + li[a]) * g.stride[a];
+      const int rw = act_idx[node];
+      Rrow[warp][lane] = rw;
+      if (rw >= 0) {
+        Rmask[warp][lane] = *reinterpret_cast<const uint4*>(row_mask + static_cast<int64_t>(rw) * 4);
+        Rcp[warp][lane] = cpad(row_nzb[rw], D);
+      }
+    }
+    __syncwarp();
     const int p0 = bin_start[b], p1 = bin_start[b + 1];
     for (int r0 = 0; r0 < ntasks; r0 += 32) {
       const int task = r0 + lane;
@@ -1219,12 +1258,50 @@ __global__ void __launch_bounds__(WARPS * 32) k_assemble_bins_staged(
       for (int t = 0; t < PPL; ++t)
 #pragma unroll
         for (int e = 0; e < DD; ++e) acc[t][e] = 0.0;
+      // the task's row metadata (node -> row -> slot mask, padding) is a
+      // dependent chain of global loads: issue it now, consume it after the
+      // particle loop
+      int lk[3] = {0, 0, 0}, row = -1, cp = 0;
+      unsigned rm[4] = {0u, 0u, 0u, 0u};
+      if (has_task) {
+        int rk = tk, node = 0;
+#pragma unroll
+        for (int a = D - 1; a >= 0; --a) {
+          lk[a] = rk % cn[a];
+          rk /= cn[a];
+        }
+#pragma unroll
+        (void)node;
+        row = Rrow[warp][tk];
+        if (row >= 0) {
+          const uint4 m4 = Rmask[warp][tk];
+          rm[0] = m4.x;
+          rm[1] = m4.y;
+          rm[2] = m4.z;
+          rm[3] = m4.w;
+          cp = Rcp[warp][tk];
+        }
+      }
       for (int pc = p0; pc < p1; pc += PCH) {
         const int np = min(PCH, p1 - pc);
         __syncwarp();
-        // stage A_p (contiguous) and the 1D weights of the chunk
+        // stage A_p (contiguous) and the 1D weights of the chunk; the A loads
+        // go to registers first so that all of them are in flight at once
         const double* Ab = A + static_cast<int64_t>(pc) * NA;
-        for (int e = lane; e < np * NA; e += 32) As[warp][e] = __ldg(Ab + e);
+        {
+          constexpr int NL = (PCH * NA + 31) / 32;
+          double ta[NL];
+#pragma unroll
+          for (int i = 0; i < NL; ++i) {
+            const int e = lane + 32 * i;
+            ta[i] = e < np * NA ? __ldg(Ab + e) : 0.0;
+          }
+#pragma unroll
+          for (int i = 0; i < NL; ++i) {
+            const int e = lane + 32 * i;
+            if (e < np * NA) As[warp][e] = ta[i];
+          }
+        }
         for (int e = lane; e < np * D * 3; e += 32) {
           const int pl = e / (D * 3), rem = e - pl * D * 3, a = rem / 3, i = rem - a * 3;
           double w = 0.0, dw = 0.0;
@@ -1295,18 +1372,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_assemble_bins_staged(
         }
       }
       if (has_task) {
-        int lk[3] = {0, 0, 0}, rk = tk, node = 0;
-#pragma unroll
-        for (int a = D - 1; a >= 0; --a) {
-          lk[a] = rk % cn[a];
-          rk /= cn[a];
-        }
-#pragma unroll
-        for (int a = 0; a < D; ++a) node += (bidx[a] + lk[a]) * g.stride[a];
-        const int row = act_idx[node];
         if (row >= 0) {
-          const unsigned* m = row_mask + static_cast<int64_t>(row) * 4;
-          const int cp = cpad(row_nzb[row], D);
           double* rbase = vals + static_cast<int64_t>(row) * row_len;
 #pragma unroll
           for (int t = 0; t < PPL; ++t) {
@@ -1320,11 +1386,15 @@ __global__ void __launch_bounds__(WARPS * 32) k_assemble_bins_staged(
             }
 #pragma unroll
             for (int a = 0; a < D; ++a) sl = sl * 5 + (ll[a] - lk[a] + 2);
-            double* rv = rbase + mask_pos(m, sl) * D;
+            double* rv = rbase + mask_pos_r(rm, sl) * D;
+            // fire-and-forget L2 reductions (RED.ADD.F64, result unused): one
+            // writer per address per colour launch and launches in stream
+            // order, so the sum is the same deterministic RMW without the
+            // warp waiting on the DRAM read
 #pragma unroll
             for (int c = 0; c < D; ++c)
 #pragma unroll
-              for (int d = 0; d < D; ++d) rv[c * cp + d] += acc[t][c * D + d];
+              for (int d = 0; d < D; ++d) atomicAdd(rv + c * cp + d, acc[t][c * D + d]);
           }
         }
         if constexpr (SYM) {
@@ -1344,15 +1414,17 @@ __global__ void __launch_bounds__(WARPS * 32) k_assemble_bins_staged(
               nodel += (bidx[a] + ll[a]) * g.stride[a];
               sl = sl * 5 + (lk[a] - ll[a] + 2);
             }
-            const int rowl = act_idx[nodel];
+            (void)nodel;
+            const int rowl = Rrow[warp][l];
             if (rowl < 0) continue;
-            const unsigned* ml = row_mask + static_cast<int64_t>(rowl) * 4;
-            const int cpl = cpad(row_nzb[rowl], D);
-            double* rv = vals + static_cast<int64_t>(rowl) * row_len + mask_pos(ml, sl) * D;
+            const uint4 m4 = Rmask[warp][l];
+            const unsigned ml[4] = {m4.x, m4.y, m4.z, m4.w};
+            const int cpl = Rcp[warp][l];
+            double* rv = vals + static_cast<int64_t>(rowl) * row_len + mask_pos_r(ml, sl) * D;
 #pragma unroll
             for (int c = 0; c < D; ++c)
 #pragma unroll
-              for (int d = 0; d < D; ++d) rv[c * cpl + d] += acc[t][d * D + c];
+              for (int d = 0; d < D; ++d) atomicAdd(rv + c * cpl + d, acc[t][d * D + c]);
           }
         }
       }
