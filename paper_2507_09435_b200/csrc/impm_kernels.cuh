@@ -1258,20 +1258,16 @@ __global__ void __launch_bounds__(WARPS * 32) k_assemble_bins_staged(
       for (int t = 0; t < PPL; ++t)
 #pragma unroll
         for (int e = 0; e < DD; ++e) acc[t][e] = 0.0;
-      // the task's row metadata (node -> row -> slot mask, padding) is a
-      // dependent chain of global loads: issue it now, consume it after the
-      // particle loop
+      // the task's row metadata (staged per bin in shared memory)
       int lk[3] = {0, 0, 0}, row = -1, cp = 0;
       unsigned rm[4] = {0u, 0u, 0u, 0u};
       if (has_task) {
-        int rk = tk, node = 0;
+        int rk = tk;
 #pragma unroll
         for (int a = D - 1; a >= 0; --a) {
           lk[a] = rk % cn[a];
           rk /= cn[a];
         }
-#pragma unroll
-        (void)node;
         row = Rrow[warp][tk];
         if (row >= 0) {
           const uint4 m4 = Rmask[warp][tk];
