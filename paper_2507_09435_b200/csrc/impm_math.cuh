@@ -12,6 +12,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <type_traits>
 
 #ifndef IMPM_HD
 #define IMPM_HD __host__ __device__ __forceinline__
@@ -747,6 +748,16 @@ IMPM_HD StressOut<T> dp_update(const Mat<T, D>& F_new, const Mat<T, D>& f_incr, 
     eps = Mat<T, 3>::zero();
 #pragma unroll
     for (int i = 0; i < 3; ++i) eps(i, i) = T(e_c / 3.0);
+    // the tip carries no stiffness: a node whose particles all sit there makes
+    // J singular. The TANGENT (dual parts only; the residual value is the exact
+    // projection) keeps 1e-6 of the elastic response, a modified-Newton
+    // regularisation that leaves converged states unchanged.
+    if constexpr (!std::is_same<T, double>::value) {
+#pragma unroll
+      for (int i = 0; i < 9; ++i)
+#pragma unroll
+        for (int k = 0; k < (int)(sizeof(eps.e[i].d) / sizeof(double)); ++k) eps.e[i].d[k] = 1e-6 * eps_tr.e[i].d[k];
+    }
     T e2 = T(0.0);
 #pragma unroll
     for (int i = 0; i < 9; ++i) e2 += (eps_tr.e[i] - eps.e[i]) * (eps_tr.e[i] - eps.e[i]);

@@ -85,3 +85,37 @@ def test_bspline_partition_of_unity_and_tangent():
     assert fd_check(sim, 0.3, u, 1e-8) <= 1e-5
     rec = sim.step(0.1)
     assert rec.iterations >= 1
+
+
+def test_cfg2_drucker_prager_full_size_gravity_ramp():
+    """BASELINE cfg 2 with its named material at full size (401,216 particles,
+    30 deg / 120 kPa Drucker-Prager on the 45 deg, 64 m slope): all 20 gravity
+    increments converge (the cone-tip tangent regularisation keeps J
+    nonsingular once particles reach the tip), and every particle ends on or
+    inside the cone."""
+    import paper_2507_09435_b200 as impm
+    from paper_2507_09435_b200 import workloads
+
+    prob = workloads.slope2d(material="drucker_prager")
+    sim = impm.MpmSim(prob.grid, prob.particles, prob.material, prob.options)
+    sim.fixed[:] = prob.fixed
+    sim.gravity = prob.gravity
+    for k in range(1, prob.load_steps + 1):
+        rec = sim.step(k / prob.load_steps)
+        assert rec.rel_residuals[-1] <= prob.options.tol
+    p = sim.particles
+    assert (p.alpha[:, 0] > 0).any()
+    E, nu, phi = prob.material.elastic.E, prob.material.elastic.nu, np.radians(prob.material.friction_deg)
+    lam, mu = E * nu / ((1 + nu) * (1 - 2 * nu)), E / (2 * (1 + nu))
+    alpha = np.sqrt(2 / 3) * 2 * np.sin(phi) / (3 - np.sin(phi))
+    e_c = 3 * prob.material.cohesion / (3 * lam + 2 * mu)
+    plastic = p.alpha[:, 0] > 0
+    worst = 0.0
+    for Be in p.B_e.reshape(-1, 3, 3)[plastic]:
+        w, V = np.linalg.eigh(0.5 * (Be + Be.T))
+        eps = (V * (0.5 * np.log(w))) @ V.T
+        tr = np.trace(eps)
+        dev = np.linalg.norm(eps - tr / 3 * np.eye(3))
+        f = dev + (3 * lam + 2 * mu) / (2 * mu) * (tr - e_c) * alpha
+        worst = max(worst, f if tr <= e_c + 1e-12 else np.linalg.norm(eps - e_c / 3 * np.eye(3)))
+    assert worst <= 1e-9
