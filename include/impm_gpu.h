@@ -182,9 +182,11 @@ impm_status impm_sim_step(impm_sim* sim, double load_scale, impm_step_record* re
 impm_status impm_sim_nodal_solution(impm_sim* sim, double* u /*[n]*/);
 impm_status impm_sim_set_nodal_solution(impm_sim* sim, const double* u /*[n]*/);
 
-/* impm::CoupledSim (porous.hpp:48-125): 2D u-p, fields (ux, uy, p) per node,
- * set_fixed takes [node*3 + field] (fixed_u merged with fixed_p). The shared
- * impm_sim_residual / _jacobian_csr / _linear_solve take dt as load_scale. */
+/* impm::CoupledSim (porous.hpp:48-125): u-p, fields (u_0 .. u_{D-1}, p) per
+ * node. D = 2 is the reference; D = 3 (4x4 node blocks) is an extension, parity
+ * unpinned. set_fixed takes [node*(D+1) + field] (fixed_u merged with fixed_p).
+ * The shared impm_sim_residual / _jacobian_csr / _linear_solve take dt as
+ * load_scale. */
 impm_status impm_coupled_create(const impm_grid* grid, const impm_poro* poro, const impm_options* opt,
                                 int32_t device, impm_sim** out);
 /* CoupledSim::initialize (src/porous.cpp:25-72): weights at the reference configuration */

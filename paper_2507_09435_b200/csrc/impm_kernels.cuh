@@ -1432,6 +1432,80 @@ __global__ void __launch_bounds__(WARPS * 32) k_assemble_bins_staged(
 // a free component can carry an exactly zero diagonal (a lone particle with
 // dw = 0 at that node), making the block singular; then fall back to the
 // inverse of the positive diagonal entries (0 for a zero diagonal).
+// 4x4 (3D u-p node blocks): Gauss-Jordan with partial pivoting; the
+// determinant is the signed product of the pivots
+__device__ __forceinline__ double det(const Mat<double, 4>& a) {
+  double m[4][4];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) m[i / 4][i % 4] = a.e[i];
+  double d = 1.0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    int piv = k;
+#pragma unroll
+    for (int i = k + 1; i < 4; ++i)
+      if (fabs(m[i][k]) > fabs(m[piv][k])) piv = i;
+    if (m[piv][k] == 0.0) return 0.0;
+    if (piv != k) {
+      d = -d;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const double t = m[k][j];
+        m[k][j] = m[piv][j];
+        m[piv][j] = t;
+      }
+    }
+    d *= m[k][k];
+#pragma unroll
+    for (int i = k + 1; i < 4; ++i) {
+      const double f = m[i][k] / m[k][k];
+#pragma unroll
+      for (int j = k; j < 4; ++j) m[i][j] -= f * m[k][j];
+    }
+  }
+  return d;
+}
+__device__ __forceinline__ Mat<double, 4> inverse(const Mat<double, 4>& a) {
+  double m[4][8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      m[i][j] = a.e[i * 4 + j];
+      m[i][4 + j] = i == j ? 1.0 : 0.0;
+    }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    int piv = k;
+#pragma unroll
+    for (int i = k + 1; i < 4; ++i)
+      if (fabs(m[i][k]) > fabs(m[piv][k])) piv = i;
+    if (piv != k)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const double t = m[k][j];
+        m[k][j] = m[piv][j];
+        m[piv][j] = t;
+      }
+    const double inv = 1.0 / m[k][k];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) m[k][j] *= inv;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (i != k) {
+        const double f = m[i][k];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) m[i][j] -= f * m[k][j];
+      }
+  }
+  Mat<double, 4> out;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) out.e[i * 4 + j] = m[i][4 + j];
+  return out;
+}
+
 template <int F>
 __device__ __forceinline__ Mat<double, F> safe_block_inverse(const Mat<double, F>& Mb) {
   double mx = 0.0;
@@ -1603,10 +1677,13 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
       if (lane < cp - nzb * F) xs[nzb * F + lane] = VT(0);
       __syncwarp();
       // 3. component-major dot products (buffered head, streamed tail)
-      double acc[3] = {0.0, 0.0, 0.0};
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
       const V16* xv = reinterpret_cast<const V16*>(xs);
       auto consume = [&](int j2, const V16 v) {
-        const int c = F == 1 ? 0 : (F == 2 ? (j2 >= h) : (j2 >= h) + (j2 >= 2 * h));
+        const int c = F == 1   ? 0
+                      : F == 2 ? (j2 >= h)
+                      : F == 3 ? (j2 >= h) + (j2 >= 2 * h)
+                               : (j2 >= h) + (j2 >= 2 * h) + (j2 >= 3 * h);
         double p;
         const V16 xx = xv[j2 - c * h];
         if constexpr (sizeof(VT) == 8) {
@@ -1617,6 +1694,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
         acc[0] += c == 0 ? p : 0.0;
         if (F > 1) acc[1] += c == 1 ? p : 0.0;
         if (F > 2) acc[2] += c == 2 ? p : 0.0;
+        if (F > 3) acc[3] += c == 3 ? p : 0.0;
       };
 #pragma unroll
       for (int t = 0; t < NB; ++t) {
@@ -1632,6 +1710,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
       double mine = acc[0];
       if (F > 1 && lane == 1) mine = acc[1];
       if (F > 2 && lane == 2) mine = acc[2];
+      if (F > 3 && lane == 3) mine = acc[3];
       if constexpr (MODE == kSpmvY) {
         if (lane < F) {
           const double v = fm ? mine : 0.0;
@@ -2163,7 +2242,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_galerkin_ptap(GridC gf, GridC gc
       if (frow < 0) continue;
 #pragma unroll
       for (int a = 0; a < D; ++a) wi *= p1w(eo[a]);
-      bool mi[3];
+      bool mi[F];
 #pragma unroll
       for (int c = 0; c < F; ++c) mi[c] = f_freem[static_cast<int64_t>(i) * F + c] != 0;
       const double* Ti = T + static_cast<int64_t>(frow) * NT * FF;
@@ -2221,7 +2300,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_galerkin_ptap(GridC gf, GridC gc
           for (int d = 0; d < F; ++d) rowv[c * cpc + pos * F + d] = acc[t][c * F + d];
       }
       if (js == (S - 1) / 2) {
-        bool fr[3];
+        bool fr[F];
 #pragma unroll
         for (int c = 0; c < F; ++c) {
           fr[c] = acc[t][c * F + c] > 0.0;
@@ -2479,78 +2558,91 @@ __global__ void k_commit(GridC g, double* __restrict__ pd, int64_t cap, int P, c
 }
 
 
-// ======================================================= coupled u-p (2D) ==
+// ================================================= coupled u-p (2D / 3D) ==
 // CoupledSim (porous.hpp:48-186, src/porous.cpp:25-168): small-strain u-p on
 // weights frozen at the reference configuration, 3 fields per node (ux, uy,
 // p), F = 3 blocks. Grid vectors are [node][3].
 struct PoroC {
-  double lam, mu, mob, rho_f, g0, g1;
+  double lam, mu, mob, rho_f, g0, g1, g2;
 };
 
-// residual phase A: per particle Q = {V0 s'(c,b) (4), V0 p_w, V0 dEv, V0 mob gp (2)}
-template <int SHAPE>
+// coupled u-p (porous.hpp:127-186) for D = 2 (the reference) and D = 3
+// (extension, parity unpinned): fields (u_0 .. u_{D-1}, p) per node, F = D + 1.
+// Particle record of phase A: Q = {V0 sigma'(c,b) (D*D), V0 p_w, V0 tr G, V0 mob grad p (D)}
+template <int D>
+struct UpQ {
+  static constexpr int F = D + 1, DD = D * D, N = DD + 2 + D;
+};
+
+__host__ __device__ __forceinline__ double poro_g(const PoroC& pc, int a) { return a == 0 ? pc.g0 : (a == 1 ? pc.g1 : pc.g2); }
+
+// residual phase A (per particle)
+template <int D, int SHAPE>
 __global__ void k_up_particles(GridC g, const double* __restrict__ pd, int64_t cap, int P,
                                const double* __restrict__ xs, const int* __restrict__ key,
                                const int* __restrict__ sup, const int* __restrict__ orig,
                                const double* __restrict__ x, PoroC pc, double* __restrict__ Q,
                                DevStatus* st) {
-  constexpr int D = 2;
+  constexpr int F = UpQ<D>::F, DD = UpQ<D>::DD, QN = UpQ<D>::N;
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= P) return;
   int first[3], cnt[3];
   AxisW aw[3];
   particle_weights<D, SHAPE>(g, pd, cap, xs, p, key[p], sup[p], first, cnt, aw);
-  Mat<double, 2> G = Mat<double, 2>::zero();
-  double pw = 0.0, gp[2] = {0.0, 0.0};
+  Mat<double, D> G = Mat<double, D>::zero();
+  double pw = 0.0, gp[3] = {0.0, 0.0, 0.0};
   for_each_support<D>(g, first, cnt, aw, [&](int node, double W, const double* grad) {
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      const double uc = x[node * 3 + c];
+    for (int c = 0; c < D; ++c) {
+      const double uc = x[node * F + c];
 #pragma unroll
-      for (int a = 0; a < 2; ++a) G(c, a) += uc * grad[a];
+      for (int a = 0; a < D; ++a) G(c, a) += uc * grad[a];
     }
-    const double pv = x[node * 3 + 2];
+    const double pv = x[node * F + D];
     pw += W * pv;
 #pragma unroll
-    for (int a = 0; a < 2; ++a) gp[a] += pv * grad[a];
+    for (int a = 0; a < D; ++a) gp[a] += pv * grad[a];
   });
-  Mat<double, 2> f_inc = G;
-  f_inc(0, 0) += 1.0;
-  f_inc(1, 1) += 1.0;
-  Mat<double, 2> Fn;
+  Mat<double, D> f_inc = G;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) Fn.e[i] = pd[(PF<D>::F + i) * cap + p];
-  const Mat<double, 2> F_new = matmul(f_inc, Fn);
-  double* q = Q + static_cast<int64_t>(p) * 8;
+  for (int a = 0; a < D; ++a) f_inc(a, a) += 1.0;
+  Mat<double, D> Fn;
+#pragma unroll
+  for (int i = 0; i < DD; ++i) Fn.e[i] = pd[(PF<D>::F + i) * cap + p];
+  const Mat<double, D> F_new = matmul(f_inc, Fn);
+  double* q = Q + static_cast<int64_t>(p) * QN;
   if (!(det(F_new) > 0.0)) {  // porous.hpp:159-160
     atomicMin(&st->err_domain, orig[p]);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) q[i] = 0.0;
+    for (int i = 0; i < QN; ++i) q[i] = 0.0;
     return;
   }
-  const StressOut<double> su = neo_hookean_update<double, 2>(F_new, pc.lam, pc.mu);
+  const StressOut<double> su = neo_hookean_update<double, D>(F_new, pc.lam, pc.mu);
   const double V0 = pd[PF<D>::V0 * cap + p];
-  q[0] = V0 * su.sigma(0, 0);
-  q[1] = V0 * su.sigma(0, 1);
-  q[2] = V0 * su.sigma(1, 0);
-  q[3] = V0 * su.sigma(1, 1);
-  q[4] = V0 * pw;
-  q[5] = V0 * (G(0, 0) + G(1, 1));
-  q[6] = V0 * (pc.mob * gp[0]);
-  q[7] = V0 * (pc.mob * gp[1]);
+#pragma unroll
+  for (int c = 0; c < D; ++c)
+#pragma unroll
+    for (int b = 0; b < D; ++b) q[c * D + b] = V0 * su.sigma(c, b);
+  q[DD] = V0 * pw;
+  double trg = G(0, 0);
+#pragma unroll
+  for (int a = 1; a < D; ++a) trg += G(a, a);
+  q[DD + 1] = V0 * trg;
+#pragma unroll
+  for (int a = 0; a < D; ++a) q[DD + 2 + a] = V0 * (pc.mob * gp[a]);
 }
 
 // residual phase B (nodes), porous.hpp:165-184 (masked, + partial r.r)
-template <int SHAPE>
+template <int D, int SHAPE>
 __global__ void k_up_nodes(GridC g, const double* __restrict__ pd, int64_t cap, const double* __restrict__ xs,
                            const int* __restrict__ bin_start, const int* __restrict__ sup,
                            const double* __restrict__ Q, const double* __restrict__ bext,
                            const int* __restrict__ act_flag, const uint8_t* __restrict__ freem, PoroC pc, double dt,
                            double* __restrict__ r, double* __restrict__ partials) {
-  constexpr int D = 2;
+  constexpr int F = UpQ<D>::F, DD = UpQ<D>::DD, QN = UpQ<D>::N;
   double rr[1] = {0.0};
   for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < g.N; n += gridDim.x * blockDim.x) {
-    double acc[3] = {0.0, 0.0, 0.0};
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
     if (act_flag[n]) {
       int idx[3];
       unflat<D>(g, n, idx);
@@ -2565,21 +2657,30 @@ __global__ void k_up_nodes(GridC g, const double* __restrict__ pd, int64_t cap, 
         }
         double W, gr[3];
         tensor_weight<D>(w, dw, W, gr);
-        const double* q = Q + static_cast<int64_t>(p) * 8;
+        const double* q = Q + static_cast<int64_t>(p) * QN;
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          const double fint = gr[0] * q[c * 2] + gr[1] * q[c * 2 + 1] - gr[c] * q[4];
+        for (int c = 0; c < D; ++c) {
+          double fint = gr[0] * q[c * D];
+#pragma unroll
+          for (int b = 1; b < D; ++b) fint += gr[b] * q[c * D + b];
+          fint -= gr[c] * q[DD];
           acc[c] += fint - W * bext[c * cap + p];
         }
         const double V0 = pd[PF<D>::V0 * cap + p];
-        const double flux = gr[0] * q[6] + gr[1] * q[7] - V0 * pc.mob * pc.rho_f * (gr[0] * pc.g0 + gr[1] * pc.g1);
-        acc[2] += W * q[5] + dt * flux;
+        double fl = gr[0] * q[DD + 2], gg = gr[0] * pc.g0;
+#pragma unroll
+        for (int a = 1; a < D; ++a) {
+          fl += gr[a] * q[DD + 2 + a];
+          gg += gr[a] * poro_g(pc, a);
+        }
+        const double flux = fl - V0 * pc.mob * pc.rho_f * gg;
+        acc[D] += W * q[DD + 1] + dt * flux;
       });
     }
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const double v = freem[n * 3 + c] ? acc[c] : 0.0;
-      r[n * 3 + c] = v;
+    for (int c = 0; c < F; ++c) {
+      const double v = freem[static_cast<int64_t>(n) * F + c] ? acc[c] : 0.0;
+      r[static_cast<int64_t>(n) * F + c] = v;
       rr[0] += v * v;
     }
   }
@@ -2587,88 +2688,98 @@ __global__ void k_up_nodes(GridC g, const double* __restrict__ pd, int64_t cap, 
 }
 
 // dP/dG with P = V0 sigma'(f_inc F_n) (the u-p internal force uses reference
-// gradients and V0, porous.hpp:171-173); duals over the 4 entries of G.
-template <int SHAPE>
+// gradients and V0, porous.hpp:171-173); duals over the D*D entries of G.
+template <int D, int SHAPE>
 __global__ void k_up_tangent(GridC g, const double* __restrict__ pd, int64_t cap, int P,
                              const double* __restrict__ xs, const int* __restrict__ key,
                              const int* __restrict__ sup, const double* __restrict__ x, PoroC pc,
                              double* __restrict__ A) {
-  constexpr int D = 2;
-  using T = Dual<4>;
+  constexpr int F = UpQ<D>::F, DD = UpQ<D>::DD;
+  using T = Dual<DD>;
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= P) return;
   int first[3], cnt[3];
   AxisW aw[3];
   particle_weights<D, SHAPE>(g, pd, cap, xs, p, key[p], sup[p], first, cnt, aw);
-  Mat<double, 2> G = Mat<double, 2>::zero();
+  Mat<double, D> G = Mat<double, D>::zero();
   for_each_support<D>(g, first, cnt, aw, [&](int node, double, const double* grad) {
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      const double uc = x[node * 3 + c];
+    for (int c = 0; c < D; ++c) {
+      const double uc = x[node * F + c];
 #pragma unroll
-      for (int a = 0; a < 2; ++a) G(c, a) += uc * grad[a];
+      for (int a = 0; a < D; ++a) G(c, a) += uc * grad[a];
     }
   });
-  Mat<T, 2> f_inc;
+  Mat<T, D> f_inc;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < DD; ++i) {
     f_inc.e[i] = T(G.e[i]);
     f_inc.e[i].d[i] = 1.0;
   }
-  f_inc(0, 0) += 1.0;
-  f_inc(1, 1) += 1.0;
-  Mat<T, 2> FnT;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) FnT.e[i] = T(pd[(PF<D>::F + i) * cap + p]);
-  const Mat<T, 2> F_new = matmul(f_inc, FnT);
-  double* out = A + static_cast<int64_t>(p) * 16;
+  for (int a = 0; a < D; ++a) f_inc(a, a) += 1.0;
+  Mat<T, D> FnT;
+#pragma unroll
+  for (int i = 0; i < DD; ++i) FnT.e[i] = T(pd[(PF<D>::F + i) * cap + p]);
+  const Mat<T, D> F_new = matmul(f_inc, FnT);
+  double* out = A + static_cast<int64_t>(p) * DD * DD;
   if (!(value_of(det(F_new)) > 0.0)) {
 #pragma unroll
-    for (int i = 0; i < 16; ++i) out[i] = 0.0;
+    for (int i = 0; i < DD * DD; ++i) out[i] = 0.0;
     return;
   }
-  const StressOut<T> su = neo_hookean_update<T, 2>(F_new, T(pc.lam), T(pc.mu));
+  const StressOut<T> su = neo_hookean_update<T, D>(F_new, T(pc.lam), T(pc.mu));
   const double V0 = pd[PF<D>::V0 * cap + p];
 #pragma unroll
-  for (int c = 0; c < 2; ++c)
+  for (int c = 0; c < D; ++c)
 #pragma unroll
-    for (int b = 0; b < 2; ++b)
+    for (int b = 0; b < D; ++b)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) out[(c * 2 + b) * 4 + j] = V0 * su.sigma(c, b).d[j];
+      for (int j = 0; j < DD; ++j) out[(c * D + b) * DD + j] = V0 * su.sigma(c, b).d[j];
 }
 
-// colour-batched bin-centric assembly of the 3x3 u-p blocks:
+// colour-batched bin-centric assembly of the F x F u-p blocks:
 //   uu(c,d) = sum_f H_k[c][d][f] g^l_f,   up(c) = -V0 g^k_c w^l,
 //   pu(d)   = V0 w^k g^l_d,               pp    = V0 dt mob g^k . g^l
-template <int SHAPE, int PPL, int WARPS>
+// one writer per block per colour launch: fire-and-forget RED adds
+template <int D, int SHAPE, int PPL, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32) k_up_assemble_bins(
     GridC g, const double* __restrict__ pd, int64_t cap, const double* __restrict__ xs,
     const int* __restrict__ bin_start, const uint8_t* __restrict__ bflag, const double* __restrict__ A,
     const int* __restrict__ act_idx, const unsigned* __restrict__ row_mask, const int* __restrict__ row_nzb,
-    double* __restrict__ vals, int64_t row_len, double dtmob, int c0, int c1, int nb0, int nb1) {
-  constexpr int D = 2, F = 3, DD = 4, D3 = 8, NK = 9;
-  __shared__ double W1s[WARPS][2][3], DW1s[WARPS][2][3];
-  __shared__ double Gs[WARPS][NK][3];
+    double* __restrict__ vals, int64_t row_len, double dtmob, int c0, int c1, int c2, int nb0, int nb1, int nb2) {
+  constexpr int F = UpQ<D>::F, DD = UpQ<D>::DD, D3 = DD * D, NK = ipow_c(3, D), FF = F * F;
+  __shared__ double W1s[WARPS][3][3], DW1s[WARPS][3][3];
+  __shared__ double Gs[WARPS][NK][4];
   __shared__ double Hs[WARPS][NK * D3];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nbins = nb0 * nb1;
+  const int nbins = nb0 * nb1 * nb2;
+  const int col[3] = {c0, c1, c2};
+  const int nbv[3] = {nb0, nb1, nb2};
   for (int bi = blockIdx.x * WARPS + warp; bi < nbins; bi += gridDim.x * WARPS) {
-    const int bidx[2] = {3 * (bi / nb1) + c0, 3 * (bi % nb1) + c1};
-    const int b = bidx[0] * g.stride[0] + bidx[1];
+    int bidx[3] = {0, 0, 0}, rr = bi, b = 0;
+#pragma unroll
+    for (int a = D - 1; a >= 0; --a) {
+      bidx[a] = 3 * (rr % nbv[a]) + col[a];
+      rr /= nbv[a];
+      b += bidx[a] * g.stride[a];
+    }
     const int fl = bflag[b];
     if (!(fl & 0x80)) continue;
-    const int cn[2] = {2 + (fl & 1), 2 + ((fl >> 1) & 1)};
-    const int nk = cn[0] * cn[1];
+    int cn[3] = {1, 1, 1};
+#pragma unroll
+    for (int a = 0; a < D; ++a) cn[a] = 2 + ((fl >> a) & 1);
+    const int nk = cn[0] * cn[1] * cn[2];
     const int npairs = nk * nk;
     const int p0 = bin_start[b], p1 = bin_start[b + 1];
     for (int q0 = 0; q0 < npairs; q0 += 32 * PPL) {
-      double acc[PPL][9];
+      double acc[PPL][FF];
 #pragma unroll
       for (int t = 0; t < PPL; ++t)
 #pragma unroll
-        for (int e = 0; e < 9; ++e) acc[t][e] = 0.0;
+        for (int e = 0; e < FF; ++e) acc[t][e] = 0.0;
       for (int p = p0; p < p1; ++p) {
-        if (lane < 6) {
+        if (lane < 3 * D) {
           const int a = lane / 3, i = lane % 3;
           double w = 0.0, dw = 0.0;
           if (i < cn[a]) {
@@ -2682,21 +2793,32 @@ __global__ void __launch_bounds__(WARPS * 32) k_up_assemble_bins(
         }
         __syncwarp();
         if (lane < nk) {
-          const int li0 = lane / cn[1], li1 = lane % cn[1];
-          const double w[2] = {W1s[warp][0][li0], W1s[warp][1][li1]};
-          const double dw[2] = {DW1s[warp][0][li0], DW1s[warp][1][li1]};
+          int li[3] = {0, 0, 0}, rk = lane;
+#pragma unroll
+          for (int a = D - 1; a >= 0; --a) {
+            li[a] = rk % cn[a];
+            rk /= cn[a];
+          }
+          double w[3], dw[3];
+#pragma unroll
+          for (int a = 0; a < D; ++a) {
+            w[a] = W1s[warp][a][li[a]];
+            dw[a] = DW1s[warp][a][li[a]];
+          }
           double W, gk[3];
           tensor_weight<D>(w, dw, W, gk);
-          Gs[warp][lane][0] = gk[0];
-          Gs[warp][lane][1] = gk[1];
-          Gs[warp][lane][2] = W;
+#pragma unroll
+          for (int a = 0; a < D; ++a) Gs[warp][lane][a] = gk[a];
+          Gs[warp][lane][3] = W;
         }
         __syncwarp();
-        const double* Ap = A + static_cast<int64_t>(p) * 16;
+        const double* Ap = A + static_cast<int64_t>(p) * DD * DD;
         for (int e = lane; e < nk * D3; e += 32) {
           const int k = e / D3, cdf = e - k * D3, c = cdf / DD, df = cdf - c * DD;
-          Hs[warp][e] = Gs[warp][k][0] * __ldg(Ap + (c * 2 + 0) * DD + df) +
-                        Gs[warp][k][1] * __ldg(Ap + (c * 2 + 1) * DD + df);
+          double h = Gs[warp][k][0] * __ldg(Ap + (c * D + 0) * DD + df);
+#pragma unroll
+          for (int bb = 1; bb < D; ++bb) h += Gs[warp][k][bb] * __ldg(Ap + (c * D + bb) * DD + df);
+          Hs[warp][e] = h;
         }
         __syncwarp();
         const double V0 = pd[PF<D>::V0 * cap + p];
@@ -2706,17 +2828,30 @@ __global__ void __launch_bounds__(WARPS * 32) k_up_assemble_bins(
           if (q < npairs) {
             const int k = q / nk, l = q - k * nk;
             const double* Hk = &Hs[warp][k * D3];
-            const double gl0 = Gs[warp][l][0], gl1 = Gs[warp][l][1], wl = Gs[warp][l][2];
-            const double gk0 = Gs[warp][k][0], gk1 = Gs[warp][k][1], wk = Gs[warp][k][2];
+            double gl[3], gk[3];
 #pragma unroll
-            for (int c = 0; c < 2; ++c)
+            for (int a = 0; a < D; ++a) {
+              gl[a] = Gs[warp][l][a];
+              gk[a] = Gs[warp][k][a];
+            }
+            const double wl = Gs[warp][l][3], wk = Gs[warp][k][3];
 #pragma unroll
-              for (int d = 0; d < 2; ++d) acc[t][c * 3 + d] += Hk[(c * 2 + d) * 2] * gl0 + Hk[(c * 2 + d) * 2 + 1] * gl1;
-            acc[t][2] += -V0 * gk0 * wl;
-            acc[t][5] += -V0 * gk1 * wl;
-            acc[t][6] += V0 * wk * gl0;
-            acc[t][7] += V0 * wk * gl1;
-            acc[t][8] += V0 * dtmob * (gk0 * gl0 + gk1 * gl1);
+            for (int c = 0; c < D; ++c)
+#pragma unroll
+              for (int d = 0; d < D; ++d) {
+                double sacc = Hk[(c * D + d) * D] * gl[0];
+#pragma unroll
+                for (int f = 1; f < D; ++f) sacc += Hk[(c * D + d) * D + f] * gl[f];
+                acc[t][c * F + d] += sacc;
+              }
+#pragma unroll
+            for (int c = 0; c < D; ++c) acc[t][c * F + D] += -V0 * gk[c] * wl;
+#pragma unroll
+            for (int d = 0; d < D; ++d) acc[t][D * F + d] += V0 * wk * gl[d];
+            double gg = gk[0] * gl[0];
+#pragma unroll
+            for (int a = 1; a < D; ++a) gg += gk[a] * gl[a];
+            acc[t][D * F + D] += V0 * dtmob * gg;
           }
         }
         __syncwarp();
@@ -2726,9 +2861,19 @@ __global__ void __launch_bounds__(WARPS * 32) k_up_assemble_bins(
         const int q = q0 + lane + 32 * t;
         if (q >= npairs) continue;
         const int k = q / nk, l = q - k * nk;
-        const int lk0 = k / cn[1], lk1 = k % cn[1], ll0 = l / cn[1], ll1 = l % cn[1];
-        const int node = (bidx[0] + lk0) * g.stride[0] + bidx[1] + lk1;
-        const int sl = (ll0 - lk0 + 2) * 5 + (ll1 - lk1 + 2);
+        int lk[3] = {0, 0, 0}, ll[3] = {0, 0, 0}, rk = k, rl = l, node = 0, sl = 0;
+#pragma unroll
+        for (int a = D - 1; a >= 0; --a) {
+          lk[a] = rk % cn[a];
+          rk /= cn[a];
+          ll[a] = rl % cn[a];
+          rl /= cn[a];
+        }
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          node += (bidx[a] + lk[a]) * g.stride[a];
+          sl = sl * 5 + (ll[a] - lk[a] + 2);
+        }
         const int row = act_idx[node];
         if (row < 0) continue;
         const unsigned* m = row_mask + static_cast<int64_t>(row) * 4;
@@ -2736,47 +2881,48 @@ __global__ void __launch_bounds__(WARPS * 32) k_up_assemble_bins(
         const int cp = cpad(row_nzb[row], F);
         double* rv = vals + static_cast<int64_t>(row) * row_len + pos * F;
 #pragma unroll
-        for (int c = 0; c < 3; ++c)
+        for (int c = 0; c < F; ++c)
 #pragma unroll
-          for (int d = 0; d < 3; ++d) rv[c * cp + d] += acc[t][c * 3 + d];
+          for (int d = 0; d < F; ++d) atomicAdd(rv + c * cp + d, acc[t][c * F + d]);
       }
     }
   }
 }
 
-// commit (src/porous.cpp:139-151): F, V, sigma, accumulated vertical displacement
-template <int SHAPE>
+// commit (src/porous.cpp:139-151): F, V, sigma, accumulated vertical
+// (last-axis) displacement
+template <int D, int SHAPE>
 __global__ void k_up_commit(GridC g, double* __restrict__ pd, int64_t cap, int P, const double* __restrict__ xs,
                             const int* __restrict__ key, const int* __restrict__ sup, const double* __restrict__ x,
                             PoroC pc, double* __restrict__ uty) {
-  constexpr int D = 2;
+  constexpr int F = UpQ<D>::F, DD = UpQ<D>::DD;
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= P) return;
   int first[3], cnt[3];
   AxisW aw[3];
   particle_weights<D, SHAPE>(g, pd, cap, xs, p, key[p], sup[p], first, cnt, aw);
-  Mat<double, 2> G = Mat<double, 2>::zero();
+  Mat<double, D> G = Mat<double, D>::zero();
   double duy = 0.0;
   for_each_support<D>(g, first, cnt, aw, [&](int node, double W, const double* grad) {
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      const double uv = x[node * 3 + c];
-      if (c == 1) duy += W * uv;
+    for (int c = 0; c < D; ++c) {
+      const double uv = x[node * F + c];
+      if (c == D - 1) duy += W * uv;
 #pragma unroll
-      for (int a = 0; a < 2; ++a) G(c, a) += uv * grad[a];
+      for (int a = 0; a < D; ++a) G(c, a) += uv * grad[a];
     }
   });
-  Mat<double, 2> f_inc = G;
-  f_inc(0, 0) += 1.0;
-  f_inc(1, 1) += 1.0;
-  Mat<double, 2> Fn;
+  Mat<double, D> f_inc = G;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) Fn.e[i] = pd[(PF<D>::F + i) * cap + p];
-  const Mat<double, 2> F = matmul(f_inc, Fn);
+  for (int a = 0; a < D; ++a) f_inc(a, a) += 1.0;
+  Mat<double, D> Fn;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) pd[(PF<D>::F + i) * cap + p] = F.e[i];
-  pd[PF<D>::V * cap + p] = det(F) * pd[PF<D>::V0 * cap + p];
-  const StressOut<double> su = neo_hookean_update<double, 2>(F, pc.lam, pc.mu);
+  for (int i = 0; i < DD; ++i) Fn.e[i] = pd[(PF<D>::F + i) * cap + p];
+  const Mat<double, D> Fm = matmul(f_inc, Fn);
+#pragma unroll
+  for (int i = 0; i < DD; ++i) pd[(PF<D>::F + i) * cap + p] = Fm.e[i];
+  pd[PF<D>::V * cap + p] = det(Fm) * pd[PF<D>::V0 * cap + p];
+  const StressOut<double> su = neo_hookean_update<double, D>(Fm, pc.lam, pc.mu);
 #pragma unroll
   for (int i = 0; i < 9; ++i) pd[(PF<D>::sigma + i) * cap + p] = su.sigma.e[i];
   uty[p] += duy;

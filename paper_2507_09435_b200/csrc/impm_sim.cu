@@ -331,6 +331,7 @@ struct Sim {
       case 22: fn(IC<2>{}, IC<2>{}); break;
       case 33: fn(IC<3>{}, IC<3>{}); break;
       case 23: fn(IC<2>{}, IC<3>{}); break;
+      case 34: fn(IC<3>{}, IC<4>{}); break;
       default: throw SimError(IMPM_ERR_CONFIG, "unsupported dimension/field combination");
     }
   }
@@ -357,13 +358,14 @@ struct Sim {
     if (D < 1 || D > 3) throw SimError(IMPM_ERR_CONFIG, "grid dimension must be 1, 2 or 3");
     F = D;
     if (poro) {
-      if (D != 2) throw SimError(IMPM_ERR_CONFIG, "coupled u-p is 2D (porous.hpp:48)");
+      // the reference's CoupledSim is 2D (porous.hpp:48); D = 3 (4x4 blocks) is an extension
+      if (D != 2 && D != 3) throw SimError(IMPM_ERR_CONFIG, "coupled u-p requires a 2D or 3D grid");
       if (!(poro->k > 0.0)) throw SimError(IMPM_ERR_CONFIG, "permeability must be positive");  // porous.hpp:32-37
       if (!(poro->mu_f > 0.0)) throw SimError(IMPM_ERR_CONFIG, "fluid viscosity must be positive");
       if (!(poro->mu > 0.0) || !(poro->lambda + 2.0 * poro->mu > 0.0))
         throw SimError(IMPM_ERR_CONFIG, "solid moduli must give a positive constrained modulus");
       coupled = true;
-      F = 3;
+      F = D + 1;
       pc.lam = poro->lambda;
       pc.mu = poro->mu;
       pc.mob = poro->k / poro->mu_f;
@@ -500,7 +502,7 @@ struct Sim {
     sup.ensure(cap);
     rank.ensure(cap);
     perm.ensure(cap);
-    Pst.ensure(cap * std::max(D * D, 8));
+    Pst.ensure(cap * (D * D + 2 + D));  // single field: D*D; u-p: UpQ<D>::N
     uty.ensure(cap);
     Atan.ensure(cap * D * D * D * D);
   }
@@ -835,6 +837,9 @@ struct Sim {
         if (coupled) {
           if constexpr (DD == 2)
             k_node_mass<2, 3, SH><<<blocks_for(N), kThreads, 0, s>>>(g, pd.p, cap, xs.p, bin_start.p, sup.p, fixed.p,
+                                                                      st.p, mass.p, act_flag.p, free_flag.p);
+          else if constexpr (DD == 3)
+            k_node_mass<3, 4, SH><<<blocks_for(N), kThreads, 0, s>>>(g, pd.p, cap, xs.p, bin_start.p, sup.p, fixed.p,
                                                                       st.p, mass.p, act_flag.p, free_flag.p);
         } else {
           k_node_mass<DD, DD, SH><<<blocks_for(N), kThreads, 0, s>>>(g, pd.p, cap, xs.p, bin_start.p, sup.p, fixed.p,
@@ -1945,34 +1950,43 @@ struct Sim {
   }
 
 
-  // ----------------------------------------------- coupled u-p (2D, F=3)
+  // ------------------------------- coupled u-p (2D reference F=3; 3D extension F=4)
   PoroC poro_c() const {
     PoroC q = pc;
     q.g0 = gravity[0];
     q.g1 = gravity[1];
+    q.g2 = gravity[2];
     return q;
   }
 
   // CoupledSim::assemble<double> (porous.hpp:127-186); dt > 0 required
+  template <class Fn>
+  void dispatch_up(Fn&& fn) {  // (D, shape) of a coupled simulation
+    if (D == 2) {
+      if (shape == 2) fn(IC<2>{}, IC<2>{});
+      else fn(IC<2>{}, IC<1>{});
+    } else {
+      if (shape == 2) fn(IC<3>{}, IC<2>{});
+      else fn(IC<3>{}, IC<1>{});
+    }
+  }
   double residual_up(const double* xd, double dt, double* rd) {
     if (!(dt > 0.0)) throw SimError(IMPM_ERR_CONFIG, "coupled step requires dt > 0");
     const PoroC q = poro_c();
-    auto run = [&](auto Sc) {
-      constexpr int SH = decltype(Sc)::value;
+    dispatch_up([&](auto Dc, auto Sc) {
+      constexpr int DD = decltype(Dc)::value, SH = decltype(Sc)::value;
       if (P > 0) {
         Prof::Scope ps(&prof, kcResP);
-        k_up_particles<SH><<<blocks_for(P), kThreads, 0, s>>>(g, pd.p, cap, P, xs.p, key.p, sup.p, orig.p, xd, q,
-                                                              Pst.p, st.p); ++g_launches;
+        k_up_particles<DD, SH><<<blocks_for(P), kThreads, 0, s>>>(g, pd.p, cap, P, xs.p, key.p, sup.p, orig.p, xd, q,
+                                                                  Pst.p, st.p); ++g_launches;
         CKL();
       }
       Prof::Scope ps(&prof, kcResN);
-      k_up_nodes<SH><<<kRedBlocks, kThreads, 0, s>>>(g, pd.p, cap, xs.p, bin_start.p, sup.p, Pst.p, bext.p,
-                                                     act_flag.p, freem.p, q, dt, rd, partials.p); ++g_launches;
+      k_up_nodes<DD, SH><<<kRedBlocks, kThreads, 0, s>>>(g, pd.p, cap, xs.p, bin_start.p, sup.p, Pst.p, bext.p,
+                                                         act_flag.p, freem.p, q, dt, rd, partials.p); ++g_launches;
       k_finalize_sum<1><<<1, 1024, 0, s>>>(partials.p, kRedBlocks, &st.p->norm2); ++g_launches;
       CKL();
-    };
-    if (shape == 2) run(IC<2>{});
-    else run(IC<1>{});
+    });
     read_status();
     prof.flush();
     if (h_st->err_domain != INT_MAX)
@@ -1982,34 +1996,39 @@ struct Sim {
 
   void jacobian_up(const double* xd, double dt) {
     const PoroC q = poro_c();
-    auto run = [&](auto Sc) {
-      constexpr int SH = decltype(Sc)::value;
+    dispatch_up([&](auto Dc, auto Sc) {
+      constexpr int DD = decltype(Dc)::value, SH = decltype(Sc)::value;
       if (P > 0) {
         Prof::Scope ps(&prof, kcTangent);
-        k_up_tangent<SH><<<blocks_for(P, 128), 128, 0, s>>>(g, pd.p, cap, P, xs.p, key.p, sup.p, xd, q, Atan.p);
+        k_up_tangent<DD, SH><<<blocks_for(P, 128), 128, 0, s>>>(g, pd.p, cap, P, xs.p, key.p, sup.p, xd, q, Atan.p);
         ++g_launches;
         CKL();
       }
       if (n_act > 0) {
         Prof::Scope ps(&prof, kcAssemble);
-        k_zero_rows<<<blocks_for(static_cast<int64_t>(n_act) * 32), kThreads, 0, s>>>(n_act, 3, row_nzb.p, vals.p,
+        k_zero_rows<<<blocks_for(static_cast<int64_t>(n_act) * 32), kThreads, 0, s>>>(n_act, DD + 1, row_nzb.p, vals.p,
                                                                                     row_len); ++g_launches;
         constexpr int W = 4;
-        for (int col = 0; col < 9; ++col) {
-          const int c0 = col / 3, c1 = col % 3;
-          const int nb0 = std::max(0, (g.nodes[0] - c0 + 2) / 3), nb1 = std::max(0, (g.nodes[1] - c1 + 2) / 3);
-          if (nb0 * nb1 == 0) continue;
-          k_up_assemble_bins<SH, 3, W><<<std::min<unsigned>(blocks_for(nb0 * nb1, W), 148 * 16), W * 32, 0, s>>>(
-              g, pd.p, cap, xs.p, bin_start.p, bflag.p, Atan.p, act_idx.p, row_mask.p, row_nzb.p, vals.p, row_len,
-              dt * q.mob, c0, c1, nb0, nb1); ++g_launches;
+        const int nc = ipow_c(3, DD);
+        for (int col = 0; col < nc; ++col) {
+          int cc[3] = {0, 0, 0}, nb[3] = {1, 1, 1}, rr = col;
+          for (int a = DD - 1; a >= 0; --a) {
+            cc[a] = rr % 3;
+            rr /= 3;
+            nb[a] = std::max(0, (g.nodes[a] - cc[a] + 2) / 3);
+          }
+          const int nbins = nb[0] * nb[1] * nb[2];
+          if (nbins == 0) continue;
+          k_up_assemble_bins<DD, SH, (DD == 2 ? 3 : 2), W>
+              <<<std::min<unsigned>(blocks_for(nbins, W), 148 * 16), W * 32, 0, s>>>(
+                  g, pd.p, cap, xs.p, bin_start.p, bflag.p, Atan.p, act_idx.p, row_mask.p, row_nzb.p, vals.p, row_len,
+                  dt * q.mob, cc[0], cc[1], cc[2], nb[0], nb[1], nb[2]); ++g_launches;
         }
-        k_diag_inverse<2, 3><<<blocks_for(n_act), kThreads, 0, s>>>(n_act, act_list.p, freem.p, row_mask.p,
-                                                                    row_nzb.p, vals.p, row_len, dinv.p); ++g_launches;
+        k_diag_inverse<DD, DD + 1><<<blocks_for(n_act), kThreads, 0, s>>>(n_act, act_list.p, freem.p, row_mask.p,
+                                                                          row_nzb.p, vals.p, row_len, dinv.p); ++g_launches;
         CKL();
       }
-    };
-    if (shape == 2) run(IC<2>{});
-    else run(IC<1>{});
+    });
     matrix_valid = true;
   }
 
@@ -2060,7 +2079,7 @@ struct Sim {
       rec->diff_seconds = diff_s;
       rec->solve_seconds = solve_s;
       rec->krylov_iterations = kry;
-      rec->backward_passes = iters * F * 25;
+      rec->backward_passes = iters * F * (D == 2 ? 25 : 125);
       rec->nnz_assembled = iters * ref_nnz();
       finish_record(rec, rels);
     }
@@ -2071,16 +2090,16 @@ struct Sim {
     const PoroC q = poro_c();
     if (P > 0) {
       Prof::Scope ps(&prof, kcCommit);
-      if (shape == 2)
-        k_up_commit<2><<<blocks_for(P), kThreads, 0, s>>>(g, pd.p, cap, P, xs.p, key.p, sup.p, u.p, q, uty.p);
-      else
-        k_up_commit<1><<<blocks_for(P), kThreads, 0, s>>>(g, pd.p, cap, P, xs.p, key.p, sup.p, u.p, q, uty.p);
+      dispatch_up([&](auto Dc, auto Sc) {
+        constexpr int DD = decltype(Dc)::value, SH = decltype(Sc)::value;
+        k_up_commit<DD, SH><<<blocks_for(P), kThreads, 0, s>>>(g, pd.p, cap, P, xs.p, key.p, sup.p, u.p, q, uty.p);
+      });
       ++g_launches;
       CKL();
     }
     // p_nodes <- pressure DOFs of x (displacement components are not kept)
     CK(cudaMemsetAsync(prev.p, 0, sizeof(double) * NF(), s));
-    k_copy_field<<<blocks_for(g.N), kThreads, 0, s>>>(g.N, 3, 2, freem.p, u.p, prev.p); ++g_launches;
+    k_copy_field<<<blocks_for(g.N), kThreads, 0, s>>>(g.N, F, D, freem.p, u.p, prev.p); ++g_launches;
     CKL();
     up_time += dt;
     sync();
@@ -2477,7 +2496,7 @@ impm_status impm_coupled_nodal_pressure(impm_sim* h, double* p) {
   std::vector<double> gv(sim->NF());
   CK(cudaMemcpyAsync(gv.data(), sim->prev.p, sizeof(double) * gv.size(), cudaMemcpyDeviceToHost, sim->s));
   sim->sync();
-  for (int n = 0; n < sim->g.N; ++n) p[n] = gv[static_cast<size_t>(n) * 3 + 2];
+  for (int n = 0; n < sim->g.N; ++n) p[n] = gv[static_cast<size_t>(n) * sim->F + sim->D];
   API_END(sim)
 }
 impm_status impm_coupled_settlement(impm_sim* h, double* u_total_y, double* time) {

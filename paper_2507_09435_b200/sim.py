@@ -369,24 +369,27 @@ class PoroParams:
 
 
 class CoupledSim:
-    """impm::CoupledSim (porous.hpp:48-125): 2D small-strain u-p on reference-
-    configuration weights, fields (ux, uy, p) per node, stepped on the GPU."""
+    """impm::CoupledSim (porous.hpp:48-125): small-strain u-p on reference-
+    configuration weights, fields (u_0 .. u_{D-1}, p) per node, stepped on the
+    GPU. D = 2 is the reference; D = 3 (4x4 node blocks) is an extension
+    (parity unpinned)."""
 
     def __init__(self, grid: GridSpec, particles, poro: PoroParams, options: Optional[SolverOptions] = None,
                  device: int = 0):
-        if grid.dim != 2:
+        if grid.dim not in (2, 3):
             from .errors import ConfigError
-            raise ConfigError("coupled u-p is 2D")
+            raise ConfigError("coupled u-p requires a 2D or 3D grid")
         self.grid = grid
-        self.D = 2
+        self.D = D = grid.dim
+        self.F = D + 1
         self.poro = poro
         self.options = options or SolverOptions()
         L = _abi.lib()
         g = _abi.Grid()
-        g.dim = 2
+        g.dim = D
         for a in range(3):
-            g.nodes[a] = int(grid.nodes[a]) if a < 2 else 1
-            g.origin[a] = float(grid.origin[a]) if a < 2 else 0.0
+            g.nodes[a] = int(grid.nodes[a]) if a < D else 1
+            g.origin[a] = float(grid.origin[a]) if a < D else 0.0
         g.h = float(grid.h)
         pc = _abi.Poro(poro.lambda_, poro.mu, poro.k, poro.mu_f, poro.rho_f)
         o = self.options.to_c()
@@ -398,16 +401,16 @@ class CoupledSim:
         self._h._L = L
         self._h.h = h
         self._N = grid.node_count()
-        self.fixed_u = np.zeros(self._N * 2, dtype=np.uint8)  # [node*2 + comp]
+        self.fixed_u = np.zeros(self._N * D, dtype=np.uint8)  # [node*D + comp]
         self.fixed_p = np.zeros(self._N, dtype=np.uint8)
-        self._gravity = np.zeros(2)
+        self._gravity = np.zeros(D)
         data = np.ascontiguousarray(particles.data if isinstance(particles, ParticleArray) else particles,
                                     dtype=np.float64)
         self._h.call("impm_sim_set_particles", _abi.ptr(data), data.shape[0], data.strides[0])
         self._n_particles = data.shape[0]
-        self._X1 = data[:, 1].copy()  # reference y (Particle<2>::X[1])
+        self._X1 = data[:, D - 1].copy()  # reference vertical coordinate (Particle<D>::X[D-1])
         self._initialized = False
-        self.gravity = np.zeros(2)
+        self.gravity = np.zeros(D)
 
     @property
     def gravity(self):
@@ -415,23 +418,23 @@ class CoupledSim:
 
     @gravity.setter
     def gravity(self, gv):
-        self._gravity = np.asarray(gv, dtype=np.float64).reshape(2).copy()
+        self._gravity = np.asarray(gv, dtype=np.float64).reshape(self.D).copy()
         g3 = np.zeros(3)
-        g3[:2] = self._gravity
+        g3[: self.D] = self._gravity
         self._h.call("impm_sim_set_gravity", _abi.ptr(g3))
 
     @property
     def particles(self) -> ParticleArray:
-        out = np.zeros((self._n_particles, particle_doubles(2)))
+        out = np.zeros((self._n_particles, particle_doubles(self.D)))
         self._h.call("impm_sim_get_particles", _abi.ptr(out), self._n_particles, out.strides[0])
-        return ParticleArray(out, 2)
+        return ParticleArray(out, self.D)
 
     def fix_displacement(self, predicate, component=-1):
         pos = self.grid.node_positions()
         mask = np.asarray(predicate(pos), dtype=bool).reshape(-1)
-        for c in range(2):
+        for c in range(self.D):
             if component < 0 or component == c:
-                self.fixed_u[np.nonzero(mask)[0] * 2 + c] = 1
+                self.fixed_u[np.nonzero(mask)[0] * self.D + c] = 1
 
     def fix_pressure(self, predicate):
         pos = self.grid.node_positions()
@@ -440,10 +443,11 @@ class CoupledSim:
 
     def initialize(self):
         """src/porous.cpp:25-72"""
-        fixed3 = np.zeros(self._N * 3, dtype=np.uint8)
-        fixed3[0::3] = self.fixed_u[0::2]
-        fixed3[1::3] = self.fixed_u[1::2]
-        fixed3[2::3] = self.fixed_p
+        D, F = self.D, self.F
+        fixed3 = np.zeros(self._N * F, dtype=np.uint8)
+        for c in range(D):
+            fixed3[c::F] = self.fixed_u[c::D]
+        fixed3[D::F] = self.fixed_p
         self._h.call("impm_sim_set_fixed", _abi.ptr(fixed3))
         self._h.call("impm_coupled_initialize")
         self._initialized = True
@@ -455,11 +459,11 @@ class CoupledSim:
 
     def dofs(self) -> DofMap:
         n = self.n_dofs()
-        dof_of = np.zeros(self._N * 3, dtype=np.int32)
+        dof_of = np.zeros(self._N * self.F, dtype=np.int32)
         node_of = np.zeros(max(n, 1), dtype=np.int32)
         field_of = np.zeros(max(n, 1), dtype=np.int32)
         self._h.call("impm_sim_dof_map", _abi.ptr(dof_of), _abi.ptr(node_of), _abi.ptr(field_of))
-        return DofMap(3, n, dof_of, node_of[:n], field_of[:n])
+        return DofMap(self.F, n, dof_of, node_of[:n], field_of[:n])
 
     def residual(self, x, dt):
         x = _abi.f64(x)
@@ -498,19 +502,23 @@ class CoupledSim:
         return float(-uty[top].sum() / top.sum()) if top.any() else 0.0
 
     def pressure_profile(self, x_index, surface_y):
-        """nodal pressures on one grid column by depth (src/porous.cpp:185-199)"""
+        """nodal pressures on one vertical grid column by depth (src/porous.cpp:185-199);
+        x_index: the column's index along axis 0 (2D) or its (i, j) pair (3D)"""
         mass = np.zeros(self._N)
         self._h.call("impm_sim_node_mass", _abi.ptr(mass))
         pm = self.particles.m[:, 0].max() if self._n_particles else 0.0
         active = mass > 1e-12 * pm
         pos = self.grid.node_positions()
         p = self.nodal_pressure()
-        ny = int(self.grid.nodes[1])
+        D = self.D
+        nv = int(self.grid.nodes[D - 1])
+        col = x_index if D == 2 else int(x_index[0]) * int(self.grid.nodes[1]) + int(x_index[1])
+        nodes = col * nv + np.arange(nv)
         out = []
-        for n in range(self._N):
-            if not active[n] or n // ny != x_index:
+        for n in nodes:
+            if not active[n]:
                 continue
-            y = pos[n, 1]
+            y = pos[n, D - 1]
             if y < -1e-9 or y > surface_y + 1e-9:
                 continue
             out.append((surface_y - y, 0.0 if self.fixed_p[n] else p[n]))

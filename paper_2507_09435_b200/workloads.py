@@ -180,21 +180,34 @@ def terzaghi2d(cells=(512, 512), ppc=2, height=10.0, t_hat=1e3, tol=1e-10):
     lambda = mu = 600 kPa, k = 1e-12 m^2, mu_f = 0.1 Pa s, drained top, base
     fixed, lateral rollers, 1 kPa surface traction) widened from one column to
     a square block. Returns a ready CoupledSim and its parameters."""
+    return terzaghi(cells, ppc, height, t_hat, tol)
+
+
+def terzaghi3d(cells=(8, 8, 64), ppc=2, height=10.0, t_hat=1e3, tol=1e-10):
+    """cfg 3, 3D variant (4x4 u-p node blocks; extension, parity unpinned):
+    the same column with rollers on all four lateral faces."""
+    return terzaghi(cells, ppc, height, t_hat, tol)
+
+
+def terzaghi(cells, ppc=2, height=10.0, t_hat=1e3, tol=1e-10):
     from .sim import CoupledSim, PoroParams
 
-    nx, ny = cells
-    h = height / ny
-    grid = GridSpec(2, (-h, -h), h, (nx + 3, ny + 3))
-    parts = seed_box(grid, (0.0, 0.0), (nx * h, height), ppc, 2000.0)
-    pa = ParticleArray(parts, 2)
-    top = pa.X[:, 1] >= pa.X[:, 1].max() - 1e-9
-    pa.traction_force[top, 1] = -t_hat * (nx * h) / top.sum()
+    D = len(cells)
+    h = height / cells[-1]
+    grid = GridSpec(D, (-h,) * D, h, tuple(c + 3 for c in cells))
+    ext = tuple(c * h for c in cells[:-1]) + (height,)
+    parts = seed_box(grid, (0.0,) * D, ext, ppc, 2000.0)
+    pa = ParticleArray(parts, D)
+    top = pa.X[:, D - 1] >= pa.X[:, D - 1].max() - 1e-9
+    area = float(np.prod(ext[:-1]))
+    pa.traction_force[top, D - 1] = -t_hat * area / top.sum()
     pp = PoroParams(600e3, 600e3, 1e-12, 0.1, 1000.0)
     sim = CoupledSim(grid, parts, pp, SolverOptions(tol=tol))
-    width = nx * h
-    sim.fix_displacement(lambda x: (x[:, 0] <= 1e-12) | (x[:, 0] >= width - 1e-9), 0)
-    sim.fix_displacement(lambda x: x[:, 1] <= 1e-12)
-    sim.fix_pressure(lambda x: x[:, 1] >= height - 1e-9)
+    for a in range(D - 1):
+        w = ext[a]
+        sim.fix_displacement(lambda x, a=a, w=w: (x[:, a] <= 1e-12) | (x[:, a] >= w - 1e-9), a)
+    sim.fix_displacement(lambda x: x[:, D - 1] <= 1e-12)
+    sim.fix_pressure(lambda x: x[:, D - 1] >= height - 1e-9)
     sim.initialize()
     return sim, {"height": height, "t_hat": t_hat, "c_v": 1e-12 * (600e3 + 2 * 600e3) / 0.1, "h": h,
                  "particles": parts.shape[0]}

@@ -89,3 +89,45 @@ def test_cfg3_terzaghi_full_size_matches_series_solution():
         num += (p - pa) ** 2
         den += pa * pa
     assert np.sqrt(num / den) <= 0.02
+
+
+def test_3d_up_terzaghi_column_matches_series_solution():
+    """3D u-p (4x4 node blocks; extension, parity unpinned): a 3D column with
+    rollers on the four lateral faces consolidates like the 1D series solution
+    (the reference's acceptance bound L2 <= 0.02), and the 2-Newton-iteration
+    behaviour of the 2D column is kept."""
+    from paper_2507_09435_b200 import workloads
+    from paper_2507_09435_b200.scenarios import terzaghi_pressure_ratio
+
+    sim, prm = workloads.terzaghi3d(cells=(4, 4, 64))
+    H, cv, t_hat = prm["height"], prm["c_v"], prm["t_hat"]
+    Tv, n = 0.05, 10
+    dt = Tv * H * H / cv / n
+    for _ in range(n):
+        rec = sim.step(dt)
+        assert rec.iterations <= 3
+    prof = sim.pressure_profile((2, 2), H)
+    num = den = 0.0
+    for depth, p in prof:
+        pa = t_hat * terzaghi_pressure_ratio(depth / H, Tv)
+        num += (p - pa) ** 2
+        den += pa * pa
+    assert np.sqrt(num / den) <= 0.02
+    assert sim.dofs().n_fields == 4
+
+
+def test_3d_up_jacobian_matches_finite_differences():
+    import scipy.sparse as sp
+    from paper_2507_09435_b200 import workloads
+
+    sim, prm = workloads.terzaghi3d(cells=(3, 3, 8))
+    dt = 1e4
+    sim.step(dt)
+    n = sim.n_dofs()
+    x = 1e-6 * np.random.default_rng(4).standard_normal(n)
+    rp, cols, vals = sim.jacobian_csr(x, dt)
+    J = sp.csr_matrix((vals, cols, rp), shape=(n, n))
+    v = np.random.default_rng(5).standard_normal(n)
+    eps = 1e-7
+    fd = (sim.residual(x + eps * v, dt) - sim.residual(x - eps * v, dt)) / (2 * eps)
+    assert np.linalg.norm(J @ v - fd) <= 1e-6 * np.linalg.norm(J @ v)
