@@ -1597,7 +1597,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
                                                      double* __restrict__ partials, const int* __restrict__ done,
                                                      const double* __restrict__ b = nullptr,
                                                      const double* __restrict__ dinv = nullptr, double omega = 0.0,
-                                                     int rows_per_warp = 16) {
+                                                     int rows_per_warp = 16,
+                                                     const float* __restrict__ x4 = nullptr,
+                                                     float* __restrict__ y4 = nullptr) {
   constexpr int S = ipow_c(5, D);
   constexpr int FF = F * F;
   constexpr int XS = chunk_len<VT>(S, F);
@@ -1669,10 +1671,29 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
       }
       // 2. stage the x records of the stored neighbours
       const uint8_t* rsl = row_slots + static_cast<int64_t>(row) * S;
-      for (int pos = lane; pos < nzb; pos += 32) {
-        const int64_t nb = static_cast<int64_t>(k + offt[rsl[pos]]) * F;
+      if constexpr (sizeof(VT) == 4 && F <= 4) {
+        if (x4 != nullptr) {
+          // fp32 twin of x, one 16-byte record per node: one load per neighbour
+          for (int pos = lane; pos < nzb; pos += 32) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(x4) + (k + offt[rsl[pos]]));
+            xs[pos * F + 0] = v.x;
+            if (F > 1) xs[pos * F + 1] = v.y;
+            if (F > 2) xs[pos * F + 2] = v.z;
+            if (F > 3) xs[pos * F + 3] = v.w;
+          }
+        } else {
+          for (int pos = lane; pos < nzb; pos += 32) {
+            const int64_t nb = static_cast<int64_t>(k + offt[rsl[pos]]) * F;
 #pragma unroll
-        for (int d = 0; d < F; ++d) xs[pos * F + d] = static_cast<VT>(__ldg(x + nb + d));
+            for (int d = 0; d < F; ++d) xs[pos * F + d] = static_cast<VT>(__ldg(x + nb + d));
+          }
+        }
+      } else {
+        for (int pos = lane; pos < nzb; pos += 32) {
+          const int64_t nb = static_cast<int64_t>(k + offt[rsl[pos]]) * F;
+#pragma unroll
+          for (int d = 0; d < F; ++d) xs[pos * F + d] = static_cast<VT>(__ldg(x + nb + d));
+        }
       }
       if (lane < cp - nzb * F) xs[nzb * F + lane] = VT(0);
       __syncwarp();
@@ -1728,7 +1749,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
           double sacc = 0.0;
 #pragma unroll
           for (int d = 0; d < F; ++d) sacc += di[d] * rr[d];
-          y[base + lane] = fm ? e1 + omega * sacc : 0.0;
+          const double yv = fm ? e1 + omega * sacc : 0.0;
+          y[base + lane] = yv;
+          if (y4) y4[static_cast<int64_t>(k) * 4 + lane] = static_cast<float>(yv);
         }
       }
       __syncwarp();
@@ -2360,7 +2383,8 @@ __global__ void k_restrict(GridC gf, GridC gc, const int* __restrict__ done, con
 // x_f += P x_c (masked to fine free components)
 template <int D, int F>
 __global__ void k_prolong_add(GridC gf, GridC gc, const int* __restrict__ done, const double* __restrict__ xc,
-                              const uint8_t* __restrict__ f_freem, double* __restrict__ xf) {
+                              const uint8_t* __restrict__ f_freem, double* __restrict__ xf,
+                              float* __restrict__ xf4 = nullptr) {
   if (done && *done) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= gf.N) return;
@@ -2393,7 +2417,11 @@ __global__ void k_prolong_add(GridC gf, GridC gc, const int* __restrict__ done, 
   }
 #pragma unroll
   for (int c = 0; c < F; ++c)
-    if (f_freem[static_cast<int64_t>(i) * F + c]) xf[static_cast<int64_t>(i) * F + c] += acc[c];
+    if (f_freem[static_cast<int64_t>(i) * F + c]) {
+      const double v = xf[static_cast<int64_t>(i) * F + c] + acc[c];
+      xf[static_cast<int64_t>(i) * F + c] = v;
+      if (F <= 4 && xf4) xf4[static_cast<int64_t>(i) * 4 + c] = static_cast<float>(v);
+    }
 }
 
 __global__ void k_fill_free(int64_t n, const uint8_t* __restrict__ freem, double* __restrict__ v) {
@@ -2416,16 +2444,19 @@ __global__ void k_power_step(int64_t n, const double* __restrict__ sums, const d
 template <int F>
 __global__ void k_jacobi0(int n_act, const int* __restrict__ done, const int* __restrict__ act_list,
                           const double* __restrict__ dinv, const uint8_t* __restrict__ freem, double omega,
-                          const double* __restrict__ b, double* __restrict__ x) {
+                          const double* __restrict__ b, double* __restrict__ x, float* __restrict__ x4 = nullptr) {
   if (done && *done) return;
   for (int row = blockIdx.x * blockDim.x + threadIdx.x; row < n_act; row += gridDim.x * blockDim.x) {
-    const int64_t base = static_cast<int64_t>(act_list[row]) * F;
+    const int64_t node = act_list[row];
+    const int64_t base = node * F;
 #pragma unroll
     for (int c = 0; c < F; ++c) {
       double s = 0.0;
 #pragma unroll
       for (int d = 0; d < F; ++d) s += dinv[static_cast<int64_t>(row) * F * F + c * F + d] * b[base + d];
-      x[base + c] = freem[base + c] ? omega * s : 0.0;
+      const double v = freem[base + c] ? omega * s : 0.0;
+      x[base + c] = v;
+      if (F <= 4 && x4) x4[node * 4 + c] = static_cast<float>(v);
     }
   }
 }

@@ -149,6 +149,7 @@ struct MgLevel {
   DBuf<double> vals_b, dinv_b;
   DBuf<float> vals32_b;          // fp32 copy for the smoother / residual SpMVs
   DBuf<double> xa, xb, r, bvec;  // level vectors (grid layout)
+  DBuf<float> x4a, x4b;          // fp32 twins of xa / xb, 4 floats per node (fp32 SpMV gathers)
   // views
   const int* act_idx = nullptr;
   const int* act_list = nullptr;
@@ -161,6 +162,7 @@ struct MgLevel {
   const double* dinv = nullptr;
   double* x = nullptr;  // current iterate (ping-pong between xa / xb)
   double* t = nullptr;
+  float* twin(const double* v) { return v == xa.p ? x4a.p : (v == xb.p ? x4b.p : nullptr); }
   double omega = 0.5;
 };
 
@@ -242,6 +244,8 @@ struct Sim {
   // 3D tangent: one dual direction per pass (160 registers, 9 passes) beats
   // three per pass (255 registers, 12% occupancy): 13.7 -> 10.3 ms per step
   bool tangent_k1 = true;
+  // fp32 twins of the V-cycle iterates feed the fp32 level SpMV gathers
+  bool mg_x4 = !(std::getenv("IMPM_MG_X4") && std::atoi(std::getenv("IMPM_MG_X4")) == 0);
   bool krylov_debug = std::getenv("IMPM_DEBUG_KRYLOV") != nullptr;
   bool res_staged = !(std::getenv("IMPM_RES_UNSTAGED") && std::atoi(std::getenv("IMPM_RES_UNSTAGED")) != 0);
 
@@ -1209,7 +1213,9 @@ struct Sim {
     if (mg_f32)
       k_spmv<DD, FE, W, MODE, float, 0><<<grid, W * 32, 0, s>>>(L.g, L.act_list, L.n_act, L.vals32, L.row_len32,
                                                                    L.row_slots, L.row_nzb, x, L.freem, y, dotv, parts,
-                                                                   dflag.p, b, L.dinv, omega, rpw);
+                                                                   dflag.p, b, L.dinv, omega, rpw,
+                                                                   mg_x4 ? L.twin(x) : nullptr,
+                                                                   mg_x4 && MODE == kSpmvJacobi ? L.twin(y) : nullptr);
     else
       k_spmv<DD, FE, W, MODE, double, 0><<<grid, W * 32, 0, s>>>(L.g, L.act_list, L.n_act, L.vals, L.row_len, L.row_slots,
                                                             L.row_nzb, x, L.freem, y, dotv, parts, dflag.p, b, L.dinv,
@@ -1351,6 +1357,13 @@ struct Sim {
       L.r.ensure(n);
       L.bvec.ensure(n);
       for (auto* v : {&L.xa, &L.xb, &L.r, &L.bvec}) CK(cudaMemsetAsync(v->p, 0, sizeof(double) * n, s));
+      if (FE <= 4) {
+        const int64_t n4 = static_cast<int64_t>(L.g.N) * 4;
+        L.x4a.ensure(n4);
+        L.x4b.ensure(n4);
+        CK(cudaMemsetAsync(L.x4a.p, 0, sizeof(float) * n4, s));
+        CK(cudaMemsetAsync(L.x4b.p, 0, sizeof(float) * n4, s));
+      }
       L.x = L.xa.p;
       L.t = L.xb.p;
     }
@@ -1506,7 +1519,8 @@ struct Sim {
     {
       Prof::Scope ps(&prof, lcls);
       // pre-smoothing from x = 0
-      k_jacobi0<FE><<<kRedBlocks, kThreads, 0, s>>>(L.n_act, dflag.p, L.act_list, L.dinv, L.freem, L.omega, b, L.x);
+      k_jacobi0<FE><<<kRedBlocks, kThreads, 0, s>>>(L.n_act, dflag.p, L.act_list, L.dinv, L.freem, L.omega, b, L.x,
+                                                    mg_x4 ? L.twin(L.x) : nullptr);
       ++g_launches;
       CKL();
       for (int i = 1; i < nu; ++i) {
@@ -1520,7 +1534,8 @@ struct Sim {
     }
     vcycle<DD, FE>(l + 1, C.bvec.p);
     Prof::Scope ps(&prof, lcls);
-    k_prolong_add<DD, FE><<<blocks_for(L.g.N), kThreads, 0, s>>>(L.g, C.g, dflag.p, C.x, L.freem, L.x);
+    k_prolong_add<DD, FE><<<blocks_for(L.g.N), kThreads, 0, s>>>(L.g, C.g, dflag.p, C.x, L.freem, L.x,
+                                                                  mg_x4 ? L.twin(L.x) : nullptr);
     ++g_launches;
     CKL();
     for (int i = 0; i < nu; ++i) {
