@@ -1587,7 +1587,7 @@ __host__ __device__ constexpr int64_t row_len_of(int S, int F) {
 // VT = double: the Jacobian itself; VT = float: the preconditioner's copy of
 // a level matrix (values rounded once, vectors and sums stay fp64)
 // RPW: rows per warp and chunk (0: the runtime rows_per_warp argument)
-template <int D, int F, int WARPS, int MODE = kSpmvY, class VT = double, int RPW = 16>
+template <int D, int F, int WARPS, int MODE = kSpmvY, class VT = double, int RPW = 16, bool HALF = false>
 __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC g, const int* __restrict__ act_list, int n_act,
                                                      const VT* __restrict__ vals, int64_t row_len,
                                                      const uint8_t* __restrict__ row_slots,
@@ -1610,10 +1610,15 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
   // its Dinv row and rhs in registers too: smaller head under the 64-reg cap)
   // fp32 rows carry half the bytes (~5 float4 per lane at 73 blocks/row)
   constexpr int NB = sizeof(VT) == 8 ? (MODE == kSpmvJacobi ? 4 : 6) : (MODE == kSpmvJacobi ? 4 : 6);
+  // lanes per row: fp32 rows carry half the bytes, so on big levels (HALF) a
+  // half-warp streams one row and each warp keeps two rows (two latency
+  // chains) in flight
+  constexpr int HW = (sizeof(VT) == 4 && HALF) ? 16 : 32;
+  constexpr int RW = 32 / HW;  // rows per warp in flight
   __shared__ int offt[S];
   // x neighbourhood staged in the matrix precision (fp32 copies: products in
   // fp32, each 4-term partial added to the fp64 row sum)
-  __shared__ __align__(16) VT xs_all[WARPS][XS];
+  __shared__ __align__(16) VT xs_all[WARPS * RW][XS];
   for (int sl = threadIdx.x; sl < S; sl += blockDim.x) {
     int rs = sl, off = 0;
 #pragma unroll
@@ -1626,17 +1631,20 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
   __syncthreads();
   double part[1] = {0.0};
   if (done == nullptr || *done == 0) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    VT* xs = xs_all[warp];
+    const int warp = threadIdx.x >> 5, wl = threadIdx.x & 31;
+    const int lane = wl % HW, sub = wl / HW;  // lane within the row group, row slot in the warp
+    VT* xs = xs_all[warp * RW + sub];
     // contiguous row chunks per CTA: consecutive rows share 4/5 of their x
     // neighbourhood, so the x gathers of a chunk hit in this SM's L1 (small
     // coarse levels use short chunks so that every warp gets a row)
     const int CH = (RPW > 0 ? RPW : rows_per_warp) * WARPS;
     const int nchunks = (n_act + CH - 1) / CH;
     for (int ci = blockIdx.x; ci < nchunks; ci += gridDim.x)
-    for (int row = ci * CH + warp; row < min(n_act, (ci + 1) * CH); row += WARPS) {
-      const int k = act_list[row];
-      const int nzb = row_nzb[row];
+    for (int row0 = ci * CH + warp * RW; row0 < min(n_act, (ci + 1) * CH); row0 += WARPS * RW) {
+      const int row = row0 + sub;
+      const bool live = row < min(n_act, (ci + 1) * CH);  // the last pair may be half empty
+      const int k = live ? act_list[row] : 0;
+      const int nzb = live ? row_nzb[row] : 0;
       const int cp = chunk_len<VT>(nzb, F);
       const int h = cp / VW, tot2 = F * h;
       const int64_t base = static_cast<int64_t>(k) * F;
@@ -1647,7 +1655,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
       double di[F];
 #pragma unroll
       for (int d = 0; d < F; ++d) di[d] = 0.0;
-      if (lane < F) {
+      if (live && lane < F) {
         fm = freem[base + lane] != 0;
         if constexpr (MODE == kSpmvY) {
           if (dotv) e0 = dotv[base + lane];
@@ -1666,7 +1674,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
       V16 buf[NB];
 #pragma unroll
       for (int t = 0; t < NB; ++t) {
-        const int j2 = lane + 32 * t;
+        const int j2 = lane + HW * t;
         buf[t] = j2 < tot2 ? __ldcs(rv + j2) : V16{};  // streamed once: evict-first
       }
       // 2. stage the x records of the stored neighbours
@@ -1674,7 +1682,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
       if constexpr (sizeof(VT) == 4 && F <= 4) {
         if (x4 != nullptr) {
           // fp32 twin of x, one 16-byte record per node: one load per neighbour
-          for (int pos = lane; pos < nzb; pos += 32) {
+          for (int pos = lane; pos < nzb; pos += HW) {
             const float4 v = __ldg(reinterpret_cast<const float4*>(x4) + (k + offt[rsl[pos]]));
             xs[pos * F + 0] = v.x;
             if (F > 1) xs[pos * F + 1] = v.y;
@@ -1682,20 +1690,20 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
             if (F > 3) xs[pos * F + 3] = v.w;
           }
         } else {
-          for (int pos = lane; pos < nzb; pos += 32) {
+          for (int pos = lane; pos < nzb; pos += HW) {
             const int64_t nb = static_cast<int64_t>(k + offt[rsl[pos]]) * F;
 #pragma unroll
             for (int d = 0; d < F; ++d) xs[pos * F + d] = static_cast<VT>(__ldg(x + nb + d));
           }
         }
       } else {
-        for (int pos = lane; pos < nzb; pos += 32) {
+        for (int pos = lane; pos < nzb; pos += HW) {
           const int64_t nb = static_cast<int64_t>(k + offt[rsl[pos]]) * F;
 #pragma unroll
           for (int d = 0; d < F; ++d) xs[pos * F + d] = static_cast<VT>(__ldg(x + nb + d));
         }
       }
-      if (lane < cp - nzb * F) xs[nzb * F + lane] = VT(0);
+      for (int e = lane; e < cp - nzb * F; e += HW) xs[nzb * F + e] = VT(0);
       __syncwarp();
       // 3. component-major dot products (buffered head, streamed tail)
       double acc[4] = {0.0, 0.0, 0.0, 0.0};
@@ -1719,33 +1727,34 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
       };
 #pragma unroll
       for (int t = 0; t < NB; ++t) {
-        const int j2 = lane + 32 * t;
+        const int j2 = lane + HW * t;
         if (j2 < tot2) consume(j2, buf[t]);
       }
 #pragma unroll TAIL_UNROLL
-      for (int j2 = lane + 32 * NB; j2 < tot2; j2 += 32) consume(j2, __ldcs(rv + j2));
-      // butterfly: every lane holds the row sums; lane c < F finishes component c
+      for (int j2 = lane + HW * NB; j2 < tot2; j2 += HW) consume(j2, __ldcs(rv + j2));
+      // butterfly within the row group: every lane holds the row sums; lane
+      // c < F finishes component c
 #pragma unroll
       for (int c = 0; c < F; ++c)
-        for (int o = 16; o > 0; o >>= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
+        for (int o = HW / 2; o > 0; o >>= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
       double mine = acc[0];
       if (F > 1 && lane == 1) mine = acc[1];
       if (F > 2 && lane == 2) mine = acc[2];
       if (F > 3 && lane == 3) mine = acc[3];
       if constexpr (MODE == kSpmvY) {
-        if (lane < F) {
+        if (live && lane < F) {
           const double v = fm ? mine : 0.0;
           y[base + lane] = v;
           if (dotv) part[0] += v * e0;
         }
       } else if constexpr (MODE == kSpmvResid) {
-        if (lane < F) y[base + lane] = fm ? e0 - mine : 0.0;
+        if (live && lane < F) y[base + lane] = fm ? e0 - mine : 0.0;
       } else {
         const double rown = (lane < F && fm) ? e0 - mine : 0.0;
         double rr[F];
 #pragma unroll
-        for (int d = 0; d < F; ++d) rr[d] = __shfl_sync(0xffffffffu, rown, d);
-        if (lane < F) {
+        for (int d = 0; d < F; ++d) rr[d] = __shfl_sync(0xffffffffu, rown, sub * HW + d);
+        if (live && lane < F) {
           double sacc = 0.0;
 #pragma unroll
           for (int d = 0; d < F; ++d) sacc += di[d] * rr[d];

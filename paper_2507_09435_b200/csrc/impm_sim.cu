@@ -1210,7 +1210,13 @@ struct Sim {
     const int rpw = std::max(1, std::min(16, (L.n_act + spmv_blocks * W - 1) / (spmv_blocks * W)));
     const unsigned grid = parts ? spmv_blocks
                                 : static_cast<unsigned>(std::max(1, std::min(spmv_blocks, (L.n_act + rpw * W - 1) / (rpw * W))));
-    if (mg_f32)
+    // big levels: half-warp rows (two fp32 rows in flight per warp); the
+    // denser, smaller coarse levels keep a full warp per row
+    if (mg_f32 && L.n_act >= 50000)
+      k_spmv<DD, FE, W, MODE, float, 0, true><<<grid, W * 32, 0, s>>>(
+          L.g, L.act_list, L.n_act, L.vals32, L.row_len32, L.row_slots, L.row_nzb, x, L.freem, y, dotv, parts, dflag.p,
+          b, L.dinv, omega, rpw, mg_x4 ? L.twin(x) : nullptr, mg_x4 && MODE == kSpmvJacobi ? L.twin(y) : nullptr);
+    else if (mg_f32)
       k_spmv<DD, FE, W, MODE, float, 0><<<grid, W * 32, 0, s>>>(L.g, L.act_list, L.n_act, L.vals32, L.row_len32,
                                                                    L.row_slots, L.row_nzb, x, L.freem, y, dotv, parts,
                                                                    dflag.p, b, L.dinv, omega, rpw,
