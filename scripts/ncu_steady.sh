@@ -24,9 +24,10 @@ cap jac  "k_spmv<${I}3, ${I}3, ${I}4, ${I}1, float>" 401
 cap asm  "k_assemble_bins_staged" 94
 cap resb "k_residual_bins" 150
 cap tan  "k_tangent" 3
-cap gap  "k_galerkin_ap" 12
+cap gap  "k_galerkin_ap" 3
 # launch list of steps 1-2 (per-launch duration + DRAM bytes)
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
   --log-file $OUT/launches_2steps.csv python scripts/profile_step.py cfg4 2 > $OUT/launches.log 2>&1
 gzip -f $OUT/launches_2steps.csv
+python scripts/ncu_traffic.py $OUT > /dev/null
 du -sh $OUT
