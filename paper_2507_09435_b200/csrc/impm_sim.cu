@@ -1017,6 +1017,7 @@ struct Sim {
                                                                                     row_len); ++g_launches;
         constexpr int W = 4;
         constexpr int PPL = DD == 3 ? 5 : (DD == 2 ? 3 : 1);
+        constexpr int asm_ppl3 = 3;  // 3D block pairs per lane (4: 78 vs 72 ms per load step)
         const int nc = ipow_c(3, DD);
         for (int col = 0; col < nc; ++col) {
           int cc[3] = {0, 0, 0}, nb[3] = {1, 1, 1}, r = col;
@@ -1033,11 +1034,11 @@ struct Sim {
           // Cam-Clay (associative, but its compaction hardening breaks major
           // symmetry of dP/dG: ~2% in tests/test_math_cpu.py terms)
           if (mat.kind != kDruckerPrager && mat.kind != kCamClay)
-            k_assemble_bins_staged<DD, SH, (DD == 3 ? 3 : PPL), WS, 4, true><<<grid, WS * 32, 0, s>>>(
+            k_assemble_bins_staged<DD, SH, (DD == 3 ? asm_ppl3 : PPL), WS, 4, true><<<grid, WS * 32, 0, s>>>(
                 g, pd.p, cap, xs.p, bin_start.p, bflag.p, Atan.p, act_idx.p, row_mask.p, row_nzb.p, vals.p, row_len,
                 cc[0], cc[1], cc[2], nb[0], nb[1], nb[2]);
           else
-            k_assemble_bins_staged<DD, SH, (DD == 3 ? 3 : PPL), WS, 4, false><<<grid, WS * 32, 0, s>>>(
+            k_assemble_bins_staged<DD, SH, (DD == 3 ? asm_ppl3 : PPL), WS, 4, false><<<grid, WS * 32, 0, s>>>(
                 g, pd.p, cap, xs.p, bin_start.p, bflag.p, Atan.p, act_idx.p, row_mask.p, row_nzb.p, vals.p, row_len,
                 cc[0], cc[1], cc[2], nb[0], nb[1], nb[2]);
           ++g_launches;
