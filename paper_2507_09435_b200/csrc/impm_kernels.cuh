@@ -13,6 +13,7 @@
 // Reductions are deterministic: per-block partials in fixed order + one
 // finalize block. No global float atomics anywhere on the path.
 #pragma once
+#include <cuda_fp16.h>
 
 #include <cuda_runtime.h>
 
@@ -1577,7 +1578,7 @@ enum SpmvMode { kSpmvY = 0, kSpmvJacobi = 1, kSpmvResid = 2 };
 // (double2 loads), fp32 rows to 4 (float4 loads); both 16-byte aligned
 template <class VT>
 __host__ __device__ constexpr int chunk_len(int nzb, int F) {
-  return sizeof(VT) == 8 ? cpad(nzb, F) : ((nzb * F + 3) & ~3);
+  return sizeof(VT) == 8 ? cpad(nzb, F) : (sizeof(VT) == 4 ? ((nzb * F + 3) & ~3) : ((nzb * F + 7) & ~7));
 }
 template <class VT>
 __host__ __device__ constexpr int64_t row_len_of(int S, int F) {
@@ -1585,7 +1586,10 @@ __host__ __device__ constexpr int64_t row_len_of(int S, int F) {
 }
 
 // VT = double: the Jacobian itself; VT = float: the preconditioner's copy of
-// a level matrix (values rounded once, vectors and sums stay fp64)
+// a level matrix (values rounded once, vectors and sums stay fp64); VT =
+// __half: the fine level's smoother copy, each row stored as fp16(a / s_row)
+// with an fp32 row scale s_row = max|a| / 1024 (rscale), products in fp32
+// against the fp32-staged x, row sums rescaled once
 // RPW: rows per warp and chunk (0: the runtime rows_per_warp argument)
 template <int D, int F, int WARPS, int MODE = kSpmvY, class VT = double, int RPW = 16, bool HALF = false>
 __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC g, const int* __restrict__ act_list, int n_act,
@@ -1599,13 +1603,16 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
                                                      const double* __restrict__ dinv = nullptr, double omega = 0.0,
                                                      int rows_per_warp = 16,
                                                      const float* __restrict__ x4 = nullptr,
-                                                     float* __restrict__ y4 = nullptr) {
+                                                     float* __restrict__ y4 = nullptr,
+                                                     const float* __restrict__ rscale = nullptr) {
   constexpr int S = ipow_c(5, D);
   constexpr int FF = F * F;
   constexpr int XS = chunk_len<VT>(S, F);
   constexpr int VW = 16 / sizeof(VT);  // values per 16-byte load
   constexpr int TAIL_UNROLL = sizeof(VT) == 8 ? 4 : 2;
-  using V16 = typename std::conditional<sizeof(VT) == 8, double2, float4>::type;
+  using V16 = typename std::conditional<sizeof(VT) == 8, double2,
+                                        typename std::conditional<sizeof(VT) == 4, float4, uint4>::type>::type;
+  using XT = typename std::conditional<sizeof(VT) == 8, double, float>::type;  // staged x
   // double2 per lane buffered ahead of the x gathers (the Jacobi sweep keeps
   // its Dinv row and rhs in registers too: smaller head under the 64-reg cap)
   // fp32 rows carry half the bytes (~5 float4 per lane at 73 blocks/row)
@@ -1613,12 +1620,12 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
   // lanes per row: fp32 rows carry half the bytes, so on big levels (HALF) a
   // half-warp streams one row and each warp keeps two rows (two latency
   // chains) in flight
-  constexpr int HW = (sizeof(VT) == 4 && HALF) ? 16 : 32;
+  constexpr int HW = (sizeof(VT) <= 4 && HALF) ? 16 : 32;
   constexpr int RW = 32 / HW;  // rows per warp in flight
   __shared__ int offt[S];
   // x neighbourhood staged in the matrix precision (fp32 copies: products in
   // fp32, each 4-term partial added to the fp64 row sum)
-  __shared__ __align__(16) VT xs_all[WARPS * RW][XS];
+  __shared__ __align__(16) XT xs_all[WARPS * RW][XS];
   for (int sl = threadIdx.x; sl < S; sl += blockDim.x) {
     int rs = sl, off = 0;
 #pragma unroll
@@ -1633,7 +1640,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
   if (done == nullptr || *done == 0) {
     const int warp = threadIdx.x >> 5, wl = threadIdx.x & 31;
     const int lane = wl % HW, sub = wl / HW;  // lane within the row group, row slot in the warp
-    VT* xs = xs_all[warp * RW + sub];
+    XT* xs = xs_all[warp * RW + sub];
     // contiguous row chunks per CTA: consecutive rows share 4/5 of their x
     // neighbourhood, so the x gathers of a chunk hit in this SM's L1 (small
     // coarse levels use short chunks so that every warp gets a row)
@@ -1652,6 +1659,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
       //    c's free mask, its dot / rhs operand, its own x and row c of Dinv
       bool fm = false;
       double e0 = 0.0, e1 = 0.0;
+      const float rsc = (sizeof(VT) == 2 && live) ? __ldg(rscale + row) : 1.0f;
       double di[F];
 #pragma unroll
       for (int d = 0; d < F; ++d) di[d] = 0.0;
@@ -1679,7 +1687,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
       }
       // 2. stage the x records of the stored neighbours
       const uint8_t* rsl = row_slots + static_cast<int64_t>(row) * S;
-      if constexpr (sizeof(VT) == 4 && F <= 4) {
+      if constexpr (sizeof(VT) <= 4 && F <= 4) {
         if (x4 != nullptr) {
           // fp32 twin of x, one 16-byte record per node: one load per neighbour
           for (int pos = lane; pos < nzb; pos += HW) {
@@ -1693,32 +1701,41 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
           for (int pos = lane; pos < nzb; pos += HW) {
             const int64_t nb = static_cast<int64_t>(k + offt[rsl[pos]]) * F;
 #pragma unroll
-            for (int d = 0; d < F; ++d) xs[pos * F + d] = static_cast<VT>(__ldg(x + nb + d));
+            for (int d = 0; d < F; ++d) xs[pos * F + d] = static_cast<XT>(__ldg(x + nb + d));
           }
         }
       } else {
         for (int pos = lane; pos < nzb; pos += HW) {
           const int64_t nb = static_cast<int64_t>(k + offt[rsl[pos]]) * F;
 #pragma unroll
-          for (int d = 0; d < F; ++d) xs[pos * F + d] = static_cast<VT>(__ldg(x + nb + d));
+          for (int d = 0; d < F; ++d) xs[pos * F + d] = static_cast<XT>(__ldg(x + nb + d));
         }
       }
-      for (int e = lane; e < cp - nzb * F; e += HW) xs[nzb * F + e] = VT(0);
+      for (int e = lane; e < cp - nzb * F; e += HW) xs[nzb * F + e] = XT(0);
       __syncwarp();
       // 3. component-major dot products (buffered head, streamed tail)
       double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      const V16* xv = reinterpret_cast<const V16*>(xs);
+      using XV = typename std::conditional<sizeof(VT) == 8, double2, float4>::type;
+      constexpr int XSTEP = sizeof(VT) == 2 ? 2 : 1;  // x vectors per value vector
+      const XV* xv = reinterpret_cast<const XV*>(xs);
       auto consume = [&](int j2, const V16 v) {
         const int c = F == 1   ? 0
                       : F == 2 ? (j2 >= h)
                       : F == 3 ? (j2 >= h) + (j2 >= 2 * h)
                                : (j2 >= h) + (j2 >= 2 * h) + (j2 >= 3 * h);
         double p;
-        const V16 xx = xv[j2 - c * h];
+        const XV xx = xv[XSTEP * (j2 - c * h)];
         if constexpr (sizeof(VT) == 8) {
           p = fma(v.x, xx.x, v.y * xx.y);
-        } else {
+        } else if constexpr (sizeof(VT) == 4) {
           p = static_cast<double>(fmaf(v.x, xx.x, fmaf(v.y, xx.y, fmaf(v.z, xx.z, v.w * xx.w))));
+        } else {
+          const __half2* hv = reinterpret_cast<const __half2*>(&v);
+          const float2 a0 = __half22float2(hv[0]), a1 = __half22float2(hv[1]);
+          const float2 a2 = __half22float2(hv[2]), a3 = __half22float2(hv[3]);
+          const float4 xb = xv[XSTEP * (j2 - c * h) + 1];
+          p = static_cast<double>(fmaf(a0.x, xx.x, fmaf(a0.y, xx.y, fmaf(a1.x, xx.z, a1.y * xx.w)))) +
+              static_cast<double>(fmaf(a2.x, xb.x, fmaf(a2.y, xb.y, fmaf(a3.x, xb.z, a3.y * xb.w))));
         }
         acc[0] += c == 0 ? p : 0.0;
         if (F > 1) acc[1] += c == 1 ? p : 0.0;
@@ -1741,6 +1758,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
       if (F > 1 && lane == 1) mine = acc[1];
       if (F > 2 && lane == 2) mine = acc[2];
       if (F > 3 && lane == 3) mine = acc[3];
+      if constexpr (sizeof(VT) == 2) mine *= static_cast<double>(rsc);
       if constexpr (MODE == kSpmvY) {
         if (live && lane < F) {
           const double v = fm ? mine : 0.0;
@@ -1773,7 +1791,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
 // assembly / Galerkin product: read 8 B + write 4 B per stored value)
 template <int F>
 __global__ void k_vals_to_f32(int n_act, const int* __restrict__ row_nzb, const double* __restrict__ vals,
-                              int64_t row_len, float* __restrict__ v32, int64_t row_len32) {
+                              int64_t row_len, float* __restrict__ v32, int64_t row_len32, int f16sim = 0) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   for (int row = warp; row < n_act; row += nw) {
@@ -1781,6 +1799,24 @@ __global__ void k_vals_to_f32(int n_act, const int* __restrict__ row_nzb, const 
     const int cp = chunk_len<double>(nzb, F), cq = chunk_len<float>(nzb, F);
     const double* src = vals + static_cast<int64_t>(row) * row_len;
     float* dst = v32 + static_cast<int64_t>(row) * row_len32;
+    if (f16sim) {  // A/B experiment: values rounded to fp16 with a per-row scale
+      double mx = 0.0;
+      for (int e = lane; e < F * cp; e += 32) mx = fmax(mx, fabs(src[e]));
+      for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      const float sc = mx > 0.0 ? static_cast<float>(mx / 1024.0) : 1.0f;
+      const int h2 = cq >> 1;
+      for (int e = lane; e < F * h2; e += 32) {
+        const int c = e / h2, j2 = e - c * h2;
+        float2 o = make_float2(0.0f, 0.0f);
+        if (2 * j2 < nzb * F) {
+          const double2 v = reinterpret_cast<const double2*>(src + c * cp)[j2];
+          o.x = __half2float(__float2half_rn(static_cast<float>(v.x) / sc)) * sc;
+          o.y = 2 * j2 + 1 < nzb * F ? __half2float(__float2half_rn(static_cast<float>(v.y) / sc)) * sc : 0.0f;
+        }
+        reinterpret_cast<float2*>(dst + c * cq)[j2] = o;
+      }
+      continue;
+    }
     // pairs: both chunk starts are 16-byte aligned (cp even, cq % 4 == 0)
     const int h2 = cq >> 1;  // float2 per fp32 chunk
     for (int e = lane; e < F * h2; e += 32) {
@@ -1791,6 +1827,40 @@ __global__ void k_vals_to_f32(int n_act, const int* __restrict__ row_nzb, const 
         o = make_float2(static_cast<float>(v.x), 2 * j2 + 1 < nzb * F ? static_cast<float>(v.y) : 0.0f);
       }
       reinterpret_cast<float2*>(dst + c * cq)[j2] = o;
+    }
+  }
+}
+
+// fp16 copy of the fine level matrix for the smoother: per row s = max|a| /
+// 1024 (fp32), values fp16(a / s) -- the MG V-cycle is a preconditioner,
+// CG's own SpMV stays fp64 (tests: Krylov and Newton counts unchanged)
+template <int F>
+__global__ void k_vals_to_f16(int n_act, const int* __restrict__ row_nzb, const double* __restrict__ vals,
+                              int64_t row_len, __half* __restrict__ v16, int64_t row_len16,
+                              float* __restrict__ rscale) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int row = warp; row < n_act; row += nw) {
+    const int nzb = row_nzb[row];
+    const int cp = chunk_len<double>(nzb, F), cq = chunk_len<__half>(nzb, F);
+    const double* src = vals + static_cast<int64_t>(row) * row_len;
+    __half* dst = v16 + static_cast<int64_t>(row) * row_len16;
+    double mx = 0.0;
+    for (int c = 0; c < F; ++c)
+      for (int e = lane; e < nzb * F; e += 32) mx = fmax(mx, fabs(__ldg(src + c * cp + e)));  // kept in L1 for the 2nd pass
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const float sc = mx > 0.0 ? static_cast<float>(mx / 1024.0) : 1.0f;
+    const float inv = 1.0f / sc;
+    if (lane == 0) rscale[row] = sc;
+    const int h2 = cq >> 1;  // __half2 per chunk
+    for (int e = lane; e < F * h2; e += 32) {
+      const int c = e / h2, j2 = e - c * h2;
+      float2 o = make_float2(0.0f, 0.0f);
+      if (2 * j2 < nzb * F) {
+        const double2 v = __ldcs(reinterpret_cast<const double2*>(src + c * cp) + j2);
+        o = make_float2(static_cast<float>(v.x) * inv, 2 * j2 + 1 < nzb * F ? static_cast<float>(v.y) * inv : 0.0f);
+      }
+      reinterpret_cast<__half2*>(dst + c * cq)[j2] = __float22half2_rn(o);
     }
   }
 }

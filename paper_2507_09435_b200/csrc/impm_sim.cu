@@ -3,6 +3,7 @@
 // /root/reference/proj/include/impm/mpm_solver.hpp:93-407 over device
 // kernels), the Krylov solve that replaces sparse_lu_solve
 // (src/linear_solver.cpp:11-88), and the C ABI of include/impm_gpu.h.
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -159,6 +160,9 @@ struct MgLevel {
   const double* vals = nullptr;
   const float* vals32 = nullptr;
   int64_t row_len32 = 0;
+  const __half* vals16 = nullptr;  // fine level only: fp16 smoother copy + row scales
+  const float* rscale = nullptr;
+  int64_t row_len16 = 0;
   const double* dinv = nullptr;
   double* x = nullptr;  // current iterate (ping-pong between xa / xb)
   double* t = nullptr;
@@ -229,6 +233,8 @@ struct Sim {
   // outer Krylov SpMV stays fp64, so the solve tolerance is unaffected)
   bool mg_f32 = true;
   DBuf<float> vals32;
+  DBuf<__half> vals16;  // fp16 smoother copy of the fine J (row-scaled)
+  DBuf<float> rscale16;
   // coarse levels (Galerkin products, dense coarsest inverse) are kept for
   // the later Newton iterations of a load step: the row structure is fixed
   // within a step and J moves little, while the fine level always smooths
@@ -244,6 +250,9 @@ struct Sim {
   // 3D tangent: one dual direction per pass (160 registers, 9 passes) beats
   // three per pass (255 registers, 12% occupancy): 13.7 -> 10.3 ms per step
   bool tangent_k1 = true;
+  int mg_f16sim = std::getenv("IMPM_MG_F16SIM") ? std::atoi(std::getenv("IMPM_MG_F16SIM")) : 0;  // A/B experiment
+  // fine-level smoother matrix in fp16 with fp32 row scales (IMPM_MG_F16=0: fp32)
+  bool mg_f16 = !(std::getenv("IMPM_MG_F16") && std::atoi(std::getenv("IMPM_MG_F16")) == 0);
   // fp32 twins of the V-cycle iterates feed the fp32 level SpMV gathers
   bool mg_x4 = !(std::getenv("IMPM_MG_X4") && std::atoi(std::getenv("IMPM_MG_X4")) == 0);
   bool krylov_debug = std::getenv("IMPM_DEBUG_KRYLOV") != nullptr;
@@ -1213,7 +1222,12 @@ struct Sim {
                                 : static_cast<unsigned>(std::max(1, std::min(spmv_blocks, (L.n_act + rpw * W - 1) / (rpw * W))));
     // big levels: half-warp rows (two fp32 rows in flight per warp); the
     // denser, smaller coarse levels keep a full warp per row
-    if (mg_f32 && L.n_act >= 50000)
+    if (L.vals16)
+      k_spmv<DD, FE, W, MODE, __half, 0, true><<<grid, W * 32, 0, s>>>(
+          L.g, L.act_list, L.n_act, L.vals16, L.row_len16, L.row_slots, L.row_nzb, x, L.freem, y, dotv, parts, dflag.p,
+          b, L.dinv, omega, rpw, mg_x4 ? L.twin(x) : nullptr, mg_x4 && MODE == kSpmvJacobi ? L.twin(y) : nullptr,
+          L.rscale);
+    else if (mg_f32 && L.n_act >= 50000)
       k_spmv<DD, FE, W, MODE, float, 0, true><<<grid, W * 32, 0, s>>>(
           L.g, L.act_list, L.n_act, L.vals32, L.row_len32, L.row_slots, L.row_nzb, x, L.freem, y, dotv, parts, dflag.p,
           b, L.dinv, omega, rpw, mg_x4 ? L.twin(x) : nullptr, mg_x4 && MODE == kSpmvJacobi ? L.twin(y) : nullptr);
@@ -1237,8 +1251,14 @@ struct Sim {
     constexpr int FF = FE * FE;
     if (mg_reuse && mg_setup_step == step_counter && !mg.empty() && mg[0]->n_act == n_act &&
         mg[0]->vals == vals.p) {
-      if (mg_f32 && n_act > 0) {  // fine level: fp32 copy of the current J
-        k_vals_to_f32<FE><<<kSpmvBlocks, 128, 0, s>>>(n_act, row_nzb.p, vals.p, row_len, vals32.p, mg[0]->row_len32);
+      if (mg_f16 && !coupled && n_act > 0) {  // fine level: fp16 smoother copy of the current J
+        k_vals_to_f16<FE><<<kSpmvBlocks, 128, 0, s>>>(n_act, row_nzb.p, vals.p, row_len, vals16.p, mg[0]->row_len16,
+                                                        rscale16.p);
+        ++g_launches;
+        CKL();
+      } else if (mg_f32 && n_act > 0) {  // fine level: fp32 copy of the current J
+        k_vals_to_f32<FE><<<kSpmvBlocks, 128, 0, s>>>(n_act, row_nzb.p, vals.p, row_len, vals32.p, mg[0]->row_len32,
+                                                        mg_f16sim);
         ++g_launches;
         CKL();
       }
@@ -1266,12 +1286,29 @@ struct Sim {
     L0->row_slots = row_slots.p;
     L0->vals = vals.p;
     L0->dinv = dinv.p;
-    if (mg_f32) {
+    L0->vals16 = nullptr;
+    L0->rscale = nullptr;
+    // fp16 only for the single-field solid: a u-p node row mixes the momentum
+    // and mass equations, 1e10 apart, which one row scale cannot hold
+    if (mg_f16 && !coupled) {
+      L0->row_len16 = row_len_of<__half>(S, FE);
+      vals16.ensure(std::max<int64_t>(1, static_cast<int64_t>(n_act) * L0->row_len16));
+      rscale16.ensure(std::max(1, n_act));
+      L0->vals16 = vals16.p;
+      L0->rscale = rscale16.p;
+      if (n_act > 0) {
+        k_vals_to_f16<FE><<<kSpmvBlocks, 128, 0, s>>>(n_act, row_nzb.p, vals.p, row_len, vals16.p, L0->row_len16,
+                                                        rscale16.p);
+        ++g_launches;
+        CKL();
+      }
+    } else if (mg_f32) {
       L0->row_len32 = row_len_of<float>(S, FE);
       vals32.ensure(std::max<int64_t>(1, static_cast<int64_t>(n_act) * L0->row_len32));
       L0->vals32 = vals32.p;
       if (n_act > 0) {
-        k_vals_to_f32<FE><<<kSpmvBlocks, 128, 0, s>>>(n_act, row_nzb.p, vals.p, row_len, vals32.p, L0->row_len32);
+        k_vals_to_f32<FE><<<kSpmvBlocks, 128, 0, s>>>(n_act, row_nzb.p, vals.p, row_len, vals32.p, L0->row_len32,
+                                                        mg_f16sim);
         ++g_launches;
         CKL();
       }
