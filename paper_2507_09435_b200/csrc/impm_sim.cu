@@ -149,6 +149,8 @@ struct MgLevel {
   DBuf<uint8_t> freem_b, row_slots_b;
   DBuf<double> vals_b, dinv_b;
   DBuf<float> vals32_b;          // fp32 copy for the smoother / residual SpMVs
+  DBuf<__half> vals16_b;         // fp16 row-scaled copy (big coarse levels)
+  DBuf<float> rscale_b;
   DBuf<double> xa, xb, r, bvec;  // level vectors (grid layout)
   DBuf<float> x4a, x4b;          // fp32 twins of xa / xb, 4 floats per node (fp32 SpMV gathers)
   // views
@@ -1382,7 +1384,19 @@ struct Sim {
           C->row_len32 = row_len_of<float>(S, FE);
           C->vals32_b.ensure(std::max<int64_t>(1, static_cast<int64_t>(na) * C->row_len32));
           C->vals32 = C->vals32_b.p;
-          if (na > 0) {
+          C->vals16 = nullptr;
+          C->rscale = nullptr;
+          if (mg_f16 && !coupled && na >= 50000) {  // big coarse level: fp16 smoother copy too
+            C->row_len16 = row_len_of<__half>(S, FE);
+            C->vals16_b.ensure(static_cast<int64_t>(na) * C->row_len16);
+            C->rscale_b.ensure(na);
+            C->vals16 = C->vals16_b.p;
+            C->rscale = C->rscale_b.p;
+            k_vals_to_f16<FE><<<kSpmvBlocks, 128, 0, s>>>(na, C->row_nzb_b.p, C->vals_b.p, C->row_len, C->vals16_b.p,
+                                                          C->row_len16, C->rscale_b.p);
+            ++g_launches;
+            CKL();
+          } else if (na > 0) {
             k_vals_to_f32<FE><<<kSpmvBlocks, 128, 0, s>>>(na, C->row_nzb_b.p, C->vals_b.p, C->row_len,
                                                           C->vals32_b.p, C->row_len32);
             ++g_launches;
