@@ -825,7 +825,8 @@ __global__ void k_mask_norm(int64_t n, const uint8_t* __restrict__ freem, double
 // ------------------------------------------------------- K6 tangent (AD) --
 // dP/dG per particle by forward-mode duals over the same expression graph as
 // the residual (hand-written AD replacing the tape, tape.hpp:107-122):
-// A[p][(c*D+b)*D*D + (d*D+f)] = dP_cb / dG_df.
+// A[p][(d*D+f)*D*D + (c*D+b)] = dP_cb / dG_df (direction-major: a pass writes
+// whole contiguous runs, so the multi-pass 3D kernel writes full sectors).
 template <int D, int SHAPE, int K, bool NHO>
 __global__ void k_tangent(GridC g, const double* __restrict__ pd, int64_t cap, int P,
                           const double* __restrict__ xs, const int* __restrict__ key,
@@ -894,7 +895,7 @@ __global__ void k_tangent(GridC g, const double* __restrict__ pd, int64_t cap, i
         for (int a = 1; a < D; ++a) s += su.sigma(c, a) * fi(b, a);
         const T Pcb = V * s;
 #pragma unroll
-        for (int j = 0; j < K; ++j) out[(c * D + b) * DD + pass * K + j] = Pcb.d[j];
+        for (int j = 0; j < K; ++j) out[(pass * K + j) * DD + c * D + b] = Pcb.d[j];
       }
   }
 }
@@ -1293,10 +1294,14 @@ __global__ void __launch_bounds__(WARPS * 32) k_assemble_bins_staged(
             const int e = lane + 32 * i;
             ta[i] = e < np * NA ? __ldg(Ab + e) : 0.0;
           }
+          // global A is direction-major [df][cb]; As keeps [cb][df] for the H loop
 #pragma unroll
           for (int i = 0; i < NL; ++i) {
             const int e = lane + 32 * i;
-            if (e < np * NA) As[warp][e] = ta[i];
+            if (e < np * NA) {
+              const int pl = e / NA, r = e - pl * NA, df = r / DD, cb = r - df * DD;
+              As[warp][pl * NA + cb * DD + df] = ta[i];
+            }
           }
         }
         for (int e = lane; e < np * D * 3; e += 32) {
