@@ -19,13 +19,13 @@ cap() {  # name regex skip   (ONLY="cg res" limits the captures)
   [ "$1" = "cg" ] || rm -f $OUT/prof_$1.ncu-rep
   tail -1 $OUT/$1.md
 }
-# fp32 level SpMVs: the half-warp variant runs on levels 0 and 1 only;
+# level SpMVs: the fp16 half-warp variant runs on levels 0 and 1 only;
 # residual sweeps go fine -> coarse (even index = level 0), post-smoothing
 # sweeps coarse -> fine (odd index = level 0); the skips land in step 2
 B='\(bool\)'
 cap cg   "k_spmv<${I}3, ${I}3, ${I}4, ${I}0, double," 63
-cap res  "k_spmv<${I}3, ${I}3, ${I}4, ${I}2, float, ${I}0, ${B}1>" 130
-cap jac  "k_spmv<${I}3, ${I}3, ${I}4, ${I}1, float, ${I}0, ${B}1>" 131
+cap res  "k_spmv<${I}3, ${I}3, ${I}4, ${I}2, __half, ${I}0, ${B}1>" 130
+cap jac  "k_spmv<${I}3, ${I}3, ${I}4, ${I}1, __half, ${I}0, ${B}1>" 131
 cap asm  "k_assemble_bins_staged" 94
 cap resb "k_residual_bins" 150
 cap tan  "k_tangent" 3
