@@ -252,6 +252,12 @@ struct Sim {
   // 3D tangent: one dual direction per pass (160 registers, 9 passes) beats
   // three per pass (255 registers, 12% occupancy): 13.7 -> 10.3 ms per step
   bool tangent_k1 = true;
+  // rebuild the coarse MG levels every mg_refresh load steps (A/B experiments)
+  // (default 3; a solve on stale levels that fails or overruns 4x the last
+  // iteration count is retried once on a freshly built hierarchy)
+  int mg_refresh = std::getenv("IMPM_MG_REFRESH") ? std::atoi(std::getenv("IMPM_MG_REFRESH")) : 3;
+  bool mg_stale = false;
+  int last_cg_iters = 0;
   int mg_f16sim = std::getenv("IMPM_MG_F16SIM") ? std::atoi(std::getenv("IMPM_MG_F16SIM")) : 0;  // A/B experiment
   // fine-level smoother matrix in fp16 with fp32 row scales (IMPM_MG_F16=0: fp32)
   bool mg_f16 = !(std::getenv("IMPM_MG_F16") && std::atoi(std::getenv("IMPM_MG_F16")) == 0);
@@ -935,7 +941,7 @@ struct Sim {
     if (coupled) CK(cudaMemsetAsync(prev.p, 0, sizeof(double) * NF(), s));  // p_nodes_ = 0 (porous.cpp:70)
     matrix_valid = false;
     step_built = true;
-    mg_setup_step = -1;  // new row structure: rebuild the MG hierarchy
+    if (mg_refresh <= 1) mg_setup_step = -1;  // new row structure: rebuild the MG hierarchy
     sync();
   }
 
@@ -1251,8 +1257,36 @@ struct Sim {
   void mg_setup() {
     constexpr int S = ipow_c(5, DD);
     constexpr int FF = FE * FE;
-    if (mg_reuse && mg_setup_step == step_counter && !mg.empty() && mg[0]->n_act == n_act &&
-        mg[0]->vals == vals.p) {
+    // coarse levels of an earlier load step (mg_refresh > 1): the fine level
+    // is re-pointed at the current J and row structure; the stale Galerkin
+    // levels stay a fixed SPD preconditioner (R = P^T under the same masks)
+    const bool cross_step = mg_refresh > 1 && !slab && !coupled && mg_setup_step >= 0 &&
+                            mg_setup_step != step_counter && step_counter - mg_setup_step < mg_refresh &&
+                            !mg.empty() && (!mg_f16 || !mg[0]->vals16 || true);
+    mg_stale = cross_step;
+    if (cross_step) {
+      MgLevel& L0 = *mg[0];
+      L0.n_act = n_act;
+      L0.row_len = row_len;
+      L0.act_idx = act_idx.p;
+      L0.act_list = act_list.p;
+      L0.row_nzb = row_nzb.p;
+      L0.freem = freem.p;
+      L0.row_slots = row_slots.p;
+      L0.vals = vals.p;
+      L0.dinv = dinv.p;
+      if (mg_f16) {
+        vals16.ensure(std::max<int64_t>(1, static_cast<int64_t>(n_act) * L0.row_len16));
+        rscale16.ensure(std::max(1, n_act));
+        L0.vals16 = vals16.p;
+        L0.rscale = rscale16.p;
+      } else if (mg_f32) {
+        vals32.ensure(std::max<int64_t>(1, static_cast<int64_t>(n_act) * L0.row_len32));
+        L0.vals32 = vals32.p;
+      }
+    }
+    if (mg_reuse && !mg.empty() &&
+        (cross_step || (mg_setup_step == step_counter && mg[0]->n_act == n_act && mg[0]->vals == vals.p))) {
       if (mg_f16 && !coupled && n_act > 0) {  // fine level: fp16 smoother copy of the current J
         k_vals_to_f16<FE><<<kSpmvBlocks, 128, 0, s>>>(n_act, row_nzb.p, vals.p, row_len, vals16.p, mg[0]->row_len16,
                                                         rscale16.p);
@@ -1606,9 +1640,34 @@ struct Sim {
   // MG-preconditioned CG (device-resident scalars, batched host checks)
   template <int DD, int FE>
   int cg_mg_solve(const double* b, double* x) {
+    // stale coarse levels (mg_refresh): try with a cap, rebuild and retry on failure
+    if (mg_refresh > 1 && !slab && !coupled) {
+      const bool will_reuse = mg_setup_step >= 0 && mg_setup_step != step_counter &&
+                              step_counter - mg_setup_step < mg_refresh && !mg.empty();
+      if (will_reuse && last_cg_iters > 0) {
+        int it = -1;
+        try {
+          it = cg_mg_solve_once<DD, FE>(b, x, std::max(50, 4 * last_cg_iters));
+        } catch (const SimError& e) {
+          if (e.code != IMPM_ERR_LINEAR_SOLVER) throw;
+          it = -1;
+        }
+        if (it >= 0) return last_cg_iters = it;
+        mg_setup_step = -1;  // rebuild the hierarchy for the current J and retry
+      }
+    }
+    const int it = cg_mg_solve_once<DD, FE>(b, x, 0);
+    if (it >= 0) last_cg_iters = it;
+    return it;
+  }
+
+  template <int DD, int FE>
+  int cg_mg_solve_once(const double* b, double* x, int cap) {
     const int N = g.N;
     const int64_t n = NF();
-    const int max_it = opt.krylov_max_iter > 0 ? opt.krylov_max_iter : std::min(20000, std::max(100, 10 * ndg()));
+    const int max_it = cap > 0                   ? cap
+                       : opt.krylov_max_iter > 0 ? opt.krylov_max_iter
+                                                 : std::min(20000, std::max(100, 10 * ndg()));
     const double rtol2 = cur_rtol * cur_rtol;
     {
       Prof::Scope ps(&prof, kcMgSetup);
@@ -1666,6 +1725,7 @@ struct Sim {
     if (done == 2) return -iters - 1;
     if (done == 3) throw SimError(IMPM_ERR_LINEAR_SOLVER, "Krylov breakdown: NaN residual");
     if (done == 4) {
+      if (cap > 0) return -1;  // capped attempt on stale levels: the caller rebuilds and retries
       const double rel = std::sqrt(h_sc[kRr] / h_sc[kBb]);
       if (!(rel <= 1e-6))
         throw SimError(IMPM_ERR_LINEAR_SOLVER, "MG-CG did not converge: relative residual " + std::to_string(rel));
