@@ -1596,6 +1596,10 @@ __host__ __device__ constexpr int64_t row_len_of(int S, int F) {
 // with an fp32 row scale s_row = max|a| / 1024 (rscale), products in fp32
 // against the fp32-staged x, row sums rescaled once
 // RPW: rows per warp and chunk (0: the runtime rows_per_warp argument)
+#ifndef IMPM_HW16
+#define IMPM_HW16 16  // 8 measured slower (level 0: 49 vs 41 ms per load step)
+#endif
+constexpr int HW16 = IMPM_HW16;  // lanes per fp16 row on the big levels
 template <int D, int F, int WARPS, int MODE = kSpmvY, class VT = double, int RPW = 16, bool HALF = false>
 __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC g, const int* __restrict__ act_list, int n_act,
                                                      const VT* __restrict__ vals, int64_t row_len,
@@ -1625,7 +1629,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
   // lanes per row: fp32 rows carry half the bytes, so on big levels (HALF) a
   // half-warp streams one row and each warp keeps two rows (two latency
   // chains) in flight
-  constexpr int HW = (sizeof(VT) <= 4 && HALF) ? 16 : 32;
+  constexpr int HW = (sizeof(VT) == 2 && HALF) ? HW16 : ((sizeof(VT) == 4 && HALF) ? 16 : 32);
   constexpr int RW = 32 / HW;  // rows per warp in flight
   __shared__ int offt[S];
   // x neighbourhood staged in the matrix precision (fp32 copies: products in
