@@ -1168,8 +1168,16 @@ __global__ void __launch_bounds__(WARPS * 32) k_assemble_bins(
 // SYM: the single-field J is symmetric (hyperelastic / associative J2: the
 // per-particle tangent has major symmetry), so only blocks with l >= k are
 // computed and the transpose is mirrored into row l: ~45% fewer task rounds.
+//
+// A bin with at most PCH particles (the common case: PCH = 8 = ppc^3 in 3D) is
+// staged once and stays resident across all of its task rounds; larger bins
+// restage per round and chunk. H_k is kept only for the rows a round touches
+// (at most HROWS: 13 in 3D with SYM, 8 without), and the 1D weights alias that
+// buffer (they are dead once G is built).
+template <int D>
+__host__ __device__ constexpr int asm_hrows(int nk) { return D == 3 ? 13 : nk; }
 template <int D, int SHAPE, int PPL, int WARPS, int PCH, bool SYM = false>
-__global__ void __launch_bounds__(WARPS * 32) k_assemble_bins_staged(
+__global__ void __launch_bounds__(WARPS * 32, D == 3 ? 5 : 1) k_assemble_bins_staged(
     GridC g, const double* __restrict__ pd, int64_t cap, const double* __restrict__ xs,
     const int* __restrict__ bin_start, const uint8_t* __restrict__ bflag, const double* __restrict__ A,
     const int* __restrict__ act_idx, const unsigned* __restrict__ row_mask, const int* __restrict__ row_nzb,
@@ -1178,14 +1186,16 @@ __global__ void __launch_bounds__(WARPS * 32) k_assemble_bins_staged(
   constexpr int D3 = D * D * D;
   constexpr int NA = DD * DD;
   constexpr int NK = ipow_c(3, D);
+  constexpr int HROWS = asm_hrows<D>(NK);
+  constexpr int NW1 = PCH * D * 6;  // 1D weights [pl][a][i][w|dw]
+  constexpr int NHW = HROWS * D3 > NW1 ? HROWS * D3 : NW1;
   __shared__ double As[WARPS][PCH * NA];
   __shared__ double Gs[WARPS][PCH][NK][D];
-  __shared__ double Hs[WARPS][NK * D3];
+  __shared__ double HWs[WARPS][NHW];  // H rows [k - k_lo] of a round; 1D weights while staging
   // row metadata of the bin's box nodes: row index, slot mask, component pitch
   __shared__ int Rrow[WARPS][NK];
   __shared__ int Rcp[WARPS][NK];
   __shared__ uint4 Rmask[WARPS][NK];
-  __shared__ double W1[WARPS][PCH][D][3][2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nbins = nb0 * nb1 * nb2;
   const int col[3] = {c0, c1, c2};
@@ -1250,6 +1260,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_assemble_bins_staged(
     }
     __syncwarp();
     const int p0 = bin_start[b], p1 = bin_start[b + 1];
+    const bool resident = p1 - p0 <= PCH;
     for (int r0 = 0; r0 < ntasks; r0 += 32) {
       const int task = r0 + lane;
       const bool has_task = task < ntasks;
@@ -1280,30 +1291,40 @@ __global__ void __launch_bounds__(WARPS * 32) k_assemble_bins_staged(
           cp = Rcp[warp][tk];
         }
       }
+      // this round's lanes use row nodes [k_lo, k_hi] only (~5 of 27)
+      int k_lo, k_hi, dummy;
+      task_of(r0, k_lo, dummy);
+      task_of(min(r0 + 31, ntasks - 1), k_hi, dummy);
+      if (k_hi - k_lo + 1 > HROWS) __trap();
+      const int nh = (k_hi - k_lo + 1) * D3;
       for (int pc = p0; pc < p1; pc += PCH) {
         const int np = min(PCH, p1 - pc);
+        if (!resident || r0 == 0) {
         __syncwarp();
         // stage A_p (contiguous) and the 1D weights of the chunk; the A loads
-        // go to registers first so that all of them are in flight at once
+        // go to registers first (4 particles at a time) so that they are in
+        // flight together
         const double* Ab = A + static_cast<int64_t>(pc) * NA;
-        {
-          constexpr int NL = (PCH * NA + 31) / 32;
+#pragma unroll 1
+        for (int q0 = 0; q0 < PCH; q0 += 4) {
+          constexpr int NL = (4 * NA + 31) / 32;
           double ta[NL];
 #pragma unroll
           for (int i = 0; i < NL; ++i) {
-            const int e = lane + 32 * i;
-            ta[i] = e < np * NA ? __ldg(Ab + e) : 0.0;
+            const int e = q0 * NA + lane + 32 * i;
+            ta[i] = (e < np * NA && e < (q0 + 4) * NA) ? __ldg(Ab + e) : 0.0;
           }
           // global A is direction-major [df][cb]; As keeps [cb][df] for the H loop
 #pragma unroll
           for (int i = 0; i < NL; ++i) {
-            const int e = lane + 32 * i;
-            if (e < np * NA) {
+            const int e = q0 * NA + lane + 32 * i;
+            if (e < np * NA && e < (q0 + 4) * NA) {
               const int pl = e / NA, r = e - pl * NA, df = r / DD, cb = r - df * DD;
               As[warp][pl * NA + cb * DD + df] = ta[i];
             }
           }
         }
+        double* W1 = HWs[warp];
         for (int e = lane; e < np * D * 3; e += 32) {
           const int pl = e / (D * 3), rem = e - pl * D * 3, a = rem / 3, i = rem - a * 3;
           double w = 0.0, dw = 0.0;
@@ -1314,8 +1335,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_assemble_bins_staged(
             w = wv.w;
             dw = wv.dw;
           }
-          W1[warp][pl][a][i][0] = w;
-          W1[warp][pl][a][i][1] = dw;
+          W1[((pl * D + a) * 3 + i) * 2] = w;
+          W1[((pl * D + a) * 3 + i) * 2 + 1] = dw;
         }
         __syncwarp();
         for (int e = lane; e < np * nk; e += 32) {
@@ -1329,19 +1350,15 @@ __global__ void __launch_bounds__(WARPS * 32) k_assemble_bins_staged(
           double w[3], dw[3], W, gk[3];
 #pragma unroll
           for (int a = 0; a < D; ++a) {
-            w[a] = W1[warp][pl][a][li[a]][0];
-            dw[a] = W1[warp][pl][a][li[a]][1];
+            w[a] = W1[((pl * D + a) * 3 + li[a]) * 2];
+            dw[a] = W1[((pl * D + a) * 3 + li[a]) * 2 + 1];
           }
           tensor_weight<D>(w, dw, W, gk);
 #pragma unroll
           for (int a = 0; a < D; ++a) Gs[warp][pl][k][a] = gk[a];
         }
+        }
         __syncwarp();
-        // this round's lanes use row nodes [k_lo, k_hi] only (~5 of 27)
-        int k_lo, k_hi, dummy;
-        task_of(r0, k_lo, dummy);
-        task_of(min(r0 + 31, ntasks - 1), k_hi, dummy);
-        const int nh = (k_hi - k_lo + 1) * D3;
         for (int pl = 0; pl < np; ++pl) {
           const double* Ap = &As[warp][pl * NA];
           for (int e = k_lo * D3 + lane; e < k_lo * D3 + nh; e += 32) {
@@ -1349,7 +1366,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_assemble_bins_staged(
             double sacc = 0.0;
 #pragma unroll
             for (int bb = 0; bb < D; ++bb) sacc += Gs[warp][pl][k][bb] * Ap[(c * D + bb) * DD + df];
-            Hs[warp][e] = sacc;
+            HWs[warp][e - k_lo * D3] = sacc;
           }
           __syncwarp();
           if (has_task) {
@@ -1358,7 +1375,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_assemble_bins_staged(
             for (int t = 0; t < PPL; ++t)
 #pragma unroll
               for (int f = 0; f < D; ++f) gl[t][f] = (tl0 + t < nk) ? Gs[warp][pl][tl0 + t][f] : 0.0;
-            const double* Hk = &Hs[warp][tk * D3];
+            const double* Hk = &HWs[warp][(tk - k_lo) * D3];
 #pragma unroll
             for (int cd = 0; cd < DD; ++cd) {
               double hv[3];

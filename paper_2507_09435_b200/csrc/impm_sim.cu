@@ -1045,17 +1045,19 @@ struct Sim {
           }
           const int nbins = nb[0] * nb[1] * nb[2];
           if (nbins == 0) continue;
-          constexpr int WS = 4;
+          // 3D: 3 warps of 8-particle resident bins (41.5 KB static shared, 5 CTAs/SM)
+          constexpr int WS = DD == 3 ? 3 : 4;
+          constexpr int PCH = DD == 3 ? 8 : 4;
           const unsigned grid = std::min<unsigned>(blocks_for(nbins, WS), 148 * 32);
           // J is symmetric except under non-associative Drucker-Prager flow and
           // Cam-Clay (associative, but its compaction hardening breaks major
           // symmetry of dP/dG: ~2% in tests/test_math_cpu.py terms)
           if (mat.kind != kDruckerPrager && mat.kind != kCamClay)
-            k_assemble_bins_staged<DD, SH, (DD == 3 ? asm_ppl3 : PPL), WS, 4, true><<<grid, WS * 32, 0, s>>>(
+            k_assemble_bins_staged<DD, SH, (DD == 3 ? asm_ppl3 : PPL), WS, PCH, true><<<grid, WS * 32, 0, s>>>(
                 g, pd.p, cap, xs.p, bin_start.p, bflag.p, Atan.p, act_idx.p, row_mask.p, row_nzb.p, vals.p, row_len,
                 cc[0], cc[1], cc[2], nb[0], nb[1], nb[2]);
           else
-            k_assemble_bins_staged<DD, SH, (DD == 3 ? asm_ppl3 : PPL), WS, 4, false><<<grid, WS * 32, 0, s>>>(
+            k_assemble_bins_staged<DD, SH, (DD == 3 ? asm_ppl3 : PPL), WS, PCH, false><<<grid, WS * 32, 0, s>>>(
                 g, pd.p, cap, xs.p, bin_start.p, bflag.p, Atan.p, act_idx.p, row_mask.p, row_nzb.p, vals.p, row_len,
                 cc[0], cc[1], cc[2], nb[0], nb[1], nb[2]);
           ++g_launches;
