@@ -1171,11 +1171,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_assemble_bins(
 //
 // A bin with at most PCH particles (the common case: PCH = 8 = ppc^3 in 3D) is
 // staged once and stays resident across all of its task rounds; larger bins
-// restage per round and chunk. H_k is kept only for the rows a round touches
-// (at most HROWS: 13 in 3D with SYM, 8 without), and the 1D weights alias that
-// buffer (they are dead once G is built).
-template <int D>
-__host__ __device__ constexpr int asm_hrows(int nk) { return D == 3 ? 13 : nk; }
+// restage per round and chunk.
 template <int D, int SHAPE, int PPL, int WARPS, int PCH, bool SYM = false>
 __global__ void __launch_bounds__(WARPS * 32, D == 3 ? 5 : 1) k_assemble_bins_staged(
     GridC g, const double* __restrict__ pd, int64_t cap, const double* __restrict__ xs,
@@ -1186,12 +1182,10 @@ __global__ void __launch_bounds__(WARPS * 32, D == 3 ? 5 : 1) k_assemble_bins_st
   constexpr int D3 = D * D * D;
   constexpr int NA = DD * DD;
   constexpr int NK = ipow_c(3, D);
-  constexpr int HROWS = asm_hrows<D>(NK);
   constexpr int NW1 = PCH * D * 6;  // 1D weights [pl][a][i][w|dw]
-  constexpr int NHW = HROWS * D3 > NW1 ? HROWS * D3 : NW1;
   __shared__ double As[WARPS][PCH * NA];
   __shared__ double Gs[WARPS][PCH][NK][D];
-  __shared__ double HWs[WARPS][NHW];  // H rows [k - k_lo] of a round; 1D weights while staging
+  __shared__ double HWs[WARPS][NW1];  // 1D weights of the staged chunk
   // row metadata of the bin's box nodes: row index, slot mask, component pitch
   __shared__ int Rrow[WARPS][NK];
   __shared__ int Rcp[WARPS][NK];
@@ -1291,12 +1285,6 @@ __global__ void __launch_bounds__(WARPS * 32, D == 3 ? 5 : 1) k_assemble_bins_st
           cp = Rcp[warp][tk];
         }
       }
-      // this round's lanes use row nodes [k_lo, k_hi] only (~5 of 27)
-      int k_lo, k_hi, dummy;
-      task_of(r0, k_lo, dummy);
-      task_of(min(r0 + 31, ntasks - 1), k_hi, dummy);
-      if (k_hi - k_lo + 1 > HROWS) __trap();
-      const int nh = (k_hi - k_lo + 1) * D3;
       for (int pc = p0; pc < p1; pc += PCH) {
         const int np = min(PCH, p1 - pc);
         if (!resident || r0 == 0) {
@@ -1359,35 +1347,36 @@ __global__ void __launch_bounds__(WARPS * 32, D == 3 ? 5 : 1) k_assemble_bins_st
         }
         }
         __syncwarp();
-        for (int pl = 0; pl < np; ++pl) {
-          const double* Ap = &As[warp][pl * NA];
-          for (int e = k_lo * D3 + lane; e < k_lo * D3 + nh; e += 32) {
-            const int k = e / D3, cdf = e - k * D3, c = cdf / DD, df = cdf - c * DD;
-            double sacc = 0.0;
+        // each lane forms its own row's H_k = g^k . A_p one component row c at
+        // a time (A_p and g^k are warp-uniform shared-memory broadcasts), so the
+        // particle loop needs no warp barrier
+        if (has_task) {
+          for (int pl = 0; pl < np; ++pl) {
+            const double* Ap = &As[warp][pl * NA];
+            double gk[3], gl[PPL][3];
 #pragma unroll
-            for (int bb = 0; bb < D; ++bb) sacc += Gs[warp][pl][k][bb] * Ap[(c * D + bb) * DD + df];
-            HWs[warp][e - k_lo * D3] = sacc;
-          }
-          __syncwarp();
-          if (has_task) {
-            double gl[PPL][3];
+            for (int bb = 0; bb < D; ++bb) gk[bb] = Gs[warp][pl][tk][bb];
 #pragma unroll
             for (int t = 0; t < PPL; ++t)
 #pragma unroll
               for (int f = 0; f < D; ++f) gl[t][f] = (tl0 + t < nk) ? Gs[warp][pl][tl0 + t][f] : 0.0;
-            const double* Hk = &HWs[warp][(tk - k_lo) * D3];
 #pragma unroll
             for (int cd = 0; cd < DD; ++cd) {
-              double hv[3];
+              const int c = cd / D, d = cd - c * D;
+              double h[3];  // H_k[c][d * D + f]
 #pragma unroll
-              for (int f = 0; f < D; ++f) hv[f] = Hk[cd * D + f];
+              for (int f = 0; f < D; ++f) {
+                double sacc = 0.0;
+#pragma unroll
+                for (int bb = 0; bb < D; ++bb) sacc = fma(gk[bb], Ap[(c * D + bb) * DD + d * D + f], sacc);
+                h[f] = sacc;
+              }
 #pragma unroll
               for (int t = 0; t < PPL; ++t)
 #pragma unroll
-                for (int f = 0; f < D; ++f) acc[t][cd] = fma(hv[f], gl[t][f], acc[t][cd]);
+                for (int f = 0; f < D; ++f) acc[t][cd] = fma(h[f], gl[t][f], acc[t][cd]);
             }
           }
-          __syncwarp();
         }
       }
       if (has_task) {
