@@ -1173,7 +1173,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_assemble_bins(
 // staged once and stays resident across all of its task rounds; larger bins
 // restage per round and chunk.
 template <int D, int SHAPE, int PPL, int WARPS, int PCH, bool SYM = false>
-__global__ void __launch_bounds__(WARPS * 32, D == 3 ? 5 : 1) k_assemble_bins_staged(
+__global__ void __launch_bounds__(WARPS * 32, D == 3 ? 4 : 1) k_assemble_bins_staged(
     GridC g, const double* __restrict__ pd, int64_t cap, const double* __restrict__ xs,
     const int* __restrict__ bin_start, const uint8_t* __restrict__ bflag, const double* __restrict__ A,
     const int* __restrict__ act_idx, const unsigned* __restrict__ row_mask, const int* __restrict__ row_nzb,

@@ -1045,8 +1045,8 @@ struct Sim {
           }
           const int nbins = nb[0] * nb[1] * nb[2];
           if (nbins == 0) continue;
-          // 3D: 3 warps of 8-particle resident bins (41.5 KB static shared, 5 CTAs/SM)
-          constexpr int WS = DD == 3 ? 3 : 4;
+          // 3D: 4 warps of 8-particle resident bins (47.5 KB static shared, 4 CTAs/SM)
+          constexpr int WS = 4;
           constexpr int PCH = DD == 3 ? 8 : 4;
           const unsigned grid = std::min<unsigned>(blocks_for(nbins, WS), 148 * 32);
           // J is symmetric except under non-associative Drucker-Prager flow and
