@@ -111,3 +111,26 @@ def test_cam_clay_elastic_limit_matches_hencky():
     for f in ("x", "sigma"):
         x, y = getattr(pa, f), getattr(pb, f)
         assert np.abs(x - y).max() <= 1e-9 * np.abs(y).max()
+
+
+@pytest.mark.parametrize("ppc", [2, 3])
+def test_3d_assembly_resident_and_restaged_bins(ppc):
+    """The staged assembly keeps a bin of <= 8 particles resident across its
+    task rounds (ppc 2: 8 per cell) and restages larger bins per round and
+    chunk (ppc 3: 27 per cell, 4 chunks). Both paths must give the FD Jacobian
+    of the GPU residual, symmetric for hyperelastic Hencky."""
+    import paper_2507_09435_b200 as impm
+    from paper_2507_09435_b200 import workloads
+
+    prob = workloads.footing3d(cells=(8, 8, 4), ppc=ppc, h=0.5, steps=10, t_hat=100e3, material="hencky")
+    sim = impm.MpmSim(prob.grid, prob.particles, prob.material, prob.options)
+    sim.fixed[:] = prob.fixed
+    sim.gravity = prob.gravity
+    assert sim.step(1 / prob.load_steps).iterations <= 8
+    sim.begin_step()
+    s = 2 / prob.load_steps
+    sim.newton_solve(s)
+    u = sim.nodal_solution()
+    err, J = fd_check(sim, s, u, 1e-9)
+    assert err <= 1e-5, err
+    assert abs(J - J.T).max() <= 1e-10 * abs(J).max()
