@@ -161,13 +161,15 @@ def make_sim(prob, device, profile, comm=None):
 
 
 def ncu_traffic(name):
-    """DRAM bytes per launch of a kernel from the committed ncu --set full
-    capture (scripts/ncu_steady.sh -> profiles/r01/ncu_steady/traffic.json)."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01", "ncu_steady", "traffic.json")
+    """DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) per launch of
+    a kernel class from the committed ncu capture of the CURRENT kernels
+    (profiles/r02/traffic.json, written by scripts/ncu_traffic.py), or None."""
+    path = os.path.join(REPO, "profiles", "r02", "traffic.json")
     try:
         with open(path) as f:
-            return json.load(f)[name]["traffic_bytes"]
-    except (OSError, KeyError, ValueError):
+            t = json.load(f)[name]
+        return {"traffic_bytes": t["traffic_bytes"], "source": t.get("source", path)}
+    except (OSError, KeyError, ValueError, TypeError):
         return None
 
 
@@ -180,6 +182,64 @@ def spmv_bytes(info, D):
     return stored_values * 8 + stored_values // (D * D) + rows * (4 + 4 + D * 8 + D * 8 + D)
 
 
+def fp64_peak():
+    """DFMA peak (TFLOP/s): profiles/r02/fp64_peak.json (scripts/fp64_peak.cu
+    on this pool's B200), else the nominal 37 TFLOP/s (148 SMs x 64 DFMA/clk x
+    1.965 GHz x 2)."""
+    path = os.path.join(REPO, "profiles", "r02", "fp64_peak.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["dfma_tflops"]), "measured (profiles/r02/fp64_peak.json)"
+    except (OSError, KeyError, ValueError):
+        return 37.2, "nominal"
+
+
+def kernel_table(kt, rec, info, D, P, n_nodes, peak):
+    """One row per kernel class of the profiled load step: CUDA-event time,
+    launches, SURVEY.md 8(d) algorithmic bytes per launch, achieved GB/s and
+    fraction of the measured HBM peak. K6 (tangent + assembly) counts as one
+    launch per Jacobian: 184 B/particle of state reads + 8 B per
+    reference-pattern nnz written (8(d) K6, ~1.31 kB/particle in 3D)."""
+    total = sum(v[0] for k, v in kt.items() if k not in ("vcycle_level0", "vcycle_level1", "vcycle_coarse",
+                                                          "galerkin", "mg_power", "mg_coarsest"))
+    its = max(rec.iterations, 1)
+    ref_nnz = rec.nnz_assembled / its  # per Jacobian
+    n_jac = kt["assemble"][1]
+    rows = []
+
+    def row(name, kernel, ms, n, byt, model, key, flops=None):
+        per = ms / n if n else None
+        ach = byt / (per / 1e3) / 1e9 if (byt and per) else None
+        r = {"class": name, "kernel": kernel, "ms_total": ms, "launches": n, "ms_per_launch": per,
+             "bytes_per_launch": byt, "bytes_model": model, "achieved_gbs": ach,
+             "frac": ach / peak if ach else None, "share": ms / total if total else None, "traffic_key": key}
+        if flops and per:
+            fpk, src = fp64_peak()
+            r["fp64"] = {"flops_per_launch": flops, "achieved_tflops": flops / (per / 1e3) / 1e12,
+                         "peak_tflops": fpk, "frac": flops / (per / 1e3) / 1e12 / fpk, "peak_source": src}
+        rows.append(r)
+
+    jm = kt["tangent"][0] + kt["assemble"][0]
+    row("jacobian", "K6 Jacobian: k_tangent (dual-number dP/dG) + k_assemble_bins_staged (colour-batched BSR)",
+        jm, n_jac, (184 * P + 8 * ref_nnz) if n_jac else None,
+        "SURVEY 8(d) K6: 184 B/particle state + 8 B x reference-pattern nnz", "jacobian")
+    row("spmv", "k_spmv<double> (compacted box-BSR y = J x, outer Krylov)", kt["spmv"][0], kt["spmv"][1],
+        spmv_bytes(info, D), "stored block values x 8 + slot ids + 33 B/row", "cg")
+    nres = kt["residual_particles"][1]
+    row("residual", "K5 residual: k_residual_bins_staged (+ per-particle pass)", kt["residual_particles"][0] +
+        kt["residual_nodes"][0], nres, (184 * P + 16 * D * n_nodes) if nres else None,
+        "SURVEY 8(d) K5: 184 B/particle + 16 F B/node", "resb")
+    row("commit", "K9 G2P k_commit", kt["commit"][0], kt["commit"][1], 384 * P if kt["commit"][1] else None,
+        "SURVEY 8(d) K9: 184 + 200 B/particle", "commit")
+    row("vcycle", "MG V-cycle (fp16/fp32 level sweeps, restriction, prolongation)", kt["vcycle"][0],
+        kt["vcycle"][1], None, "-", "jac")
+    row("mg_setup", "MG setup (Galerkin PtAP, power estimate)", kt["mg_setup"][0], kt["mg_setup"][1], None, "-",
+        "gap")
+    row("krylov_vector", "Krylov BLAS-1 (dots, axpys)", kt["krylov_vector"][0], kt["krylov_vector"][1], None,
+        "-", None)
+    return rows
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -187,7 +247,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="product", choices=["product", "reference"])
     ap.add_argument("--config", default="cfg4", choices=["cfg4", "cfg1"])
-    ap.add_argument("--material", default="neo_hookean", choices=["neo_hookean", "cam_clay", "hencky_j2", "hencky"],
+    ap.add_argument("--material", default="neo_hookean",
+                    choices=["neo_hookean", "cam_clay", "drucker_prager", "hencky_j2", "hencky"],
                     help="cfg4/cfg5 material: neo-Hookean (pinned substitute, default) or an unpinned extension")
     ap.add_argument("--e2e-steps", type=int, default=None, help="timed end-to-end load steps (default: --steps)")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
@@ -236,6 +297,13 @@ def main():
 
     from paper_2507_09435_b200 import _abi, workloads
 
+    # Load schedule: the reference ramps the load as k / steps and never
+    # re-solves a load it has reached (scenarios.cpp:130-131). The bench runs
+    # warmup + steps device load steps, one profiled step and (on a fresh sim)
+    # warmup + e2e_steps end-to-end steps, so the ramp has at least that many
+    # increments and every step advances the load.
+    n_total = max(20, args.warmup + max(args.steps + 1, args.e2e_steps))
+
     comm = None
     if world > 1:
         # cfg 5: one cfg 4 slab per GPU, stacked along axis 0, one NCCL
@@ -250,19 +318,21 @@ def main():
         comm = Communicator.nccl(rank, world, device, broadcast=bcast)
         if args.config != "cfg4":
             raise SystemExit("multi-GPU runs use the cfg 5 slab workload (--config cfg4)")
-        prob = workloads.footing3d_slab(world, rank, material=args.material)
+        prob = workloads.footing3d_slab(world, rank, material=args.material, steps=n_total)
     elif args.config == "cfg4":
-        prob = workloads.footing3d(material=args.material)
+        prob = workloads.footing3d(material=args.material, steps=n_total)
     else:
-        prob = workloads.column2d_nh()
+        prob = workloads.column2d_nh(steps=n_total)
     D = prob.grid.dim
     sim = make_sim(prob, device, profile=False, comm=comm)
     stream = torch.cuda.current_stream(device)
     sim.set_stream(stream.cuda_stream)
-    n_total = prob.load_steps
+    assert prob.load_steps == n_total
 
     def scale(k):
-        return min(1.0, k / n_total)
+        if k > n_total:
+            raise RuntimeError(f"load step {k} beyond the {n_total}-increment ramp")
+        return k / n_total
 
     # warm-up load steps
     k = 0
@@ -312,14 +382,15 @@ def main():
     ms_max = float(t.item())
     value = float(tot_its.item()) / (ms_max / 1e3)
 
-    # roofline of the dominant kernel (box-BSR SpMV) from live CUDA events
+    # per-kernel table and the roofline of the dominant kernel, from the live
+    # CUDA events of the profiled load step (events on the sim stream)
     peak, peak_kind = peaks()
-    spmv_ms, spmv_n = kt["spmv"]
-    spmv_avg = spmv_ms / max(spmv_n, 1)
-    byt = spmv_bytes(info, D)
-    achieved = byt / (spmv_avg / 1e3) / 1e9 if spmv_n else None
-    asm_ms, asm_n = kt["assemble"]
-    tan_ms, tan_n = kt["tangent"]
+    P = int(prob.particles.shape[0])
+    table = kernel_table(kt, prof_rec, info, D, P, int(prob.grid.node_count()), peak)
+    dom = max((r for r in table if r["bytes_per_launch"]), key=lambda r: r["ms_total"])
+    tr = ncu_traffic(dom["traffic_key"])
+    asm_ms, _ = kt["assemble"]
+    tan_ms, _ = kt["tangent"]
     nnz_rate = prof_rec.nnz_assembled / ((asm_ms + tan_ms) / 1e3) if asm_ms + tan_ms > 0 else None
 
     # end-to-end through the C ABI with host buffers
@@ -428,13 +499,14 @@ def main():
                    "l2": "inputs larger than L2 (particle state 3.3 GB, BSR 9.7 GB per slab)"},
         "newton_iterations": its, "krylov_iterations": kry,
         "nnz_per_s": nnz_rate, "nnz_assembled": nnz,
-        "roofline": {"bound": "hbm", "kernel": "k_spmv (compacted box-BSR, fine level of the MG-PCG solve)",
-                     "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak if achieved else None, "traffic": ncu_traffic("cg"),
-                     "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum per launch, ncu --set full of "
-                                       "the same kernel at cfg4 load step 2 (profiles/r01/ncu_steady/)",
-                     "bytes_per_launch": byt, "avg_launch_ms": spmv_avg, "launches": spmv_n,
-                     "peak_source": peak_kind},
+        "roofline": {"bound": "hbm", "kernel": dom["kernel"], "achieved": dom["achieved_gbs"], "peak": peak,
+                     "unit": "GB/s", "frac": dom["frac"], "traffic": tr["traffic_bytes"] if tr else None,
+                     "traffic_source": (tr or {}).get("source"),
+                     "bytes_per_launch": dom["bytes_per_launch"], "bytes_model": dom["bytes_model"],
+                     "avg_launch_ms": dom["ms_per_launch"], "launches": dom["launches"],
+                     "share_of_step": dom["share"], "peak_source": peak_kind,
+                     "fp64": dom.get("fp64")},
+        "kernels": table,
         "profiled_step": {"newton_iterations": prof_rec.iterations, "krylov_iterations": prof_rec.krylov_iterations,
                           "seconds": prof_rec.seconds},
         "kernel_ms": {k_: v_[0] for k_, v_ in kt.items()},

@@ -106,6 +106,25 @@ def slope2d(cells=(256, 128), ppc=4, h=0.5, steps=20, friction_deg=30.0, E=10e6,
 # = 10, tensile intercept 5 kPa
 CAM_CLAY = {"friction_deg": 30.0, "cohesion": 5e3, "pc0": 600e3, "hardening": 10.0}
 
+# north_star's target material (extension, parity unpinned): Drucker-Prager on
+# Hencky strain, 30 deg friction, 20 kPa cohesion. Under the 100 kPa strip the
+# shallow soil beside the footing edges yields (the plastic zone of a
+# bearing-capacity problem); the deeper soil stays elastic.
+DRUCKER_PRAGER = {"friction_deg": 30.0, "cohesion": 20e3}
+
+
+def _footing_material(material, E, nu):
+    """(MaterialSpec, tag, note) of the cfg 4 / cfg 5 soil."""
+    if material == "cam_clay":
+        return (MaterialSpec("cam_clay", ElasticParams(E, nu), **CAM_CLAY), "mcc",
+                "modified Cam-Clay (extension, parity unpinned); strip traction footing")
+    if material == "drucker_prager":
+        return (MaterialSpec("drucker_prager", ElasticParams(E, nu), **DRUCKER_PRAGER), "dp",
+                "Drucker-Prager (north_star target material; extension, parity unpinned); strip traction footing")
+    tag = "nh" if material == "neo_hookean" else material
+    return (MaterialSpec(material, ElasticParams(E, nu)), tag,
+            "neo-Hookean substitute for modified Cam-Clay (pinned in 3D); strip traction footing")
+
 
 def footing3d(cells=(128, 128, 64), ppc=2, h=0.5, steps=20, t_hat=100e3, frac=0.125, E=10e6, nu=0.3,
               material="neo_hookean"):
@@ -119,13 +138,8 @@ def footing3d(cells=(128, 128, 64), ppc=2, h=0.5, steps=20, t_hat=100e3, frac=0.
     ext = tuple(c * h for c in cells)
     parts = seed_box(grid, (0.0, 0.0, 0.0), ext, ppc, 2000.0)
     n_strip = _strip_traction(parts, D, ext, frac, t_hat, axes=[0])
-    if material == "cam_clay":
-        mat = MaterialSpec("cam_clay", ElasticParams(E, nu), **CAM_CLAY)
-        name, note = "cfg4_footing3d_mcc", "modified Cam-Clay (extension, parity unpinned); strip traction footing"
-    else:
-        mat = MaterialSpec(material, ElasticParams(E, nu))
-        name = "cfg4_footing3d_nh" if material == "neo_hookean" else f"cfg4_footing3d_{material}"
-        note = "neo-Hookean substitute for modified Cam-Clay (unpinned); strip traction footing"
+    mat, tag, note = _footing_material(material, E, nu)
+    name = f"cfg4_footing3d_{tag}"
     return Problem(name, grid, parts, mat, SolverOptions(tol=1e-10), _column_fixed(grid, ext),
                    np.array([0.0, 0.0, -9.81]), steps, note=note, meta={"strip_particles": n_strip})
 
@@ -161,14 +175,10 @@ def footing3d_slab(nranks, rank, cells=(128, 128, 64), ppc=2, h=0.5, steps=20, t
     top = 0.0 + (sub[2] - 1 + 0.5) * spacing
     sel = (pa.X[:, 2] >= top - 1e-9) & (pa.X[:, 0] >= lo) & (pa.X[:, 0] <= hi)
     pa.traction_force[sel, 2] = -t_hat * area / max(n_strip, 1)
-    if material == "cam_clay":
-        mat = MaterialSpec("cam_clay", ElasticParams(E, nu), **CAM_CLAY)
-    else:
-        mat = MaterialSpec(material, ElasticParams(E, nu))
-    tag = "nh" if material == "neo_hookean" else ("mcc" if material == "cam_clay" else material)
+    mat, tag, note = _footing_material(material, E, nu)
     return Problem(f"cfg5_footing3d_{tag}_slab{rank}of{nranks}", grid, parts, mat, SolverOptions(tol=1e-10),
                    _column_fixed(grid, ext), np.array([0.0, 0.0, -9.81]), steps,
-                   note="cfg4 per GPU stacked along axis 0; neo-Hookean substitute for modified Cam-Clay (unpinned)",
+                   note="cfg4 per GPU stacked along axis 0; " + note,
                    meta={"ids": ids, "cuts": cuts, "strip_particles": n_strip, "rank": rank, "nranks": nranks,
                          "global_particles": int(np.prod(sub))})
 
