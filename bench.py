@@ -105,6 +105,7 @@ rho = 2000
 bc = column
 t_hat = 100e3
 strip_fraction = 0.125
+strip_axes = 1
 steps = {steps}
 tol = 1e-10
 """)
@@ -220,7 +221,8 @@ def kernel_table(kt, rec, info, D, P, n_nodes, peak):
         rows.append(r)
 
     jm = kt["tangent"][0] + kt["assemble"][0]
-    row("jacobian", "K6 Jacobian: k_tangent (dual-number dP/dG) + k_assemble_bins_staged (colour-batched BSR)",
+    row("jacobian", "K6 Jacobian: k_tangent_nh3 (closed-form dP/dG; dual numbers for other materials) + "
+                    "k_assemble_bins_staged (colour-batched BSR, upper blocks) + k_mirror_lower + k_diag_inverse",
         jm, n_jac, (184 * P + 8 * ref_nnz) if n_jac else None,
         "SURVEY 8(d) K6: 184 B/particle state + 8 B x reference-pattern nnz", "jacobian")
     row("spmv", "k_spmv<double> (compacted box-BSR y = J x, outer Krylov)", kt["spmv"][0], kt["spmv"][1],
@@ -231,8 +233,16 @@ def kernel_table(kt, rec, info, D, P, n_nodes, peak):
         "SURVEY 8(d) K5: 184 B/particle + 16 F B/node", "resb")
     row("commit", "K9 G2P k_commit", kt["commit"][0], kt["commit"][1], 384 * P if kt["commit"][1] else None,
         "SURVEY 8(d) K9: 184 + 200 B/particle", "commit")
-    row("vcycle", "MG V-cycle (fp16/fp32 level sweeps, restriction, prolongation)", kt["vcycle"][0],
-        kt["vcycle"][1], None, "-", "jac")
+    # fine level of the V-cycle: two fp16 row-scaled sweeps (residual, Jacobi)
+    # per V-cycle + zero-start smoothing, restriction, prolongation; the
+    # profiler opens two level-0 scopes per V-cycle
+    sv, rows_ = info["row_values"], info["rows"]
+    vl0 = kt.get("vcycle_level0", (0.0, 0))
+    row("vcycle_level0", "MG fine level: k_spmv<__half> residual + Jacobi sweeps, k_jacobi0, k_restrict, "
+        "k_prolong_add", vl0[0], vl0[1], (2 * sv + sv // (D * D) + 250 * rows_) if vl0[1] else None,
+        "per scope (half a V-cycle): fp16 values 2 B x stored + slot ids + ~250 B/row of vectors and Dinv", "jac")
+    row("vcycle", "MG V-cycle, all levels (fp16/fp32 level sweeps, restriction, prolongation, coarsest solve)",
+        kt["vcycle"][0], kt["vcycle"][1], None, "-", None)
     row("mg_setup", "MG setup (Galerkin PtAP, power estimate)", kt["mg_setup"][0], kt["mg_setup"][1], None, "-",
         "gap")
     row("krylov_vector", "Krylov BLAS-1 (dots, axpys)", kt["krylov_vector"][0], kt["krylov_vector"][1], None,

@@ -72,13 +72,35 @@ typedef struct impm_material {
 /* Transfer functions: impm::ShapeFunctionKind (gimp.hpp:11). */
 typedef enum impm_shape_kind { IMPM_SHAPE_GIMP = 1, IMPM_SHAPE_BSPLINE2 = 2 } impm_shape_kind;
 
-/* Linear solver behind the sparse_lu_solve seam (src/linear_solver.cpp:11-88). */
+/* Linear solver behind the sparse_lu_solve seam (src/linear_solver.cpp:11-88).
+ * AUTO: the reference's own equilibrated pivoted LU on the device below 2048
+ * free DOFs (one GPU), else ITERATIVE. ITERATIVE: MG-CG for a symmetric J
+ * (GMRES on CG breakdown), MG-GMRES for a nonsymmetric one. CG / BICGSTAB /
+ * GMRES force one method. */
 typedef enum impm_krylov_kind {
-  IMPM_KRYLOV_AUTO = 0, IMPM_KRYLOV_CG = 1, IMPM_KRYLOV_BICGSTAB = 2, IMPM_KRYLOV_GMRES = 3
+  IMPM_KRYLOV_AUTO = 0, IMPM_KRYLOV_CG = 1, IMPM_KRYLOV_BICGSTAB = 2, IMPM_KRYLOV_GMRES = 3,
+  IMPM_KRYLOV_ITERATIVE = 4
 } impm_krylov_kind;
 
 /* Preconditioner of the Krylov solve. */
 typedef enum impm_precond_kind { IMPM_PRECOND_MG = 0, IMPM_PRECOND_BLOCK_JACOBI = 1 } impm_precond_kind;
+
+/* impm::JacobianStrategy (jacobian.hpp:18). Both produce the same values (the
+ * reference's dense == sparse tests); the GPU always assembles by bins, and the
+ * strategy sets the reference-equivalent StepRecord::backward_passes: n_dofs
+ * per Jacobian (Algorithm 1) or fields*b^D (Algorithm 2). Zero = the reference
+ * default (sparse). */
+typedef enum impm_jacobian_strategy { IMPM_STRATEGY_SPARSE = 0, IMPM_STRATEGY_DENSE = 1 } impm_jacobian_strategy;
+
+/* impm::InterferenceCheck (jacobian.hpp:20, verify_no_interference :167-182).
+ * On the GPU the seeding hazard is a particle whose support reaches beyond
+ * the (b-1)/2 = 2-node stencil of the pattern (it would write outside every
+ * seeded pattern of its group): the check verifies every particle support on
+ * the device (always: every Jacobian; sampled: 1 Jacobian in 8) and fails with
+ * IMPM_ERR_SEEDING (impm::SeedingFault) and the reference's message text. */
+typedef enum impm_interference_check {
+  IMPM_INTERFERENCE_OFF = 0, IMPM_INTERFERENCE_SAMPLED = 1, IMPM_INTERFERENCE_ALWAYS = 2
+} impm_interference_check;
 
 /* impm::SolverOptions (mpm_solver.hpp:27-36) + GPU linear-solver knobs. */
 typedef struct impm_options {
@@ -93,6 +115,8 @@ typedef struct impm_options {
   int32_t profile;            /* 1: per-kernel-class CUDA-event timing */
   int32_t precond;            /* impm_precond_kind */
   int32_t mg_smooth;          /* multigrid pre/post block-Jacobi sweeps (0 => 1) */
+  int32_t strategy;           /* impm_jacobian_strategy value; SolverOptions::strategy, mpm_solver.hpp:30 */
+  int32_t interference;       /* impm_interference_check value; SolverOptions::interference, mpm_solver.hpp:31 */
 } impm_options;
 
 /* impm::StepRecord (mpm_solver.hpp:38-46) + GPU counters. rel_residuals is
@@ -157,6 +181,11 @@ impm_status impm_sim_dof_map(impm_sim* sim, int32_t* dof_of /*[N*D]*/, int32_t* 
 impm_status impm_sim_node_mass(impm_sim* sim, double* mass /*[N]*/);
 /* JacobianAssembler colouring (jacobian.hpp:101-110): group id per DOF. */
 impm_status impm_sim_colour_groups(impm_sim* sim, int32_t* group_of_dof /*[n]*/, int32_t* n_groups);
+/* Diagnostics of the current step's supports (sizing the Jacobian work):
+ * out[34] = {P, sum s_p, sum s_p^2, sum_bins n_p*nk, sum_bins n_p*nk^2, bins,
+ * histogram of s_p over 1..27 at out[7..33]} (s_p = support nodes of
+ * particle p, nk = support box of its bin). */
+impm_status impm_sim_support_stats(impm_sim* sim, int64_t* out);
 /* p2g_map (mpm_solver.hpp:142-152) */
 impm_status impm_sim_p2g_map(impm_sim* sim, const double* per_particle, double* out /*[N]*/);
 

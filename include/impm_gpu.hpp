@@ -27,10 +27,8 @@
 #include "impm_gpu.h"
 
 #ifdef IMPM_GPU_REFERENCE_TYPES
-#include "impm/errors.hpp"
-#include "impm/grid.hpp"
-#include "impm/particle.hpp"
-#include "impm/sparse.hpp"
+// the reference's own value types (grid, particle, material, options, records)
+#include "impm/mpm_solver.hpp"
 #endif
 #include <span>
 
@@ -94,6 +92,34 @@ static_assert(sizeof(Particle<1>) == 232 && sizeof(Particle<2>) == 304 && sizeof
               "layout of impm::Particle<D>");
 #endif
 
+// GPU-only solver knobs (no counterpart in impm::SolverOptions); passed as
+// an optional extra constructor argument so that reference-typed callers keep
+// the reference constructor MpmSim(Grid, particles, MaterialSpec, SolverOptions)
+struct GpuOptions {
+  impm_krylov_kind krylov = IMPM_KRYLOV_AUTO;
+  impm_precond_kind precond = IMPM_PRECOND_MG;
+  double krylov_rtol = 1e-12;
+  int device = 0;
+};
+
+#ifdef IMPM_GPU_REFERENCE_TYPES
+// grid.hpp:18-58, materials.hpp:12-47, mpm_solver.hpp:21-46, jacobian.hpp:18-20
+template <int D>
+using Grid = impm::Grid<D>;
+using impm::DofMap;
+using impm::ElasticParams;
+using impm::InterferenceCheck;
+using impm::JacobianStrategy;
+using impm::MaterialKind;
+using impm::MaterialSpec;
+using impm::SolverOptions;
+using impm::StepRecord;
+template <int D>
+using NodeVec = impm::Vec<double, D>;
+#else
+template <int D>
+using NodeVec = std::array<double, D>;
+
 // impm::Grid<D> (grid.hpp:18-58)
 template <int D>
 struct Grid {
@@ -116,6 +142,8 @@ struct Grid {
 };
 
 enum class MaterialKind { hencky = IMPM_HENCKY, hencky_j2 = IMPM_HENCKY_J2, neo_hookean = IMPM_NEO_HOOKEAN };
+enum class JacobianStrategy { dense, sparse };          // jacobian.hpp:18
+enum class InterferenceCheck { off, sampled, always };  // jacobian.hpp:20
 
 struct ElasticParams {
   double E = 1.0, nu = 0.0;
@@ -127,17 +155,16 @@ struct MaterialSpec {  // mpm_solver.hpp:21-25
   double kappa = 0.0;
 };
 
-struct SolverOptions {  // mpm_solver.hpp:27-36 (+ GPU linear-solver knobs)
+struct SolverOptions {  // mpm_solver.hpp:27-36
   double tol = 1e-11;
   double abs_floor = 1e-14;
   int max_iterations = 20;
+  JacobianStrategy strategy = JacobianStrategy::sparse;
+  InterferenceCheck interference = InterferenceCheck::off;
   bool total_lagrangian = false;
-  impm_krylov_kind krylov = IMPM_KRYLOV_AUTO;
-  impm_precond_kind precond = IMPM_PRECOND_MG;
-  double krylov_rtol = 1e-12;
 };
 
-struct StepRecord {  // mpm_solver.hpp:38-46
+struct StepRecord {  // mpm_solver.hpp:38-46 (+ the Krylov count)
   int step = 0, iterations = 0;
   std::vector<double> rel_residuals;
   double r0_norm = 0.0, seconds = 0.0, diff_seconds = 0.0;
@@ -145,19 +172,19 @@ struct StepRecord {  // mpm_solver.hpp:38-46
   int krylov_iterations = 0;
 };
 
-#ifndef IMPM_GPU_REFERENCE_TYPES
 struct CsrMatrix {  // sparse.hpp:11-31 (fields only)
   int n = 0;
   std::vector<std::int64_t> row_ptr;
   std::vector<std::int32_t> cols;
   std::vector<double> vals;
 };
-#endif
+
 struct DofMap {  // grid.hpp:66-93
   int n_fields = 0, n_dofs = 0;
   std::vector<std::int32_t> dof_of, node_of, field_of;
   std::int32_t dof(int node, int field) const { return dof_of[static_cast<std::size_t>(node) * n_fields + field]; }
 };
+#endif
 
 namespace detail {
 inline void check(impm_status st, impm_sim* h) {
@@ -179,17 +206,34 @@ inline void check(impm_status st, impm_sim* h) {
     default: throw Error(msg);
   }
 }
-inline impm_options to_c(const SolverOptions& o) {
+inline impm_options to_c(const SolverOptions& o, const GpuOptions& gpu) {
   impm_options c{};
   c.tol = o.tol;
   c.abs_floor = o.abs_floor;
   c.max_iterations = o.max_iterations;
   c.total_lagrangian = o.total_lagrangian ? 1 : 0;
   c.shape = IMPM_SHAPE_GIMP;
-  c.krylov = o.krylov;
-  c.krylov_rtol = o.krylov_rtol;
-  c.precond = o.precond;
+  c.krylov = gpu.krylov;
+  c.krylov_rtol = gpu.krylov_rtol;
+  c.precond = gpu.precond;
+  c.strategy = o.strategy == JacobianStrategy::dense ? IMPM_STRATEGY_DENSE : IMPM_STRATEGY_SPARSE;
+  c.interference = o.interference == InterferenceCheck::always    ? IMPM_INTERFERENCE_ALWAYS
+                   : o.interference == InterferenceCheck::sampled ? IMPM_INTERFERENCE_SAMPLED
+                                                                  : IMPM_INTERFERENCE_OFF;
   return c;
+}
+inline impm_material to_c(const MaterialSpec& m) {
+  impm_material c{};
+  c.kind = static_cast<std::int32_t>(m.kind);  // same order as materials.hpp:47
+  c.E = m.elastic.E;
+  c.nu = m.elastic.nu;
+  c.kappa = m.kappa;
+  c.friction_deg = 30.0;
+  return c;
+}
+template <class R>
+inline void set_krylov(R& s, int v) {  // impm::StepRecord has no Krylov count
+  if constexpr (requires { s.krylov_iterations; }) s.krylov_iterations = v;
 }
 inline StepRecord from_c(const impm_step_record& r, const std::vector<double>& rel) {
   StepRecord s;
@@ -200,7 +244,7 @@ inline StepRecord from_c(const impm_step_record& r, const std::vector<double>& r
   s.seconds = r.seconds;
   s.diff_seconds = r.diff_seconds;
   s.backward_passes = r.backward_passes;
-  s.krylov_iterations = r.krylov_iterations;
+  set_krylov(s, r.krylov_iterations);
   return s;
 }
 }  // namespace detail
@@ -212,13 +256,16 @@ class MpmSim {
   Grid<D> grid;
   std::vector<Particle<D>> particles;
   MaterialSpec material;
-  std::array<double, D> gravity{};
+  NodeVec<D> gravity{};
   SolverOptions options;
   std::vector<std::uint8_t> fixed;  // [node * D + comp]
 
-  MpmSim(Grid<D> g, std::vector<Particle<D>> parts, MaterialSpec mat, SolverOptions opt = {}, int device = 0)
+  // mpm_solver.hpp:63-68 (+ optional GPU knobs)
+  MpmSim(Grid<D> g, std::vector<Particle<D>> parts, MaterialSpec mat, SolverOptions opt = {}, GpuOptions gpu = {})
       : grid(g), particles(std::move(parts)), material(mat), options(opt) {
     fixed.assign(static_cast<std::size_t>(grid.node_count()) * D, 0);
+    if (options.total_lagrangian && mat.kind == MaterialKind::hencky_j2)  // mpm_solver.hpp:66-67
+      throw ConfigError("total-Lagrangian stepping supports elastic materials only");
     impm_grid cg{};
     cg.dim = D;
     for (int a = 0; a < 3; ++a) {
@@ -226,15 +273,36 @@ class MpmSim {
       cg.origin[a] = a < D ? grid.origin[a] : 0.0;
     }
     cg.h = grid.h;
-    impm_material cm{static_cast<std::int32_t>(mat.kind), 0, mat.elastic.E, mat.elastic.nu, mat.kappa, 30.0, 0.0};
-    const impm_options co = detail::to_c(options);
-    detail::check(impm_sim_create(&cg, &cm, &co, device, &h_), nullptr);
+    const impm_material cm = detail::to_c(mat);
+    const impm_options co = detail::to_c(options, gpu);
+    detail::check(impm_sim_create(&cg, &cm, &co, gpu.device, &h_), nullptr);
   }
   ~MpmSim() {
     if (h_) impm_sim_destroy(h_);
   }
   MpmSim(const MpmSim&) = delete;
   MpmSim& operator=(const MpmSim&) = delete;
+  // movable, so that builders return it by value (src/scenarios.cpp:92-106)
+  MpmSim(MpmSim&& o) noexcept
+      : grid(o.grid), particles(std::move(o.particles)), material(o.material), gravity(o.gravity),
+        options(o.options), fixed(std::move(o.fixed)), h_(o.h_), shadow_(std::move(o.shadow_)) {
+    o.h_ = nullptr;
+  }
+  MpmSim& operator=(MpmSim&& o) noexcept {
+    if (this != &o) {
+      if (h_) impm_sim_destroy(h_);
+      grid = o.grid;
+      particles = std::move(o.particles);
+      material = o.material;
+      gravity = o.gravity;
+      options = o.options;
+      fixed = std::move(o.fixed);
+      h_ = o.h_;
+      shadow_ = std::move(o.shadow_);
+      o.h_ = nullptr;
+    }
+    return *this;
+  }
 
   template <class Pred>
   void fix_nodes(Pred&& predicate, int component = -1) {  // mpm_solver.hpp:70-78

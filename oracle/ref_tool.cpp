@@ -195,20 +195,24 @@ MpmSim<D> build(const Spec& s) {
   const double t_hat = s.num("t_hat", 0.0);
   if (t_hat != 0.0) {
     const double frac = s.num("strip_fraction", 0.25);
+    // strip_axes = number of leading lateral axes the strip is narrow in
+    // (default all D-1: a centred patch; 1: a strip along axis 0 only, the
+    // cfg 4 footing of paper_2507_09435_b200/workloads.py:_strip_traction)
+    const int narrow = static_cast<int>(s.num("strip_axes", D - 1));
     double top = -1e300;
     for (const auto& p : sim.particles) top = std::max(top, p.X[D - 1]);
     std::vector<std::size_t> strip;
     for (std::size_t pi = 0; pi < sim.particles.size(); ++pi) {
       const auto& p = sim.particles[pi];
       bool in = p.X[D - 1] >= top - 1e-9;
-      for (int a = 0; a < D - 1 && in; ++a) {
+      for (int a = 0; a < narrow && in; ++a) {
         const double w = cells[a] * h;
         in = p.X[a] >= 0.5 * w * (1 - frac) && p.X[a] <= 0.5 * w * (1 + frac);
       }
       if (in) strip.push_back(pi);
     }
     double area = 1.0;
-    for (int a = 0; a < D - 1; ++a) area *= cells[a] * h * frac;
+    for (int a = 0; a < D - 1; ++a) area *= cells[a] * h * (a < narrow ? frac : 1.0);
     for (std::size_t pi : strip)
       sim.particles[pi].traction_force[D - 1] = -t_hat * area / strip.size();
   }
@@ -283,6 +287,31 @@ void dump_case(const Spec& s, const std::string& dir) {
     write_vec(dir, "J1_vals", J.vals);
     std::vector<std::int32_t> passes{st.total_passes, st.passes_per_field};
     write_vec(dir, "passes", passes);
+    // colour groups (jacobian.hpp:101-110), observed through the reference's
+    // own sparse(): on a probe tape r_i = w_i * sum_j u_j (generic weights
+    // w_i), every entry of seeded row d equals the sum of w over d's group,
+    // so two dofs share a group iff their rows hold the same value
+    {
+      ad::Tape probe_tape;
+      std::vector<ad::Var> in;
+      in.reserve(n);
+      for (int d = 0; d < n; ++d) in.push_back(probe_tape.input(0.0));
+      ad::Var sum = in.empty() ? ad::Var() : in[0];
+      for (int d = 1; d < n; ++d) sum = sum + in[d];
+      std::mt19937 wr(2507);
+      std::uniform_real_distribution<double> W(1.0, 2.0);
+      std::vector<ad::Var> outs;
+      outs.reserve(n);
+      for (int d = 0; d < n; ++d) outs.push_back(sum * W(wr));
+      probe_tape.set_outputs(outs);
+      JacobianStats pst;
+      const CsrMatrix G = sim.assembler().sparse(probe_tape, &pst);
+      std::vector<double> colour_probe(n);
+      for (int d = 0; d < n; ++d) colour_probe[d] = G.vals[G.row_ptr[d]];
+      write_vec(dir, "colour_probe", colour_probe);
+      std::vector<std::int32_t> cpasses{pst.total_passes, pst.passes_per_field};
+      write_vec(dir, "colour_passes", cpasses);
+    }
     // the linear solve at the probe (the seam sparse_lu_solve replaces)
     std::vector<double> r1 = sim.residual(u1, s0), rhs(n);
     for (int i = 0; i < n; ++i) rhs[i] = -r1[i];

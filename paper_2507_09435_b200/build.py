@@ -55,5 +55,27 @@ def build(force=False, verbose=False):
     return OUT
 
 
+REF_INCLUDE = "/root/reference/proj/include"
+BAR_SWAP = os.path.join(os.path.dirname(HERE), "tests", "_build", "bar_swap")
+
+
+def build_bar_swap(force=False):
+    """tests/cpp/bar_swap.cpp: the reference's bar scenario with impm_gpu::MpmSim
+    swapped in, compiled against the reference's own headers (only where
+    /root/reference exists; the binary travels to the GPU box in-tree)."""
+    src = os.path.join(os.path.dirname(HERE), "tests", "cpp", "bar_swap.cpp")
+    hdr = os.path.join(os.path.dirname(HERE), "include", "impm_gpu.hpp")
+    if not os.path.isdir(REF_INCLUDE):
+        return BAR_SWAP if os.path.exists(BAR_SWAP) else None
+    if not force and os.path.exists(BAR_SWAP) and all(
+            os.path.getmtime(f) <= os.path.getmtime(BAR_SWAP) for f in (src, hdr, OUT)):
+        return BAR_SWAP
+    os.makedirs(os.path.dirname(BAR_SWAP), exist_ok=True)
+    subprocess.run(["g++", "-std=c++20", "-O2", "-I", os.path.join(os.path.dirname(HERE), "include"),
+                    "-I", REF_INCLUDE, "-o", BAR_SWAP, src, "-L", HERE, "-limpm_gpu",
+                    "-Wl,-rpath,$ORIGIN/../../paper_2507_09435_b200"], check=True)
+    return BAR_SWAP
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose=True)

@@ -318,6 +318,22 @@ struct DevCsr {
     }
   }
 
+  // device-resident CSR (already validated by construction): device-to-device copies
+  void upload_device(int n_, const int64_t* row_ptr, const int32_t* cols, const double* vals, int64_t nnz_,
+                     cudaStream_t st) {
+    n = n_;
+    s = st;
+    nnz = nnz_;
+    rp.ensure(n + 1);
+    ci.ensure(std::max<int64_t>(nnz, 1));
+    v.ensure(std::max<int64_t>(nnz, 1));
+    CK(cudaMemcpyAsync(rp.get(), row_ptr, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+    if (nnz) {
+      CK(cudaMemcpyAsync(ci.get(), cols, nnz * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+      CK(cudaMemcpyAsync(v.get(), vals, nnz * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    }
+  }
+
   template <int MODE>
   void spmv(const double* x, double* y, const double* b = nullptr, const double* scale = nullptr) const {
     if (n == 0) return;
@@ -469,8 +485,14 @@ struct LuSolver {
     }
   }
 
-  // sparse_lu_solve (src/linear_solver.cpp:11-88)
-  void solve(const double* bh, double* xh) {
+  // sparse_lu_solve (src/linear_solver.cpp:11-88); host right-hand side and solution
+  void solve(const double* bh, double* xh) { solve_io(bh, cudaMemcpyHostToDevice, xh, cudaMemcpyDeviceToHost); }
+  // the same on device vectors (the direct path of the GPU Newton solve)
+  void solve_device(const double* bd, double* xd) {
+    solve_io(bd, cudaMemcpyDeviceToDevice, xd, cudaMemcpyDeviceToDevice);
+  }
+
+  void solve_io(const double* bh, cudaMemcpyKind kin, double* xh, cudaMemcpyKind kout) {
     const int n = A.n;
     const cudaStream_t s = A.s;
     red.s = s;
@@ -481,7 +503,7 @@ struct LuSolver {
     flags.ensure(2);
     const int init[2] = {INT_MAX, -1};
     CK(cudaMemcpyAsync(flags.get(), init, sizeof(init), cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(b.get(), bh, n * sizeof(double), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(b.get(), bh, n * sizeof(double), kin, s));
     CSR_LAUNCH((k_csr_row_stats<<<grid_rows_warp(n), 256, 0, s>>>(n, A.rp.get(), A.v.get(), scale.get(), rabs.get(),
                                                                    flags.get(), diag.get(), A.ci.get())));
     int empty = INT_MAX;
@@ -518,7 +540,7 @@ struct LuSolver {
                                                    " exceeds 1e-10; matrix is ill-conditioned or singular");
       }
     }
-    CK(cudaMemcpyAsync(xh, x.get(), n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(xh, x.get(), n * sizeof(double), kout, s));
     CK(cudaStreamSynchronize(s));
   }
 };

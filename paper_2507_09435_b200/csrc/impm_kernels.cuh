@@ -129,6 +129,7 @@ struct DevStatus {
   int perm_moved;     // counting sort moved at least one particle
   int err_lp;         // commit: min original id with lp >= h/2 or <= 0
   int err_migrate;    // slab migration: min original id that left the neighbour slabs
+  int err_seed;       // min (orig*4 + axis) whose support exceeds the 3-node stencil (seeding hazard)
 };
 
 template <int D, int SHAPE>
@@ -161,7 +162,14 @@ __global__ void k_support(const double* __restrict__ pd, int64_t cap, int P, Gri
     }
     if (SHAPE != 2 && (!(lp > 0.0) || lp >= 0.5 * g.h)) atomicMin(&st->err_cfg, orig[i]);  // gimp.cpp:28-30
     if (count < 1) count = 1;
-    if (count > 3) count = 3;
+    // a support wider than 3 nodes would couple nodes beyond the +-2 pattern
+    // (b = 5, gimp.cpp:7-15) and break the colour/owner separation of the
+    // assembly: the GPU form of the reference's seeding hazard
+    // (jacobian.hpp:167-182), reported as SeedingFault when checked
+    if (count > 3) {
+      atomicMin(&st->err_seed, orig[i] * 4 + a);
+      count = 3;
+    }
     if (first < 0) first = 0;
     if (first + count > g.nodes[a]) first = g.nodes[a] - count;
     k += first * g.stride[a];
@@ -900,6 +908,111 @@ __global__ void k_tangent(GridC g, const double* __restrict__ pd, int64_t cap, i
   }
 }
 
+// Analytic neo-Hookean tangent (3D), the closed form of what k_tangent's
+// dual numbers compute on the same expression graph: with f = I + G,
+// F = f F_n (updated Lagrangian; F = f total Lagrangian), b = F F^T,
+// tau = mu (b - I) + lam ln J I (neo_hookean_update, materials.hpp:139-158)
+// and P = V sigma f^-T = V0 tau f^-T (mpm_solver.hpp:187-198),
+//   dP_cb/dG_df = V0 [ mu d_cd (Fi b Fi^T)_fb + mu (Fi b)_fc Fi_bd
+//                      + lam Fi_fd Fi_bc - Fi_bd (tau Fi^T)_cf ],  Fi = f^-1.
+// ~900 flops per particle instead of nine dual-number passes of the stress
+// update; A is written through a per-warp transpose in contiguous 216-byte
+// runs (one output direction d at a time), same layout as k_tangent.
+template <int SHAPE>
+__global__ void __launch_bounds__(128) k_tangent_nh3(GridC g, const double* __restrict__ pd, int64_t cap, int P,
+                                                     const double* __restrict__ xs, const int* __restrict__ key,
+                                                     const int* __restrict__ sup, const double* __restrict__ u,
+                                                     MatParams mp, int tl, double* __restrict__ A) {
+  constexpr int D = 3;
+  __shared__ double tb[4][32][28];  // [warp][particle][27 values of one direction d] (+1 pad)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int p0 = (blockIdx.x * 4 + warp) * 32;
+  const int p = p0 + lane;
+  const bool live = p < P;
+  double Fi[9] = {}, Y[9] = {}, X[9] = {}, Z[9] = {}, V0 = 0.0;
+  const double lam = mp.lam, mu = mp.mu;
+  bool ok = false;
+  if (live) {
+    int first[3], cnt[3];
+    AxisW aw[3];
+    particle_weights<D, SHAPE>(g, pd, cap, xs, p, key[p], sup[p], first, cnt, aw);
+    Mat<double, D> G = Mat<double, D>::zero();
+    for_each_support<D>(g, first, cnt, aw, [&](int node, double, const double* grad) {
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        const double uc = u[node * D + c];
+#pragma unroll
+        for (int a = 0; a < D; ++a) G(c, a) += uc * grad[a];
+      }
+    });
+    Mat<double, D> f = G;
+#pragma unroll
+    for (int a = 0; a < D; ++a) f(a, a) += 1.0;
+    Mat<double, D> F = f;
+    if (!tl) {
+      Mat<double, D> Fn;
+#pragma unroll
+      for (int i = 0; i < 9; ++i) Fn.e[i] = pd[(PF<D>::F + i) * cap + p];
+      F = matmul(f, Fn);
+    }
+    const double J = det(F);
+    V0 = pd[PF<D>::V0 * cap + p];
+    if (J > 0.0) {
+      ok = true;
+      const Mat<double, D> fi = inverse(f);
+      const Mat<double, D> b = matmul(F, transpose(F));
+      const double lnJ = log(J);
+#pragma unroll
+      for (int i = 0; i < 9; ++i) Fi[i] = fi.e[i];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          double x = 0.0;
+#pragma unroll
+          for (int a = 0; a < 3; ++a) x += fi(i, a) * b(a, j);
+          X[i * 3 + j] = x;  // (Fi b)_ij
+        }
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          double y = 0.0, z = 0.0;
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            y += X[i * 3 + a] * fi(j, a);  // (Fi b Fi^T)_ij
+            const double tau = mu * (b(i, a) - (i == a ? 1.0 : 0.0)) + (i == a ? lam * lnJ : 0.0);
+            z += tau * fi(j, a);  // (tau Fi^T)_ij
+          }
+          Y[i * 3 + j] = y;
+          Z[i * 3 + j] = z;
+        }
+    }
+  }
+  double* tw = &tb[warp][0][0];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    // this lane's particle: the 27 values of direction d, index (f, c, b)
+#pragma unroll
+    for (int f = 0; f < 3; ++f)
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int bb = 0; bb < 3; ++bb) {
+          double v = 0.0;
+          if (ok)
+            v = V0 * ((c == d ? mu * Y[f * 3 + bb] : 0.0) + mu * X[f * 3 + c] * Fi[bb * 3 + d] +
+                      lam * Fi[f * 3 + d] * Fi[bb * 3 + c] - Fi[bb * 3 + d] * Z[c * 3 + f]);
+          tw[lane * 28 + f * 9 + c * 3 + bb] = v;
+        }
+    __syncwarp();
+    // write the warp's 32 particles, 27 contiguous doubles each (df = d*3 + f)
+    for (int q = 0; q < 32 && p0 + q < P; ++q)
+      if (lane < 27) A[static_cast<int64_t>(p0 + q) * 81 + d * 27 + lane] = tw[q * 28 + lane];
+    __syncwarp();
+  }
+}
+
 // ------------------------------------------- K6 Jacobian: structure ------
 // Per bin (= first support node): bit a set when some particle of the bin
 // has a 3-node support on axis a; bit 7 = bin non-empty.
@@ -1172,8 +1285,24 @@ __global__ void __launch_bounds__(WARPS * 32) k_assemble_bins(
 // A bin with at most PCH particles (the common case: PCH = 8 = ppc^3 in 3D) is
 // staged once and stays resident across all of its task rounds; larger bins
 // restage per round and chunk.
-template <int D, int SHAPE, int PPL, int WARPS, int PCH, bool SYM = false>
-__global__ void __launch_bounds__(WARPS * 32, D == 3 ? 4 : 1) k_assemble_bins_staged(
+// RMW: flush through a per-warp shared-memory transpose and plain coalesced
+// read-modify-writes instead of per-lane RED.ADD.F64 (exclusive per colour, so
+// no atomics are needed; same one add per block per colour, bitwise the same
+// sums). A RED costs ~1.3 LSU cycles per lane; a transposed RMW moves the
+// 27 values of one task with one load and one store instruction.
+template <int PPL, int DD>
+struct AsmFlush {
+  static constexpr int NV = PPL * DD;
+  double F[32][NV];
+  long long DB[32][PPL], MB[32][PPL];
+  int DCP[32], MCP[32][PPL];
+};
+
+// MIRROR (SYM only): add K_kl^T into row l inside the kernel (RED); false:
+// only the upper blocks (flat(l) >= flat(k)) are formed and k_mirror_lower
+// copies the transposes once after the last colour (half the reductions)
+template <int D, int SHAPE, int PPL, int WARPS, int PCH, bool SYM = false, bool RMW = false, bool MIRROR = true>
+__global__ void __launch_bounds__(WARPS * 32, D == 3 ? (RMW ? 2 : 4) : 1) k_assemble_bins_staged(
     GridC g, const double* __restrict__ pd, int64_t cap, const double* __restrict__ xs,
     const int* __restrict__ bin_start, const uint8_t* __restrict__ bflag, const double* __restrict__ A,
     const int* __restrict__ act_idx, const unsigned* __restrict__ row_mask, const int* __restrict__ row_nzb,
@@ -1191,6 +1320,9 @@ __global__ void __launch_bounds__(WARPS * 32, D == 3 ? 4 : 1) k_assemble_bins_st
   __shared__ int Rcp[WARPS][NK];
   __shared__ uint4 Rmask[WARPS][NK];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  extern __shared__ __align__(16) unsigned char asm_dyn[];
+  using FL = AsmFlush<PPL, DD>;
+  FL& fls = reinterpret_cast<FL*>(asm_dyn)[RMW ? warp : 0];
   const int nbins = nb0 * nb1 * nb2;
   const int col[3] = {c0, c1, c2};
   const int nbv[3] = {nb0, nb1, nb2};
@@ -1379,6 +1511,77 @@ __global__ void __launch_bounds__(WARPS * 32, D == 3 ? 4 : 1) k_assemble_bins_st
           }
         }
       }
+      if constexpr (RMW) {
+        // publish the task's blocks (values + element offsets) to the warp's
+        // transpose buffer, then move them with coalesced RMWs
+#pragma unroll
+        for (int t = 0; t < PPL; ++t) {
+          long long db = -1, mb = -1;
+          int mcp = 0;
+          const int l = tl0 + t;
+          if (has_task && l < nk) {
+            int ll[3] = {0, 0, 0}, rl = l, sl = 0, slm = 0;
+#pragma unroll
+            for (int a = D - 1; a >= 0; --a) {
+              ll[a] = rl % cn[a];
+              rl /= cn[a];
+            }
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+              sl = sl * 5 + (ll[a] - lk[a] + 2);
+              slm = slm * 5 + (lk[a] - ll[a] + 2);
+            }
+            if (row >= 0) db = static_cast<long long>(row) * row_len + mask_pos_r(rm, sl) * D;
+            if constexpr (SYM) {
+              const int rowl = Rrow[warp][l];
+              if (l != tk && rowl >= 0) {
+                const uint4 m4 = Rmask[warp][l];
+                const unsigned ml[4] = {m4.x, m4.y, m4.z, m4.w};
+                mb = static_cast<long long>(rowl) * row_len + mask_pos_r(ml, slm) * D;
+                mcp = Rcp[warp][l];
+              }
+            }
+          }
+          fls.DB[lane][t] = db;
+          fls.MB[lane][t] = mb;
+          fls.MCP[lane][t] = mcp;
+#pragma unroll
+          for (int e = 0; e < DD; ++e) fls.F[lane][t * DD + e] = acc[t][e];
+        }
+        fls.DCP[lane] = cp;
+        __syncwarp();
+        const int tq = lane / DD, cq = (lane % DD) / D, dq = lane % D;
+        const bool vl = lane < FL::NV;
+        const int ntr = min(32, ntasks - r0);
+        for (int i0 = 0; i0 < ntr; i0 += 4) {
+          long long oa[4], ma[4];
+          double ov[4], mv[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int i = i0 + q;
+            oa[q] = -1;
+            ma[q] = -1;
+            if (vl && i < ntr) {
+              const long long db = fls.DB[i][tq];
+              if (db >= 0) oa[q] = db + static_cast<long long>(cq) * fls.DCP[i] + dq;
+              if constexpr (SYM) {
+                const long long mb = fls.MB[i][tq];
+                if (mb >= 0) ma[q] = mb + static_cast<long long>(cq) * fls.MCP[i][tq] + dq;
+              }
+            }
+            ov[q] = oa[q] >= 0 ? __ldcg(vals + oa[q]) : 0.0;
+            mv[q] = ma[q] >= 0 ? __ldcg(vals + ma[q]) : 0.0;
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int i = i0 + q;
+            if (oa[q] >= 0) __stcg(vals + oa[q], ov[q] + fls.F[i][tq * DD + cq * D + dq]);
+            if (ma[q] >= 0) __stcg(vals + ma[q], mv[q] + fls.F[i][tq * DD + dq * D + cq]);
+          }
+        }
+        __syncwarp();
+        continue;
+      }
       if (has_task) {
         if (row >= 0) {
           double* rbase = vals + static_cast<int64_t>(row) * row_len;
@@ -1405,7 +1608,7 @@ __global__ void __launch_bounds__(WARPS * 32, D == 3 ? 4 : 1) k_assemble_bins_st
               for (int d = 0; d < D; ++d) atomicAdd(rv + c * cp + d, acc[t][c * D + d]);
           }
         }
-        if constexpr (SYM) {
+        if constexpr (SYM && MIRROR) {
           // mirrored blocks: row l, column k, K_lk = K_kl^T
 #pragma unroll
           for (int t = 0; t < PPL; ++t) {
@@ -1437,6 +1640,50 @@ __global__ void __launch_bounds__(WARPS * 32, D == 3 ? 4 : 1) k_assemble_bins_st
         }
       }
     }
+  }
+}
+
+// Lower blocks of a symmetric J from the upper ones (the assembly ran with
+// MIRROR = false): K_ab = K_ba^T for flat(b) < flat(a). One warp per row, a
+// lane per value; stored slots are ascending, so the lower ones come first.
+// A column node that is not a row (no DOF) gets a zero block.
+template <int D>
+__global__ void k_mirror_lower(GridC g, int n_act, const int* __restrict__ act_list, const int* __restrict__ act_idx,
+                               const int* __restrict__ row_nzb, const uint8_t* __restrict__ row_slots,
+                               const unsigned* __restrict__ row_mask, double* __restrict__ vals, int64_t row_len) {
+  constexpr int S = ipow_c(5, D);
+  constexpr int DD = D * D;
+  constexpr int center = (S - 1) / 2;  // slot of delta = 0
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (row >= n_act) return;
+  const int node = act_list[row];
+  const int nzb = row_nzb[row], cp = cpad(nzb, D);
+  const uint8_t* sl = row_slots + static_cast<int64_t>(row) * S;
+  double* out = vals + static_cast<int64_t>(row) * row_len;
+  for (int e = lane; e < nzb * DD; e += 32) {
+    const int pos = e / DD, cd = e - pos * DD, c = cd / D, d = cd - c * D;
+    const int slot = sl[pos];
+    if (slot >= center) break;
+    int r = slot, off = 0;
+#pragma unroll
+    for (int a = D - 1; a >= 0; --a) {
+      off += (r % 5 - 2) * g.stride[a];
+      r /= 5;
+    }
+    const int rb = act_idx[node + off];
+    double v = 0.0;
+    if (rb >= 0) {
+      const int ms = S - 1 - slot;  // the slot of -delta in row b
+      const unsigned* m = row_mask + static_cast<int64_t>(rb) * 4;
+      const int w = ms >> 5;
+      int pb = 0;
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+        if (k < w) pb += __popc(m[k]);
+      pb += __popc(m[w] & ((1u << (ms & 31)) - 1u));
+      v = vals[static_cast<int64_t>(rb) * row_len + d * cpad(row_nzb[rb], D) + pb * D + c];
+    }
+    out[c * cp + pos * D + d] = v;
   }
 }
 

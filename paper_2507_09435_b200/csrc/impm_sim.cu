@@ -140,6 +140,14 @@ struct Prof {
 };
 
 // ---------------------------------------------------------- multigrid ---
+}  // namespace
+
+// device CSR linear algebra (the sparse_lu_solve seam), also the direct path of
+// the Newton solve on small systems
+#include "impm_csr.cuh"
+
+namespace {
+
 struct MgLevel {
   GridC g{};
   int n_act = 0;
@@ -256,7 +264,21 @@ struct Sim {
   // (default 3; a solve on stale levels that fails or overruns 4x the last
   // iteration count is retried once on a freshly built hierarchy)
   int mg_refresh = std::getenv("IMPM_MG_REFRESH") ? std::atoi(std::getenv("IMPM_MG_REFRESH")) : 3;
-  bool mg_stale = false;
+  double exact_rtol = 1e-13;         // Krylov target of an exact-equivalent Newton step
+  int exact_newton_env = -1;         // IMPM_EXACT_NEWTON: -1 = by material
+  bool exact_newton = false;         // set per material at create / set_material
+  bool mg_cross_ok = false;  // set by cg_mg_solve around its capped solve on stale levels
+  // assembly flush: per-lane RED.ADD.F64 (default) or the transposed plain RMW
+  // (IMPM_ASM_RMW=1: 40 vs 34 ms per cfg 4 Jacobian);
+  // symmetric mirroring for symmetric J (IMPM_ASM_SYM=0: full)
+  // 3D neo-Hookean tangent in closed form (IMPM_TANGENT_DUAL=1: dual numbers)
+  bool tangent_analytic = !(std::getenv("IMPM_TANGENT_DUAL") && std::atoi(std::getenv("IMPM_TANGENT_DUAL")) != 0);
+  bool asm_rmw = std::getenv("IMPM_ASM_RMW") && std::atoi(std::getenv("IMPM_ASM_RMW")) != 0;
+  bool asm_sym = !(std::getenv("IMPM_ASM_SYM") && std::atoi(std::getenv("IMPM_ASM_SYM")) == 0);
+  // symmetric J: upper blocks in the colour launches, lower ones by one
+  // transpose pass (IMPM_ASM_MIRROR_PASS=0: mirrored REDs in the kernel). A
+  // slab's halo nodes are not rows, so slabs keep the in-kernel mirror.
+  bool mirror_pass_env = !(std::getenv("IMPM_ASM_MIRROR_PASS") && std::atoi(std::getenv("IMPM_ASM_MIRROR_PASS")) == 0);
   int last_cg_iters = 0;
   int mg_f16sim = std::getenv("IMPM_MG_F16SIM") ? std::atoi(std::getenv("IMPM_MG_F16SIM")) : 0;  // A/B experiment
   // fine-level smoother matrix in fp16 with fp32 row scales (IMPM_MG_F16=0: fp32)
@@ -421,6 +443,8 @@ struct Sim {
     if (const char* e = std::getenv("IMPM_MG_F64")) mg_f32 = std::atoi(e) == 0;  // A/B experiments only
     if (const char* e = std::getenv("IMPM_MG_REUSE")) mg_reuse = std::atoi(e) != 0;
     if (const char* e = std::getenv("IMPM_ETA0_FACTOR")) newton_eta_factor = std::atof(e);  // A/B experiments
+    if (const char* e = std::getenv("IMPM_EXACT_RTOL")) exact_rtol = std::atof(e);       // A/B experiments
+    if (const char* e = std::getenv("IMPM_EXACT_NEWTON")) exact_newton_env = std::atoi(e);  // A/B experiments
     if (const char* e = std::getenv("IMPM_MG_SMOOTH")) mg_smooth_env = std::atoi(e);
     if (const char* e = std::getenv("IMPM_TANGENT_K1")) tangent_k1 = std::atoi(e) != 0;
     if (const char* e = std::getenv("IMPM_SPMV_BLOCKS"))  // tuning experiments only
@@ -478,6 +502,7 @@ struct Sim {
     z.err_ood = INT_MAX;
     z.err_cfg = INT_MAX;
     z.err_lp = INT_MAX;
+    z.err_seed = INT_MAX;
     z.max_mass = 0.0;
     *h_st = z;
     CK(cudaMemcpyAsync(st.p, h_st, sizeof(DevStatus), cudaMemcpyHostToDevice, s));
@@ -769,6 +794,7 @@ struct Sim {
   }
 
   void begin_step() {
+    ref_nnz_cache = -1;  // the pattern follows this step's DOF map
     if ((opt.total_lagrangian || coupled) && step_built) return;  // mpm_solver.hpp:94, porous.cpp:92
     const int N = g.N;
     reset_status();
@@ -806,6 +832,14 @@ struct Sim {
     if (h_st->err_ood != INT_MAX) throw SimError(IMPM_ERR_OUT_OF_DOMAIN, ood_message(h_st->err_ood));
     if (h_st->err_cfg != INT_MAX)
       throw SimError(IMPM_ERR_CONFIG, "GIMP requires 0 < lp < h/2 (particle " + std::to_string(h_st->err_cfg) + ")");
+    // SolverOptions::interference (mpm_solver.hpp:31, jacobian.hpp:126-128):
+    // the supports fix every Jacobian of the step, so the check runs here
+    if (opt.interference != IMPM_INTERFERENCE_OFF && h_st->err_seed != INT_MAX) {
+      const int pid = h_st->err_seed / 4, ax = h_st->err_seed % 4;
+      throw SimError(IMPM_ERR_SEEDING, "backward pass touched a dof outside every seeded pattern of its group "
+                                       "(particle " + std::to_string(pid) + " spans more than 3 nodes on axis " +
+                                       std::to_string(ax) + ")");
+    }
     {
       Prof::Scope ps(&prof, kcSort);
       // counting sort by first support node (K1)
@@ -1016,7 +1050,10 @@ struct Sim {
         constexpr int K = DD == 3 ? 3 : DD * DD;
         // plastic kinds (one return map per pass) take K = 3 directions per pass in 3D
         const bool nho = mp.kind == kNeoHookean;
-        if (DD == 3 && tangent_k1 && nho)
+        if (DD == 3 && nho && tangent_analytic)
+          k_tangent_nh3<SH><<<blocks_for(P, 128), 128, 0, s>>>(g, pd.p, cap, P, xs.p, key.p, sup.p, ud, mp,
+                                                               opt.total_lagrangian, Atan.p);
+        else if (DD == 3 && tangent_k1 && nho)
           k_tangent<DD, SH, 1, true><<<blocks_for(P, 128), 128, 0, s>>>(g, pd.p, cap, P, xs.p, key.p, sup.p, ud, mp,
                                                                         opt.total_lagrangian, Atan.p);
         else if (nho)
@@ -1052,15 +1089,35 @@ struct Sim {
           // J is symmetric except under non-associative Drucker-Prager flow and
           // Cam-Clay (associative, but its compaction hardening breaks major
           // symmetry of dP/dG: ~2% in tests/test_math_cpu.py terms)
-          if (mat.kind != kDruckerPrager && mat.kind != kCamClay)
-            k_assemble_bins_staged<DD, SH, (DD == 3 ? asm_ppl3 : PPL), WS, PCH, true><<<grid, WS * 32, 0, s>>>(
-                g, pd.p, cap, xs.p, bin_start.p, bflag.p, Atan.p, act_idx.p, row_mask.p, row_nzb.p, vals.p, row_len,
-                cc[0], cc[1], cc[2], nb[0], nb[1], nb[2]);
-          else
-            k_assemble_bins_staged<DD, SH, (DD == 3 ? asm_ppl3 : PPL), WS, PCH, false><<<grid, WS * 32, 0, s>>>(
-                g, pd.p, cap, xs.p, bin_start.p, bflag.p, Atan.p, act_idx.p, row_mask.p, row_nzb.p, vals.p, row_len,
-                cc[0], cc[1], cc[2], nb[0], nb[1], nb[2]);
+          constexpr int PP = DD == 3 ? asm_ppl3 : PPL;
+          const bool sym = asm_sym && mat.kind != kDruckerPrager && mat.kind != kCamClay;
+          const bool mirror_pass = mirror_pass_env && !multi();
+          auto launch = [&](auto kern, bool rmw) {
+            const size_t dyn = rmw ? WS * sizeof(AsmFlush<PP, DD * DD>) : 0;
+            if (rmw) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)));
+            kern<<<grid, WS * 32, dyn, s>>>(g, pd.p, cap, xs.p, bin_start.p, bflag.p, Atan.p, act_idx.p, row_mask.p,
+                                            row_nzb.p, vals.p, row_len, cc[0], cc[1], cc[2], nb[0], nb[1], nb[2]);
+          };
+          if (asm_rmw) {
+            if (sym)
+              launch(k_assemble_bins_staged<DD, SH, PP, WS, PCH, true, true>, true);
+            else
+              launch(k_assemble_bins_staged<DD, SH, PP, WS, PCH, false, true>, true);
+          } else if (sym && mirror_pass) {
+            launch(k_assemble_bins_staged<DD, SH, PP, WS, PCH, true, false, false>, false);
+          } else if (sym) {
+            launch(k_assemble_bins_staged<DD, SH, PP, WS, PCH, true, false>, false);
+          } else {
+            launch(k_assemble_bins_staged<DD, SH, PP, WS, PCH, false, false>, false);
+          }
           ++g_launches;
+        }
+        if (asm_sym && mirror_pass_env && !multi() && !asm_rmw && mat.kind != kDruckerPrager &&
+            mat.kind != kCamClay) {
+          k_mirror_lower<DD><<<blocks_for(static_cast<int64_t>(n_act) * 32), kThreads, 0, s>>>(
+              g, n_act, act_list.p, act_idx.p, row_nzb.p, row_slots.p, row_mask.p, vals.p, row_len);
+          ++g_launches;
+          CKL();
         }
         k_diag_inverse<DD><<<blocks_for(n_act), kThreads, 0, s>>>(n_act, act_list.p, freem.p, row_mask.p, row_nzb.p,
                                                                    vals.p, row_len, dinv.p); ++g_launches;
@@ -1262,12 +1319,28 @@ struct Sim {
     // coarse levels of an earlier load step (mg_refresh > 1): the fine level
     // is re-pointed at the current J and row structure; the stale Galerkin
     // levels stay a fixed SPD preconditioner (R = P^T under the same masks)
-    const bool cross_step = mg_refresh > 1 && !slab && !coupled && mg_setup_step >= 0 &&
-                            mg_setup_step != step_counter && step_counter - mg_setup_step < mg_refresh &&
-                            !mg.empty() && (!mg_f16 || !mg[0]->vals16 || true);
-    mg_stale = cross_step;
+    // Only the CG path reuses across load steps: it alone caps the solve on
+    // stale levels and rebuilds on failure (cg_mg_solve); GMRES / BiCGStab
+    // always build the hierarchy of the current step.
+    const bool cross_step = mg_cross_ok && mg_reuse && mg_refresh > 1 && !slab && !coupled &&
+                            mg_setup_step >= 0 && mg_setup_step != step_counter &&
+                            step_counter - mg_setup_step < mg_refresh && !mg.empty();
     if (cross_step) {
       MgLevel& L0 = *mg[0];
+      // the fine row set changed since the levels were built: clear every
+      // level-0 vector so that k_restrict (which reads the fine residual at
+      // every grid node) sees zeros at nodes outside the current active set;
+      // otherwise stale entries make the V-cycle affine and break PCG
+      {
+        const int64_t n0 = static_cast<int64_t>(L0.g.N) * FE;
+        for (auto* v : {&L0.xa, &L0.xb, &L0.r, &L0.bvec}) CK(cudaMemsetAsync(v->p, 0, sizeof(double) * n0, s));
+        if (FE <= 4) {
+          CK(cudaMemsetAsync(L0.x4a.p, 0, sizeof(float) * L0.g.N * 4, s));
+          CK(cudaMemsetAsync(L0.x4b.p, 0, sizeof(float) * L0.g.N * 4, s));
+        }
+        L0.x = L0.xa.p;
+        L0.t = L0.xb.p;
+      }
       L0.n_act = n_act;
       L0.row_len = row_len;
       L0.act_idx = act_idx.p;
@@ -1643,17 +1716,20 @@ struct Sim {
   template <int DD, int FE>
   int cg_mg_solve(const double* b, double* x) {
     // stale coarse levels (mg_refresh): try with a cap, rebuild and retry on failure
-    if (mg_refresh > 1 && !slab && !coupled) {
+    if (mg_reuse && mg_refresh > 1 && !slab && !coupled) {
       const bool will_reuse = mg_setup_step >= 0 && mg_setup_step != step_counter &&
                               step_counter - mg_setup_step < mg_refresh && !mg.empty();
       if (will_reuse && last_cg_iters > 0) {
         int it = -1;
+        mg_cross_ok = true;
         try {
           it = cg_mg_solve_once<DD, FE>(b, x, std::max(50, 4 * last_cg_iters));
         } catch (const SimError& e) {
+          mg_cross_ok = false;
           if (e.code != IMPM_ERR_LINEAR_SOLVER) throw;
           it = -1;
         }
+        mg_cross_ok = false;
         if (it >= 0) return last_cg_iters = it;
         mg_setup_step = -1;  // rebuild the hierarchy for the current J and retry
       }
@@ -1855,7 +1931,55 @@ struct Sim {
   // delta = J^-1 rhs (grid layout); returns Krylov iterations. Symmetric
   // single-field J: CG (MG or block-Jacobi preconditioned), falling back to
   // BiCGStab on breakdown; coupled u-p (nonsymmetric): BiCGStab.
+  // Direct path (small systems): the reference's own algorithm, sparse_lu_solve
+  // (src/linear_solver.cpp:11-88: row equilibration, pivoted LU, <= 2
+  // refinement sweeps, backward-error gate), on the CSR of J over the free DOFs
+  // (the reference pattern, jacobian.hpp:36-65), device-resident end to end.
+  // Used by the auto solver for n_dofs <= kDirectMax on one GPU: below that
+  // size a dense device LU costs milliseconds, and it resolves the numerically
+  // singular systems of non-lattice particle sets (fringe nodes at ~1e-14 of
+  // the bulk stiffness, cond(S J) ~ 1e19) exactly as the reference's LU does,
+  // which no Krylov method can.
+  static constexpr int kDirectMax = csr::kDenseMax;
+  std::unique_ptr<csr::LuSolver> lu;
+  DBuf<int32_t> lu_cols;
+  DBuf<double> lu_vals, lu_b, lu_x;
+  bool use_direct() const {
+    return opt.krylov == IMPM_KRYLOV_AUTO && !multi() && n_dofs > 0 && n_dofs <= kDirectMax && !direct_off;
+  }
+  bool direct_off = std::getenv("IMPM_DIRECT") && std::atoi(std::getenv("IMPM_DIRECT")) == 0;
+  int direct_solve(const double* rhs, double* x) {
+    const int n = n_dofs;
+    const int64_t z = ref_nnz();
+    std::vector<int64_t> rl(n), rp(n + 1, 0);
+    CK(cudaMemcpyAsync(rl.data(), rowlen.p, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, s));
+    sync();
+    for (int i = 0; i < n; ++i) rp[i + 1] = rp[i] + rl[i];
+    CK(cudaMemcpyAsync(rowptr.p, rp.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, s));
+    lu_cols.ensure(std::max<int64_t>(z, 1));
+    lu_vals.ensure(std::max<int64_t>(z, 1));
+    lu_b.ensure(n);
+    lu_x.ensure(n);
+    dispatch_df([&](auto Dc, auto Fc) {
+      constexpr int DD = decltype(Dc)::value, FE = decltype(Fc)::value;
+      k_csr_fill<DD, FE><<<blocks_for(n), kThreads, 0, s>>>(g, n, node_of.p, field_of.p, dof_of.p, act_idx.p, vals.p,
+                                                            row_len, row_slots.p, row_nzb.p, rowptr.p, lu_cols.p,
+                                                            lu_vals.p); ++g_launches;
+      CKL();
+    });
+    k_grid_to_dof<<<blocks_for(n), kThreads, 0, s>>>(n, rhs, node_of.p, field_of.p, F, lu_b.p); ++g_launches;
+    CKL();
+    if (!lu) lu = std::make_unique<csr::LuSolver>();
+    lu->A.upload_device(n, rowptr.p, lu_cols.p, lu_vals.p, z, s);
+    lu->solve_device(lu_b.p, lu_x.p);
+    CK(cudaMemsetAsync(x, 0, sizeof(double) * NF(), s));
+    k_dof_to_grid<<<blocks_for(n), kThreads, 0, s>>>(n, lu_x.p, node_of.p, field_of.p, F, x); ++g_launches;
+    CKL();
+    return 0;
+  }
+
   int solve_dev(const double* rhs, double* x) {
+    if (use_direct()) return direct_solve(rhs, x);
     int out = 0;
     dispatch_df([&](auto Dc, auto Fc) {
       constexpr int DD = decltype(Dc)::value, FE = decltype(Fc)::value;
@@ -1891,6 +2015,7 @@ struct Sim {
           // carry no stiffness): retry with block Jacobi before giving up
           if (e.code != IMPM_ERR_LINEAR_SOLVER) throw;
           if (krylov_debug) std::fprintf(stderr, "[gmres] MG failed (%s): block-Jacobi retry\n", e.what());
+          mg_setup_step = -1;  // the next MG solve rebuilds the hierarchy
           out = gmres_solve<DD, FE>(rhs, x, false);
         }
         return;
@@ -1935,6 +2060,7 @@ struct Sim {
   // r0_known >= 0: r already holds r(u) with that norm (the warm-start test
   // of newton_solve evaluated it; mpm_solver.hpp:297 recomputes the same value)
   void newton_attempt(double load_scale, impm_step_record* rec, double r0_known = -1.0) {
+    exact_newton = exact_newton_env >= 0 ? exact_newton_env != 0 : mat.kind == kHenckyJ2;
     std::vector<double> rels;
     const auto t0 = std::chrono::steady_clock::now();
     double diff_s = 0.0, solve_s = 0.0, res_s = 0.0, rnorm_prev = 0.0, ratio1_now = -1.0;
@@ -1952,7 +2078,8 @@ struct Sim {
       rec->solve_seconds = solve_s;
       rec->residual_seconds = res_s;
       rec->krylov_iterations = kry;
-      rec->backward_passes = iters * F * ipow_c(5, D);  // jacobian.hpp:117-125 equivalent
+      // jacobian.hpp:117-125 (sparse: fields * b^D passes) or :71-91 (dense: one per dof)
+      rec->backward_passes = iters * (opt.strategy == IMPM_STRATEGY_DENSE ? ndg() : F * ipow_c(5, D));
       rec->nnz_assembled = iters * ref_nnz();
       finish_record(rec, rels);
     };
@@ -1972,7 +2099,13 @@ struct Sim {
       // outcome; floor = krylov_rtol (1e-12).
       auto ts = std::chrono::steady_clock::now();
       axpbypcz(-1.0, r.p, 0.0, tmp2.p);
-      if (it == 1) {
+      if (exact_newton) {
+        // return-map materials: the elastic/plastic branch of every particle
+        // (materials.hpp:185-190) is decided on the iterate, so an inexact
+        // step can flip a branch the reference's LU (backward error ~1e-14,
+        // linear_solver.cpp:71-78) does not; solve to the exact-solve target
+        cur_rtol = exact_rtol;
+      } else if (it == 1) {
         // first iteration: its linear error lands in r1 as <= eta r0, so eta =
         // 1% of the contraction |r1| / r0 seen at the previous load step keeps
         // r1 within ~1% of the exact-solve value (no history: 1% of tol)
@@ -2214,7 +2347,7 @@ struct Sim {
       rec->diff_seconds = diff_s;
       rec->solve_seconds = solve_s;
       rec->krylov_iterations = kry;
-      rec->backward_passes = iters * F * (D == 2 ? 25 : 125);
+      rec->backward_passes = iters * (opt.strategy == IMPM_STRATEGY_DENSE ? ndg() : F * (D == 2 ? 25 : 125));
       rec->nnz_assembled = iters * ref_nnz();
       finish_record(rec, rels);
     }
@@ -2330,8 +2463,6 @@ impm_status fail(Sim* sim, const SimError& e) {
 thread_local std::string g_create_error;
 
 }  // namespace
-
-#include "impm_csr.cuh"
 
 namespace {
 thread_local std::string g_csr_error;
@@ -2523,6 +2654,38 @@ impm_status impm_sim_colour_groups(impm_sim* h, int32_t* group_of_dof, int32_t* 
       for (int a = 0; a < sim->D; ++a) off = off * 5 + ((node_of[d] / sim->g.stride[a]) % sim->g.nodes[a]) % 5;
       group_of_dof[d] = field_of[d] * S + off;
     }
+  }
+  API_END(sim)
+}
+impm_status impm_sim_support_stats(impm_sim* h, int64_t* out) {
+  SIM;
+  API_BEGIN(sim)
+  // [P, sum s_p, sum s_p^2, sum_bins n_p * nk, sum_bins n_p * nk^2, bins, histogram of s_p (1..27)]
+  if (!sim->step_built) throw SimError(IMPM_ERR_CONFIG, "support_stats before begin_step");
+  const int P = sim->P, N = sim->g.N;
+  std::vector<int> sup(std::max(P, 1)), bs(N + 1);
+  std::vector<uint8_t> bf(std::max(N, 1));
+  CK(cudaMemcpyAsync(sup.data(), sim->sup.p, sizeof(int) * P, cudaMemcpyDeviceToHost, sim->s));
+  CK(cudaMemcpyAsync(bs.data(), sim->bin_start.p, sizeof(int) * (N + 1), cudaMemcpyDeviceToHost, sim->s));
+  CK(cudaMemcpyAsync(bf.data(), sim->bflag.p, N, cudaMemcpyDeviceToHost, sim->s));
+  sim->sync();
+  for (int i = 0; i < 34; ++i) out[i] = 0;
+  out[0] = P;
+  for (int p = 0; p < P; ++p) {
+    int sp = 1;
+    for (int a = 0; a < sim->D; ++a) sp *= (sup[p] >> (2 * a)) & 3;
+    out[1] += sp;
+    out[2] += static_cast<int64_t>(sp) * sp;
+    if (sp <= 27) out[6 + sp] += 1;
+  }
+  for (int b = 0; b < N; ++b) {
+    const int np = bs[b + 1] - bs[b];
+    if (np == 0) continue;
+    int nk = 1;
+    for (int a = 0; a < sim->D; ++a) nk *= 2 + ((bf[b] >> a) & 1);
+    out[3] += static_cast<int64_t>(np) * nk;
+    out[4] += static_cast<int64_t>(np) * nk * nk;
+    out[5] += 1;
   }
   API_END(sim)
 }

@@ -17,8 +17,10 @@ from .particles import GridSpec, ParticleArray, particle_doubles
 
 MATERIAL_KINDS = {"hencky": 0, "hencky_j2": 1, "neo_hookean": 2, "drucker_prager": 3, "cam_clay": 4}
 SHAPES = {"gimp": 1, "quadratic-bspline": 2, "quadratic_bspline": 2}
-KRYLOV = {"auto": 0, "cg": 1, "bicgstab": 2, "gmres": 3}
+KRYLOV = {"auto": 0, "cg": 1, "bicgstab": 2, "gmres": 3, "iterative": 4}
 PRECOND = {"mg": 0, "multigrid": 0, "block_jacobi": 1, "jacobi": 1}
+STRATEGIES = {"sparse": 0, "dense": 1}
+INTERFERENCE = {"off": 0, "sampled": 1, "always": 2}
 
 
 @dataclass
@@ -60,11 +62,14 @@ class SolverOptions:
     profile: bool = False
     precond: str = "mg"
     mg_smooth: int = 1
+    strategy: str = "sparse"  # JacobianStrategy (jacobian.hpp:18)
+    interference: str = "off"  # InterferenceCheck (jacobian.hpp:20)
 
     def to_c(self):
         return _abi.Options(self.tol, self.abs_floor, int(self.max_iterations), int(bool(self.total_lagrangian)),
                             SHAPES[self.shape], KRYLOV[self.krylov], self.krylov_rtol, int(self.krylov_max_iter),
-                            int(bool(self.profile)), PRECOND[self.precond], int(self.mg_smooth))
+                            int(bool(self.profile)), PRECOND[self.precond], int(self.mg_smooth),
+                            STRATEGIES[self.strategy], INTERFERENCE[self.interference])
 
 
 @dataclass
@@ -245,6 +250,15 @@ class MpmSim:
         ng = ctypes.c_int32()
         self._h.call("impm_sim_colour_groups", _abi.ptr(out), ctypes.byref(ng))
         return out[:n], ng.value
+
+    def support_stats(self):
+        """Support-size statistics of the current step (impm_sim_support_stats)."""
+        out = np.zeros(34, dtype=np.int64)
+        self._h.call("impm_sim_support_stats", _abi.ptr(out))
+        P = max(int(out[0]), 1)
+        return {"particles": int(out[0]), "mean_s": out[1] / P, "mean_s2": out[2] / P,
+                "mean_bin_box": out[3] / P, "mean_bin_box2": out[4] / P, "bins": int(out[5]),
+                "s_hist": {int(k): int(out[6 + k]) for k in range(1, 28) if out[6 + k]}}
 
     def node_mass(self):
         out = np.zeros(self._N)

@@ -9,8 +9,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 GOLDEN = os.path.join(HERE, "golden")
 MATERIAL_NAMES = {0: "hencky", 1: "hencky_j2", 2: "neo_hookean"}
 
-MPM_CASES = ["bar1d_j2", "cant2d_hencky", "cant2d_hencky_newton", "col2d_j2", "col2d_nh", "cube3d_nh",
-             "cube3d_nh_newton", "footing3d_nh", "tl2d_hencky", "cfg1_nh"]
+MPM_CASES = ["bar1d_j2", "cant2d_hencky", "cant2d_hencky_newton", "col2d_j2", "col2d_nh", "col2d_nh_newton",
+             "cube3d_nh", "cube3d_nh_newton", "footing3d_nh", "footing3d_16", "bench_sample3d", "tl2d_hencky",
+             "cfg1_nh"]
 
 
 def load(name):

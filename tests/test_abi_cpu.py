@@ -145,3 +145,35 @@ def build_facade_smoke(out_path):
 
 def test_cpp_facade_compiles_and_links(lib, tmp_path):
     assert os.path.exists(build_facade_smoke(str(tmp_path / "facade_smoke")))
+
+
+REF_INCLUDE = "/root/reference/proj/include"
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_INCLUDE), reason="reference headers not present (GPU box)")
+def test_integration_snippet_compiles_against_reference(lib, tmp_path):
+    """INTEGRATION.md section 1's snippet, verbatim, compiled in
+    IMPM_GPU_REFERENCE_TYPES mode against the reference's own headers and
+    linked with libimpm_gpu.so: impm_gpu::MpmSim<D> takes impm::Grid<D>,
+    impm::Particle<D>, impm::MaterialSpec and impm::SolverOptions
+    (mpm_solver.hpp:20-68)."""
+    text = open(os.path.join(REPO, "INTEGRATION.md")).read()
+    block = text.split("<!-- snippet:reference-types -->", 1)[1].split("<!-- /snippet -->", 1)[0]
+    code = block.split("```cpp", 1)[1].split("```", 1)[0]
+    src = tmp_path / "snippet.cpp"
+    src.write_text(code + "\nint main() { return settle_column(0) == 12345.0; }\n")
+    exe = tmp_path / "snippet"
+    subprocess.run(["g++", "-std=c++20", "-O1", "-I", os.path.join(REPO, "include"), "-I", REF_INCLUDE,
+                    "-o", str(exe), str(src), "-L", os.path.join(REPO, "paper_2507_09435_b200"), "-limpm_gpu"],
+                   check=True)
+    assert exe.exists()
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_INCLUDE), reason="reference headers not present (GPU box)")
+def test_bar_swap_builds_against_reference(lib):
+    """tests/cpp/bar_swap.cpp (the reference's build_bar/run_bar with only the
+    MpmSim type swapped) builds against the reference headers; the binary
+    travels to the GPU box for tests/test_gpu_facade.py."""
+    from paper_2507_09435_b200 import build
+
+    assert os.path.exists(build.build_bar_swap())

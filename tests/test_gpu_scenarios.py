@@ -32,11 +32,7 @@ def test_bar_scenario_matches_reference_outputs(case, tmp_path):
     assert (np.abs(got - want).max(axis=0) / scale).max() <= 1e-7
     its_got = np.bincount(load_csv(tmp_path / "iterations.csv")[:, 0].astype(int))
     its_ref = np.bincount(ref(case + "__iterations")[:, 0].astype(int))
-    diff = np.abs(its_got - its_ref)
-    if case == "bar_elastic":
-        assert diff.max() == 0
-    else:  # J2 plastic onset, see tests/test_gpu_parity.py
-        assert diff.max() <= 1 and (diff > 0).sum() <= 4
+    np.testing.assert_array_equal(its_got, its_ref)  # identical Newton counts, J2 included
     assert os.path.exists(tmp_path / "summary.json")
 
 

@@ -148,11 +148,9 @@ def test_slab_newton_steps_match_reference(name, nranks):
     for it in iters[1:]:
         np.testing.assert_array_equal(it, iters[0])  # every rank took the same Newton path
     ref_iters = fx["newton_iters"]
-    if spec.get("material") == "hencky_j2":  # see test_gpu_parity.test_newton_counts_and_final_state
-        diff = np.abs(iters[0] - ref_iters)
-        assert diff.max() <= 1 and (diff > 0).sum() <= max(1, steps // 10), (iters[0], ref_iters)
-    else:
-        np.testing.assert_array_equal(iters[0], ref_iters)
+    # identical counts on every case, J2 included (exact-equivalent solves on
+    # return-map materials, see test_gpu_parity.test_newton_counts_and_final_state)
+    np.testing.assert_array_equal(iters[0], ref_iters)
     owned, ids = gather_owned([r[1] for r in res], g.dim)
     np.testing.assert_array_equal(ids, np.arange(len(parts)))  # every particle owned exactly once
     _assert_state_close(owned.data, fx["particles_final"], g.dim, g.h)
