@@ -240,7 +240,8 @@ def kernel_table(kt, rec, info, D, P, n_nodes, peak):
     vl0 = kt.get("vcycle_level0", (0.0, 0))
     row("vcycle_level0", "MG fine level: k_spmv<__half> residual + Jacobi sweeps, k_jacobi0, k_restrict, "
         "k_prolong_add", vl0[0], vl0[1], (2 * sv + sv // (D * D) + 250 * rows_) if vl0[1] else None,
-        "per scope (half a V-cycle): fp16 values 2 B x stored + slot ids + ~250 B/row of vectors and Dinv", "jac")
+        "per scope (half a V-cycle): fp16 values 2 B x stored + slot ids + ~250 B/row of vectors and Dinv",
+        "vcycle_level0")
     row("vcycle", "MG V-cycle, all levels (fp16/fp32 level sweeps, restriction, prolongation, coarsest solve)",
         kt["vcycle"][0], kt["vcycle"][1], None, "-", None)
     row("mg_setup", "MG setup (Galerkin PtAP, power estimate)", kt["mg_setup"][0], kt["mg_setup"][1], None, "-",

@@ -1120,13 +1120,30 @@ __device__ __forceinline__ int mask_pos_r(const unsigned (&m)[4], int sl) {
 }
 
 // zero the stored part of every row (component chunks incl. padding)
+// row_mask != nullptr: zero only the upper blocks (slot >= the centre slot
+// S/2; the assembly then forms only those and k_mirror_lower writes the rest)
 __global__ void k_zero_rows(int n_act, int F, const int* __restrict__ row_nzb, double* __restrict__ vals,
-                            int64_t row_len) {
+                            int64_t row_len, const unsigned* __restrict__ row_mask = nullptr, int center = 0) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= n_act) return;
-  const int n = F * cpad(row_nzb[warp], F);
+  const int nzb = row_nzb[warp], cp = cpad(nzb, F);
+  int lo = 0;  // first stored position at or above the centre slot
+  if (row_mask) {
+    const unsigned* m = row_mask + static_cast<int64_t>(warp) * 4;
+    for (int w = 0; w < 4; ++w) {
+      const int b0 = w * 32;
+      unsigned bits = m[w];
+      if (b0 + 32 <= center) {
+        lo += __popc(bits);
+      } else if (b0 < center) {
+        lo += __popc(bits & ((1u << (center - b0)) - 1u));
+      }
+    }
+  }
   double* r = vals + static_cast<int64_t>(warp) * row_len;
-  for (int j = lane; j < n; j += 32) r[j] = 0.0;
+  const int len = cp - lo * F;
+  for (int c = 0; c < F; ++c)
+    for (int j = lane; j < len; j += 32) r[c * cp + lo * F + j] = 0.0;
 }
 
 // ------------------------------------------- K6 Jacobian: numeric ---------
@@ -1644,47 +1661,76 @@ __global__ void __launch_bounds__(WARPS * 32, D == 3 ? (RMW ? 2 : 4) : 1) k_asse
 }
 
 // Lower blocks of a symmetric J from the upper ones (the assembly ran with
-// MIRROR = false): K_ab = K_ba^T for flat(b) < flat(a). One warp per row, a
-// lane per value; stored slots are ascending, so the lower ones come first.
-// A column node that is not a row (no DOF) gets a zero block.
+// MIRROR = false): K_ab = K_ba^T for flat(b) < flat(a). One warp per row.
+// First each lane resolves one lower block's source (row b, position of
+// -delta in row b, its component pitch) into shared memory, so the per-value
+// loop is one load and one coalesced store. A column node that is not a row
+// (no DOF) gets a zero block.
 template <int D>
-__global__ void k_mirror_lower(GridC g, int n_act, const int* __restrict__ act_list, const int* __restrict__ act_idx,
-                               const int* __restrict__ row_nzb, const uint8_t* __restrict__ row_slots,
-                               const unsigned* __restrict__ row_mask, double* __restrict__ vals, int64_t row_len) {
+__global__ void __launch_bounds__(256) k_mirror_lower(GridC g, int n_act, const int* __restrict__ act_list,
+                                                      const int* __restrict__ act_idx, const int* __restrict__ row_nzb,
+                                                      const uint8_t* __restrict__ row_slots,
+                                                      const unsigned* __restrict__ row_mask,
+                                                      double* __restrict__ vals, int64_t row_len) {
   constexpr int S = ipow_c(5, D);
-  constexpr int DD = D * D;
   constexpr int center = (S - 1) / 2;  // slot of delta = 0
-  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  __shared__ long long src_s[8][center];
+  __shared__ int cpb_s[8][center];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 8 + warp;
   if (row >= n_act) return;
   const int node = act_list[row];
   const int nzb = row_nzb[row], cp = cpad(nzb, D);
   const uint8_t* sl = row_slots + static_cast<int64_t>(row) * S;
-  double* out = vals + static_cast<int64_t>(row) * row_len;
-  for (int e = lane; e < nzb * DD; e += 32) {
-    const int pos = e / DD, cd = e - pos * DD, c = cd / D, d = cd - c * D;
-    const int slot = sl[pos];
-    if (slot >= center) break;
-    int r = slot, off = 0;
+  // stored slots ascend, so the lower blocks are the first nl positions
+  int nl = 0;
+  {
+    const unsigned* m = row_mask + static_cast<int64_t>(row) * 4;
+    for (int w = 0; w < 4; ++w) {
+      const int b0 = w * 32;
+      if (b0 + 32 <= center)
+        nl += __popc(m[w]);
+      else if (b0 < center)
+        nl += __popc(m[w] & ((1u << (center - b0)) - 1u));
+    }
+  }
+  for (int j = lane; j < nl; j += 32) {
+    int r = sl[j], off = 0;
+    const int slot = r;
 #pragma unroll
     for (int a = D - 1; a >= 0; --a) {
       off += (r % 5 - 2) * g.stride[a];
       r /= 5;
     }
     const int rb = act_idx[node + off];
-    double v = 0.0;
+    long long src = -1;
+    int cpb = 0;
     if (rb >= 0) {
       const int ms = S - 1 - slot;  // the slot of -delta in row b
-      const unsigned* m = row_mask + static_cast<int64_t>(rb) * 4;
+      const uint4 m4 = *reinterpret_cast<const uint4*>(row_mask + static_cast<int64_t>(rb) * 4);
+      const unsigned mw[4] = {m4.x, m4.y, m4.z, m4.w};
       const int w = ms >> 5;
       int pb = 0;
 #pragma unroll
-      for (int k = 0; k < 3; ++k)
-        if (k < w) pb += __popc(m[k]);
-      pb += __popc(m[w] & ((1u << (ms & 31)) - 1u));
-      v = vals[static_cast<int64_t>(rb) * row_len + d * cpad(row_nzb[rb], D) + pb * D + c];
+      for (int k = 0; k < 4; ++k) {
+        if (k < w) pb += __popc(mw[k]);
+        if (k == w) pb += __popc(mw[k] & ((1u << (ms & 31)) - 1u));
+      }
+      cpb = cpad(row_nzb[rb], D);
+      src = static_cast<long long>(rb) * row_len + pb * D;
     }
-    out[c * cp + pos * D + d] = v;
+    src_s[warp][j] = src;
+    cpb_s[warp][j] = cpb;
   }
+  __syncwarp();
+  double* out = vals + static_cast<int64_t>(row) * row_len;
+  // value (c, j, d) of the lower part: component chunk c is contiguous
+  for (int c = 0; c < D; ++c)
+    for (int e = lane; e < nl * D; e += 32) {
+      const int j = e / D, d = e - j * D;
+      const long long src = src_s[warp][j];
+      out[c * cp + e] = src >= 0 ? vals[src + d * cpb_s[warp][j] + c] : 0.0;
+    }
 }
 
 // Block inverse for the smoother / block-Jacobi preconditioner, safeguarded:

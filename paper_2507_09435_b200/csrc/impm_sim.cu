@@ -1067,8 +1067,11 @@ struct Sim {
       }
       if (n_act > 0) {
         Prof::Scope ps(&prof, kcAssemble);
-        k_zero_rows<<<blocks_for(static_cast<int64_t>(n_act) * 32), kThreads, 0, s>>>(n_act, DD, row_nzb.p, vals.p,
-                                                                                    row_len); ++g_launches;
+        const bool upper_only = asm_sym && mirror_pass_env && !multi() && !asm_rmw &&
+                                mat.kind != kDruckerPrager && mat.kind != kCamClay;
+        k_zero_rows<<<blocks_for(static_cast<int64_t>(n_act) * 32), kThreads, 0, s>>>(
+            n_act, DD, row_nzb.p, vals.p, row_len, upper_only ? row_mask.p : nullptr, (ipow_c(5, DD) - 1) / 2);
+        ++g_launches;
         constexpr int W = 4;
         constexpr int PPL = DD == 3 ? 5 : (DD == 2 ? 3 : 1);
         constexpr int asm_ppl3 = 3;  // 3D block pairs per lane (4: 78 vs 72 ms per load step)
@@ -1112,9 +1115,8 @@ struct Sim {
           }
           ++g_launches;
         }
-        if (asm_sym && mirror_pass_env && !multi() && !asm_rmw && mat.kind != kDruckerPrager &&
-            mat.kind != kCamClay) {
-          k_mirror_lower<DD><<<blocks_for(static_cast<int64_t>(n_act) * 32), kThreads, 0, s>>>(
+        if (upper_only) {
+          k_mirror_lower<DD><<<static_cast<unsigned>((n_act + 7) / 8), 256, 0, s>>>(
               g, n_act, act_list.p, act_idx.p, row_nzb.p, row_slots.p, row_mask.p, vals.p, row_len);
           ++g_launches;
           CKL();
