@@ -195,7 +195,7 @@ def fp64_peak():
         return 37.2, "nominal"
 
 
-def kernel_table(kt, rec, info, D, P, n_nodes, peak):
+def kernel_table(kt, rec, info, D, P, n_nodes, peak, symmetric_nh=True):
     """One row per kernel class of the profiled load step: CUDA-event time,
     launches, SURVEY.md 8(d) algorithmic bytes per launch, achieved GB/s and
     fraction of the measured HBM peak. K6 (tangent + assembly) counts as one
@@ -221,8 +221,10 @@ def kernel_table(kt, rec, info, D, P, n_nodes, peak):
         rows.append(r)
 
     jm = kt["tangent"][0] + kt["assemble"][0]
-    row("jacobian", "K6 Jacobian: k_tangent_nh3 (closed-form dP/dG; dual numbers for other materials) + "
-                    "k_assemble_bins_staged (colour-batched BSR, upper blocks) + k_mirror_lower + k_diag_inverse",
+    row("jacobian", ("K6 Jacobian: k_tangent_nh3 (closed-form dP/dG) + k_assemble_bins_staged (colour-batched "
+                     "BSR, upper blocks) + k_mirror_lower + k_diag_inverse") if symmetric_nh else
+        ("K6 Jacobian: k_tangent (dual-number dP/dG) + k_assemble_bins_staged (colour-batched BSR, full blocks: "
+         "nonsymmetric J) + k_diag_inverse"),
         jm, n_jac, (184 * P + 8 * ref_nnz) if n_jac else None,
         "SURVEY 8(d) K6: 184 B/particle state + 8 B x reference-pattern nnz", "jacobian")
     row("spmv", "k_spmv<double> (compacted box-BSR y = J x, outer Krylov)", kt["spmv"][0], kt["spmv"][1],
@@ -397,7 +399,8 @@ def main():
     # CUDA events of the profiled load step (events on the sim stream)
     peak, peak_kind = peaks()
     P = int(prob.particles.shape[0])
-    table = kernel_table(kt, prof_rec, info, D, P, int(prob.grid.node_count()), peak)
+    table = kernel_table(kt, prof_rec, info, D, P, int(prob.grid.node_count()), peak,
+                         symmetric_nh=prob.material.kind == "neo_hookean")
     dom = max((r for r in table if r["bytes_per_launch"]), key=lambda r: r["ms_total"])
     tr = ncu_traffic(dom["traffic_key"])
     asm_ms, _ = kt["assemble"]

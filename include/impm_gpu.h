@@ -186,6 +186,9 @@ impm_status impm_sim_colour_groups(impm_sim* sim, int32_t* group_of_dof /*[n]*/,
  * histogram of s_p over 1..27 at out[7..33]} (s_p = support nodes of
  * particle p, nk = support box of its bin). */
 impm_status impm_sim_support_stats(impm_sim* sim, int64_t* out);
+/* Checked builds (-DIMPM_CHECKED): number of out-of-range scattered accesses
+ * the device has counted so far; -1 in a regular build. */
+int64_t impm_debug_oob_count(void);
 /* p2g_map (mpm_solver.hpp:142-152) */
 impm_status impm_sim_p2g_map(impm_sim* sim, const double* per_particle, double* out /*[N]*/);
 

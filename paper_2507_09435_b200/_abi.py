@@ -99,6 +99,7 @@ _SIGNATURES = {
     "impm_sim_node_mass": (c_int32, [c_void_p, c_void_p]),
     "impm_sim_colour_groups": (c_int32, [c_void_p, c_void_p, _P(c_int32)]),
     "impm_sim_support_stats": (c_int32, [c_void_p, c_void_p]),
+    "impm_debug_oob_count": (c_int64, []),
     "impm_sim_p2g_map": (c_int32, [c_void_p, c_void_p, c_void_p]),
     "impm_sim_residual": (c_int32, [c_void_p, c_void_p, c_double, c_void_p]),
     "impm_sim_jacobian_csr": (c_int32, [c_void_p, c_void_p, c_double, _P(c_int64), c_void_p, c_void_p, c_void_p]),

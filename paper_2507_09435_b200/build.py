@@ -48,7 +48,8 @@ def up_to_date():
 def build(force=False, verbose=False):
     if not force and up_to_date():
         return OUT
-    cmd = [NVCC, *FLAGS, "-o", OUT, SRC, *nccl_flags()]
+    extra = os.environ.get("IMPM_NVCC_EXTRA", "").split()  # tuning experiments (e.g. -DIMPM_ASM_PPL3=2)
+    cmd = [NVCC, *FLAGS, *extra, "-o", OUT, SRC, *nccl_flags()]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)

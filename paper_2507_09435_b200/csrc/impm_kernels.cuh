@@ -17,12 +17,28 @@
 
 #include <cuda_runtime.h>
 
+#include <climits>
 #include <cstdint>
 #include <type_traits>
 
 #include "impm_math.cuh"
 
 namespace impm_gpu {
+
+// Checked build (-DIMPM_CHECKED, scripts/checked_cases.sh): the index math of
+// the scattered accesses (assembly block updates, transpose pass, SpMV gathers,
+// residual node updates) is range-checked on the device and violations are
+// counted (impm_debug_oob_count). compute-sanitizer is closed on this pool.
+#ifdef IMPM_CHECKED
+__device__ unsigned long long g_oob_count = 0;
+#define IMPM_CHECK_IDX(i, n)                                                              \
+  do {                                                                                    \
+    if (static_cast<unsigned long long>(i) >= static_cast<unsigned long long>(n))         \
+      atomicAdd(&g_oob_count, 1ull);                                                      \
+  } while (0)
+#else
+#define IMPM_CHECK_IDX(i, n) ((void)0)
+#endif
 
 __host__ __device__ constexpr int ipow_c(int b, int e) { return e == 0 ? 1 : b * ipow_c(b, e - 1); }
 __host__ __device__ constexpr int pad4(int x) { return (x + 3) / 4 * 4; }
@@ -811,6 +827,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_residual_bins_staged(
       int node = 0;
 #pragma unroll
       for (int a = 0; a < D; ++a) node += (bidx[a] + li[a]) * g.stride[a];
+      IMPM_CHECK_IDX(node, g.N);
 #pragma unroll
       for (int c = 0; c < D; ++c) atomicAdd(r + static_cast<int64_t>(node) * D + c, acc[c]);  // RED, one writer per colour
     }
@@ -1105,6 +1122,14 @@ __device__ __forceinline__ int mask_pos(const unsigned* m, int sl) {
   return pos + __popc(m[w] & ((1u << (sl & 31)) - 1u));
 }
 
+// 8-byte asynchronous global -> shared copy (LDGSTS): no register staging,
+// so the copies of a whole bin are in flight while the warp does other work
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 __device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 
 // mask_pos over a register copy of the row's 128-bit slot mask (no dynamic
@@ -1319,7 +1344,10 @@ struct AsmFlush {
 // only the upper blocks (flat(l) >= flat(k)) are formed and k_mirror_lower
 // copies the transposes once after the last colour (half the reductions)
 template <int D, int SHAPE, int PPL, int WARPS, int PCH, bool SYM = false, bool RMW = false, bool MIRROR = true>
-__global__ void __launch_bounds__(WARPS * 32, D == 3 ? (RMW ? 2 : 4) : 1) k_assemble_bins_staged(
+#ifndef IMPM_ASM_MINB
+#define IMPM_ASM_MINB 4  // resident CTAs per SM the 3D assembly is compiled for
+#endif
+__global__ void __launch_bounds__(WARPS * 32, D == 3 ? (RMW ? 2 : IMPM_ASM_MINB) : 1) k_assemble_bins_staged(
     GridC g, const double* __restrict__ pd, int64_t cap, const double* __restrict__ xs,
     const int* __restrict__ bin_start, const uint8_t* __restrict__ bflag, const double* __restrict__ A,
     const int* __restrict__ act_idx, const unsigned* __restrict__ row_mask, const int* __restrict__ row_nzb,
@@ -1336,6 +1364,8 @@ __global__ void __launch_bounds__(WARPS * 32, D == 3 ? (RMW ? 2 : 4) : 1) k_asse
   __shared__ int Rrow[WARPS][NK];
   __shared__ int Rcp[WARPS][NK];
   __shared__ uint4 Rmask[WARPS][NK];
+  static_assert(sizeof(As) + sizeof(Gs) + sizeof(HWs) + sizeof(Rrow) + sizeof(Rcp) + sizeof(Rmask) <= 48 * 1024,
+                "k_assemble_bins_staged: static shared memory above the 48 KB launch limit");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   extern __shared__ __align__(16) unsigned char asm_dyn[];
   using FL = AsmFlush<PPL, DD>;
@@ -1381,9 +1411,23 @@ __global__ void __launch_bounds__(WARPS * 32, D == 3 ? (RMW ? 2 : 4) : 1) k_asse
         l_out = (t - k_out * nchunk) * PPL;
       }
     };
+    // resident bin (<= PCH particles): its tangent blocks go to shared memory
+    // by asynchronous copies now, so that they are in flight during the row
+    // metadata and 1D-weight staging below (global A is direction-major
+    // [df][cb]; As keeps [cb][df] for the H loop)
+    const int p0 = bin_start[b], p1 = bin_start[b + 1];
+    const bool resident = p1 - p0 <= PCH;
+    __syncwarp();
+    if (resident) {
+      const int np0 = p1 - p0;
+      const double* Ab = A + static_cast<int64_t>(p0) * NA;
+      for (int e = lane; e < np0 * NA; e += 32) {
+        const int pl = e / NA, r = e - pl * NA, df = r / DD, cb = r - df * DD;
+        cp_async8(&As[warp][pl * NA + cb * DD + df], Ab + e);
+      }
+    }
     // stage the box nodes' row metadata once per bin (all lanes in parallel)
     // so that the per-task block lookups read shared memory only
-    __syncwarp();
     if (lane < nk) {
       int rk = lane, node = 0;
       int li[3] = {0, 0, 0};
@@ -1402,8 +1446,6 @@ __global__ void __launch_bounds__(WARPS * 32, D == 3 ? (RMW ? 2 : 4) : 1) k_asse
       }
     }
     __syncwarp();
-    const int p0 = bin_start[b], p1 = bin_start[b + 1];
-    const bool resident = p1 - p0 <= PCH;
     for (int r0 = 0; r0 < ntasks; r0 += 32) {
       const int task = r0 + lane;
       const bool has_task = task < ntasks;
@@ -1440,10 +1482,10 @@ __global__ void __launch_bounds__(WARPS * 32, D == 3 ? (RMW ? 2 : 4) : 1) k_asse
         __syncwarp();
         // stage A_p (contiguous) and the 1D weights of the chunk; the A loads
         // go to registers first (4 particles at a time) so that they are in
-        // flight together
+        // flight together (resident bins: already copied asynchronously)
         const double* Ab = A + static_cast<int64_t>(pc) * NA;
 #pragma unroll 1
-        for (int q0 = 0; q0 < PCH; q0 += 4) {
+        for (int q0 = 0; q0 < (resident ? 0 : PCH); q0 += 4) {
           constexpr int NL = (4 * NA + 31) / 32;
           double ta[NL];
 #pragma unroll
@@ -1475,6 +1517,7 @@ __global__ void __launch_bounds__(WARPS * 32, D == 3 ? (RMW ? 2 : 4) : 1) k_asse
           W1[((pl * D + a) * 3 + i) * 2] = w;
           W1[((pl * D + a) * 3 + i) * 2 + 1] = dw;
         }
+        if (resident) cp_async_wait_all();  // this lane's tangent copies have landed
         __syncwarp();
         for (int e = lane; e < np * nk; e += 32) {
           const int pl = e / nk, k = e - pl * nk;
@@ -1614,6 +1657,7 @@ __global__ void __launch_bounds__(WARPS * 32, D == 3 ? (RMW ? 2 : 4) : 1) k_asse
             }
 #pragma unroll
             for (int a = 0; a < D; ++a) sl = sl * 5 + (ll[a] - lk[a] + 2);
+            IMPM_CHECK_IDX((D - 1) * cp + mask_pos_r(rm, sl) * D + D - 1, row_len);
             double* rv = rbase + mask_pos_r(rm, sl) * D;
             // fire-and-forget L2 reductions (RED.ADD.F64, result unused): one
             // writer per address per colour launch and launches in stream
@@ -1648,6 +1692,7 @@ __global__ void __launch_bounds__(WARPS * 32, D == 3 ? (RMW ? 2 : 4) : 1) k_asse
             const uint4 m4 = Rmask[warp][l];
             const unsigned ml[4] = {m4.x, m4.y, m4.z, m4.w};
             const int cpl = Rcp[warp][l];
+            IMPM_CHECK_IDX((D - 1) * cpl + mask_pos_r(ml, sl) * D + D - 1, row_len);
             double* rv = vals + static_cast<int64_t>(rowl) * row_len + mask_pos_r(ml, sl) * D;
 #pragma unroll
             for (int c = 0; c < D; ++c)
@@ -1717,6 +1762,8 @@ __global__ void __launch_bounds__(256) k_mirror_lower(GridC g, int n_act, const 
         if (k == w) pb += __popc(mw[k] & ((1u << (ms & 31)) - 1u));
       }
       cpb = cpad(row_nzb[rb], D);
+      IMPM_CHECK_IDX(pb, row_nzb[rb]);
+      IMPM_CHECK_IDX(rb, n_act);
       src = static_cast<long long>(rb) * row_len + pb * D;
     }
     src_s[warp][j] = src;
@@ -1912,7 +1959,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
                                                      int rows_per_warp = 16,
                                                      const float* __restrict__ x4 = nullptr,
                                                      float* __restrict__ y4 = nullptr,
-                                                     const float* __restrict__ rscale = nullptr) {
+                                                     const float* __restrict__ rscale = nullptr,
+                                                     int use_box = 1) {
   constexpr int S = ipow_c(5, D);
   constexpr int FF = F * F;
   constexpr int XS = chunk_len<VT>(S, F);
@@ -1934,6 +1982,16 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
   // x neighbourhood staged in the matrix precision (fp32 copies: products in
   // fp32, each 4-term partial added to the fp64 row sum)
   __shared__ __align__(16) XT xs_all[WARPS * RW][XS];
+  // BOX (3D level sweeps with fp32 twins): the fp32 x records of a chunk's
+  // whole node neighbourhood (its bounding box +-2 planes; a 64-row chunk is
+  // one 4x4x4 brick of the brick-ordered rows) are staged once per chunk with
+  // coalesced loads, so a row's neighbour gathers read shared memory and the
+  // row's chain is slots -> shared x instead of slots -> global x
+  constexpr bool BOX = HALF && sizeof(VT) <= 4 && F <= 4 && D == 3 && MODE != kSpmvY;
+  constexpr int BOXMAX = BOX ? 768 : 1;  // nodes (12 KB of float4: 8 CTAs per SM still fit)
+  __shared__ __align__(16) float4 xbox[BOXMAX];
+  __shared__ int offb[BOX ? S : 1];
+  __shared__ int bbox[8];  // lo[3], hi[3], ok
   for (int sl = threadIdx.x; sl < S; sl += blockDim.x) {
     int rs = sl, off = 0;
 #pragma unroll
@@ -1954,7 +2012,55 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
     // coarse levels use short chunks so that every warp gets a row)
     const int CH = (RPW > 0 ? RPW : rows_per_warp) * WARPS;
     const int nchunks = (n_act + CH - 1) / CH;
-    for (int ci = blockIdx.x; ci < nchunks; ci += gridDim.x)
+    for (int ci = blockIdx.x; ci < nchunks; ci += gridDim.x) {
+    bool box_ok = false;
+    int bl[3] = {0, 0, 0}, bd[3] = {1, 1, 1};
+    if constexpr (BOX) {
+      if (x4 != nullptr && use_box) {
+        __syncthreads();  // the previous chunk's rows are done with xbox / offb
+        if (threadIdx.x < 3) {
+          bbox[threadIdx.x] = INT_MAX;
+          bbox[3 + threadIdx.x] = -1;
+        }
+        __syncthreads();
+        const int r1 = min(n_act, (ci + 1) * CH);
+        for (int rr = ci * CH + threadIdx.x; rr < r1; rr += blockDim.x) {
+          int idx[3];
+          unflat<D>(g, act_list[rr], idx);
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            atomicMin(&bbox[a], idx[a]);
+            atomicMax(&bbox[3 + a], idx[a]);
+          }
+        }
+        __syncthreads();
+        int vol = 1;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          bl[a] = max(0, bbox[a] - 2);
+          bd[a] = min(g.nodes[a] - 1, bbox[3 + a] + 2) - bl[a] + 1;
+          vol *= bd[a];
+        }
+        box_ok = vol <= BOXMAX;
+        if (box_ok) {
+          for (int e = threadIdx.x; e < vol; e += blockDim.x) {
+            const int i2 = e % bd[2], r = e / bd[2], i1 = r % bd[1], i0 = r / bd[1];
+            const int node = (bl[0] + i0) * g.stride[0] + (bl[1] + i1) * g.stride[1] + bl[2] + i2;
+            xbox[e] = __ldg(reinterpret_cast<const float4*>(x4) + node);
+          }
+          for (int sl = threadIdx.x; sl < S; sl += blockDim.x) {
+            int rs = sl, off = 0;
+#pragma unroll
+            for (int a = D - 1; a >= 0; --a) {
+              off = off + (rs % 5 - 2) * (a == 2 ? 1 : (a == 1 ? bd[2] : bd[1] * bd[2]));
+              rs /= 5;
+            }
+            offb[sl] = off;
+          }
+        }
+        __syncthreads();
+      }
+    }
     for (int row0 = ci * CH + warp * RW; row0 < min(n_act, (ci + 1) * CH); row0 += WARPS * RW) {
       const int row = row0 + sub;
       const bool live = row < min(n_act, (ci + 1) * CH);  // the last pair may be half empty
@@ -1996,9 +2102,26 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
       // 2. stage the x records of the stored neighbours
       const uint8_t* rsl = row_slots + static_cast<int64_t>(row) * S;
       if constexpr (sizeof(VT) <= 4 && F <= 4) {
-        if (x4 != nullptr) {
+        if (BOX && box_ok) {
+          // neighbours from the chunk's staged box
+          int kl = 0;
+          if (live) {
+            int idx[3];
+            unflat<D>(g, k, idx);
+            kl = ((idx[0] - bl[0]) * bd[1] + (idx[1] - bl[1])) * bd[2] + (idx[2] - bl[2]);
+          }
+          for (int pos = lane; pos < nzb; pos += HW) {
+            IMPM_CHECK_IDX(kl + offb[rsl[pos]], BOXMAX);
+            const float4 v = xbox[kl + offb[rsl[pos]]];
+            xs[pos * F + 0] = v.x;
+            if (F > 1) xs[pos * F + 1] = v.y;
+            if (F > 2) xs[pos * F + 2] = v.z;
+            if (F > 3) xs[pos * F + 3] = v.w;
+          }
+        } else if (x4 != nullptr) {
           // fp32 twin of x, one 16-byte record per node: one load per neighbour
           for (int pos = lane; pos < nzb; pos += HW) {
+            IMPM_CHECK_IDX(k + offt[rsl[pos]], g.N);
             const float4 v = __ldg(reinterpret_cast<const float4*>(x4) + (k + offt[rsl[pos]]));
             xs[pos * F + 0] = v.x;
             if (F > 1) xs[pos * F + 1] = v.y;
@@ -2007,6 +2130,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
           }
         } else {
           for (int pos = lane; pos < nzb; pos += HW) {
+            IMPM_CHECK_IDX(k + offt[rsl[pos]], g.N);
             const int64_t nb = static_cast<int64_t>(k + offt[rsl[pos]]) * F;
 #pragma unroll
             for (int d = 0; d < F; ++d) xs[pos * F + d] = static_cast<XT>(__ldg(x + nb + d));
@@ -2014,6 +2138,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
         }
       } else {
         for (int pos = lane; pos < nzb; pos += HW) {
+          IMPM_CHECK_IDX(k + offt[rsl[pos]], g.N);
           const int64_t nb = static_cast<int64_t>(k + offt[rsl[pos]]) * F;
 #pragma unroll
           for (int d = 0; d < F; ++d) xs[pos * F + d] = static_cast<XT>(__ldg(x + nb + d));
@@ -2090,6 +2215,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
         }
       }
       __syncwarp();
+    }
     }
   }
   if (partials) block_sum_store<1>(part, partials);

@@ -284,6 +284,8 @@ struct Sim {
   // fine-level smoother matrix in fp16 with fp32 row scales (IMPM_MG_F16=0: fp32)
   bool mg_f16 = !(std::getenv("IMPM_MG_F16") && std::atoi(std::getenv("IMPM_MG_F16")) == 0);
   // fp32 twins of the V-cycle iterates feed the fp32 level SpMV gathers
+  // level sweeps stage each row chunk's x neighbourhood in shared memory (IMPM_MG_BOX=0: per-row gathers)
+  bool mg_box = !(std::getenv("IMPM_MG_BOX") && std::atoi(std::getenv("IMPM_MG_BOX")) == 0);
   bool mg_x4 = !(std::getenv("IMPM_MG_X4") && std::atoi(std::getenv("IMPM_MG_X4")) == 0);
   bool krylov_debug = std::getenv("IMPM_DEBUG_KRYLOV") != nullptr;
   bool res_staged = !(std::getenv("IMPM_RES_UNSTAGED") && std::atoi(std::getenv("IMPM_RES_UNSTAGED")) != 0);
@@ -1074,7 +1076,10 @@ struct Sim {
         ++g_launches;
         constexpr int W = 4;
         constexpr int PPL = DD == 3 ? 5 : (DD == 2 ? 3 : 1);
-        constexpr int asm_ppl3 = 3;  // 3D block pairs per lane (4: 78 vs 72 ms per load step)
+#ifndef IMPM_ASM_PPL3
+#define IMPM_ASM_PPL3 2  // 3D block pairs per lane (B200 cfg 4, ms per Jacobian: 2: 21.7, 3: 23.1, 4: 27.7)
+#endif
+        constexpr int asm_ppl3 = IMPM_ASM_PPL3;
         const int nc = ipow_c(3, DD);
         for (int col = 0; col < nc; ++col) {
           int cc[3] = {0, 0, 0}, nb[3] = {1, 1, 1}, r = col;
@@ -1295,11 +1300,12 @@ struct Sim {
       k_spmv<DD, FE, W, MODE, __half, 0, true><<<grid, W * 32, 0, s>>>(
           L.g, L.act_list, L.n_act, L.vals16, L.row_len16, L.row_slots, L.row_nzb, x, L.freem, y, dotv, parts, dflag.p,
           b, L.dinv, omega, rpw, mg_x4 ? L.twin(x) : nullptr, mg_x4 && MODE == kSpmvJacobi ? L.twin(y) : nullptr,
-          L.rscale);
+          L.rscale, mg_box ? 1 : 0);
     else if (mg_f32 && L.n_act >= 50000)
       k_spmv<DD, FE, W, MODE, float, 0, true><<<grid, W * 32, 0, s>>>(
           L.g, L.act_list, L.n_act, L.vals32, L.row_len32, L.row_slots, L.row_nzb, x, L.freem, y, dotv, parts, dflag.p,
-          b, L.dinv, omega, rpw, mg_x4 ? L.twin(x) : nullptr, mg_x4 && MODE == kSpmvJacobi ? L.twin(y) : nullptr);
+          b, L.dinv, omega, rpw, mg_x4 ? L.twin(x) : nullptr, mg_x4 && MODE == kSpmvJacobi ? L.twin(y) : nullptr,
+          nullptr, mg_box ? 1 : 0);
     else if (mg_f32)
       k_spmv<DD, FE, W, MODE, float, 0><<<grid, W * 32, 0, s>>>(L.g, L.act_list, L.n_act, L.vals32, L.row_len32,
                                                                    L.row_slots, L.row_nzb, x, L.freem, y, dotv, parts,
@@ -2658,6 +2664,15 @@ impm_status impm_sim_colour_groups(impm_sim* h, int32_t* group_of_dof, int32_t* 
     }
   }
   API_END(sim)
+}
+int64_t impm_debug_oob_count(void) {
+#ifdef IMPM_CHECKED
+  unsigned long long v = 0;
+  if (cudaMemcpyFromSymbol(&v, impm_gpu::g_oob_count, sizeof(v)) != cudaSuccess) return -2;
+  return static_cast<int64_t>(v);
+#else
+  return -1;
+#endif
 }
 impm_status impm_sim_support_stats(impm_sim* h, int64_t* out) {
   SIM;

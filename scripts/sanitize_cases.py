@@ -34,6 +34,8 @@ for name, kry in [("cube3d_nh_newton", "iterative"), ("cube3d_nh_newton", "auto"
     fixture_steps(name, kry)
 for mat in ["drucker_prager", "cam_clay", "hencky_j2"]:
     prob = workloads.footing3d(cells=(6, 6, 4), steps=10, t_hat=300e3, material=mat)
+    if mat == "hencky_j2":
+        prob.material.kappa = 40e3
     sim = impm.MpmSim(prob.grid, prob.particles, prob.material, prob.options)
     sim.fixed[:] = prob.fixed
     sim.gravity = prob.gravity
@@ -48,3 +50,9 @@ from paper_2507_09435_b200.sparse import CsrMatrix, sparse_lu_solve  # noqa: E40
 
 A = CsrMatrix(2, [0, 2, 4], [0, 1, 0, 1], [2.0, 1.0, 1.0, 2.0])
 print("csr ok", sparse_lu_solve(A, np.array([3.0, 3.0])), flush=True)
+from paper_2507_09435_b200 import _abi  # noqa: E402
+
+oob = _abi.lib().impm_debug_oob_count()
+print("out-of-range scattered accesses counted:", oob, "(-1: not a checked build)", flush=True)
+if oob > 0:
+    sys.exit(1)
