@@ -211,9 +211,11 @@ def kernel_table(kt, rec, info, D, P, n_nodes, peak, symmetric_nh=True):
     def row(name, kernel, ms, n, byt, model, key, flops=None):
         per = ms / n if n else None
         ach = byt / (per / 1e3) / 1e9 if (byt and per) else None
+        tr = ncu_traffic(key) if key else None
         r = {"class": name, "kernel": kernel, "ms_total": ms, "launches": n, "ms_per_launch": per,
              "bytes_per_launch": byt, "bytes_model": model, "achieved_gbs": ach,
-             "frac": ach / peak if ach else None, "share": ms / total if total else None, "traffic_key": key}
+             "frac": ach / peak if ach else None, "share": ms / total if total else None, "traffic_key": key,
+             "ncu_dram_bytes_per_launch": tr["traffic_bytes"] if tr else None}
         if flops and per:
             fpk, src = fp64_peak()
             r["fp64"] = {"flops_per_launch": flops, "achieved_tflops": flops / (per / 1e3) / 1e12,

@@ -1959,8 +1959,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
                                                      int rows_per_warp = 16,
                                                      const float* __restrict__ x4 = nullptr,
                                                      float* __restrict__ y4 = nullptr,
-                                                     const float* __restrict__ rscale = nullptr,
-                                                     int use_box = 1) {
+                                                     const float* __restrict__ rscale = nullptr) {
   constexpr int S = ipow_c(5, D);
   constexpr int FF = F * F;
   constexpr int XS = chunk_len<VT>(S, F);
@@ -1982,16 +1981,6 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
   // x neighbourhood staged in the matrix precision (fp32 copies: products in
   // fp32, each 4-term partial added to the fp64 row sum)
   __shared__ __align__(16) XT xs_all[WARPS * RW][XS];
-  // BOX (3D level sweeps with fp32 twins): the fp32 x records of a chunk's
-  // whole node neighbourhood (its bounding box +-2 planes; a 64-row chunk is
-  // one 4x4x4 brick of the brick-ordered rows) are staged once per chunk with
-  // coalesced loads, so a row's neighbour gathers read shared memory and the
-  // row's chain is slots -> shared x instead of slots -> global x
-  constexpr bool BOX = HALF && sizeof(VT) <= 4 && F <= 4 && D == 3 && MODE != kSpmvY;
-  constexpr int BOXMAX = BOX ? 768 : 1;  // nodes (12 KB of float4: 8 CTAs per SM still fit)
-  __shared__ __align__(16) float4 xbox[BOXMAX];
-  __shared__ int offb[BOX ? S : 1];
-  __shared__ int bbox[8];  // lo[3], hi[3], ok
   for (int sl = threadIdx.x; sl < S; sl += blockDim.x) {
     int rs = sl, off = 0;
 #pragma unroll
@@ -2012,55 +2001,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
     // coarse levels use short chunks so that every warp gets a row)
     const int CH = (RPW > 0 ? RPW : rows_per_warp) * WARPS;
     const int nchunks = (n_act + CH - 1) / CH;
-    for (int ci = blockIdx.x; ci < nchunks; ci += gridDim.x) {
-    bool box_ok = false;
-    int bl[3] = {0, 0, 0}, bd[3] = {1, 1, 1};
-    if constexpr (BOX) {
-      if (x4 != nullptr && use_box) {
-        __syncthreads();  // the previous chunk's rows are done with xbox / offb
-        if (threadIdx.x < 3) {
-          bbox[threadIdx.x] = INT_MAX;
-          bbox[3 + threadIdx.x] = -1;
-        }
-        __syncthreads();
-        const int r1 = min(n_act, (ci + 1) * CH);
-        for (int rr = ci * CH + threadIdx.x; rr < r1; rr += blockDim.x) {
-          int idx[3];
-          unflat<D>(g, act_list[rr], idx);
-#pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            atomicMin(&bbox[a], idx[a]);
-            atomicMax(&bbox[3 + a], idx[a]);
-          }
-        }
-        __syncthreads();
-        int vol = 1;
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          bl[a] = max(0, bbox[a] - 2);
-          bd[a] = min(g.nodes[a] - 1, bbox[3 + a] + 2) - bl[a] + 1;
-          vol *= bd[a];
-        }
-        box_ok = vol <= BOXMAX;
-        if (box_ok) {
-          for (int e = threadIdx.x; e < vol; e += blockDim.x) {
-            const int i2 = e % bd[2], r = e / bd[2], i1 = r % bd[1], i0 = r / bd[1];
-            const int node = (bl[0] + i0) * g.stride[0] + (bl[1] + i1) * g.stride[1] + bl[2] + i2;
-            xbox[e] = __ldg(reinterpret_cast<const float4*>(x4) + node);
-          }
-          for (int sl = threadIdx.x; sl < S; sl += blockDim.x) {
-            int rs = sl, off = 0;
-#pragma unroll
-            for (int a = D - 1; a >= 0; --a) {
-              off = off + (rs % 5 - 2) * (a == 2 ? 1 : (a == 1 ? bd[2] : bd[1] * bd[2]));
-              rs /= 5;
-            }
-            offb[sl] = off;
-          }
-        }
-        __syncthreads();
-      }
-    }
+    for (int ci = blockIdx.x; ci < nchunks; ci += gridDim.x)
     for (int row0 = ci * CH + warp * RW; row0 < min(n_act, (ci + 1) * CH); row0 += WARPS * RW) {
       const int row = row0 + sub;
       const bool live = row < min(n_act, (ci + 1) * CH);  // the last pair may be half empty
@@ -2102,27 +2043,12 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
       // 2. stage the x records of the stored neighbours
       const uint8_t* rsl = row_slots + static_cast<int64_t>(row) * S;
       if constexpr (sizeof(VT) <= 4 && F <= 4) {
-        if (BOX && box_ok) {
-          // neighbours from the chunk's staged box
-          int kl = 0;
-          if (live) {
-            int idx[3];
-            unflat<D>(g, k, idx);
-            kl = ((idx[0] - bl[0]) * bd[1] + (idx[1] - bl[1])) * bd[2] + (idx[2] - bl[2]);
-          }
-          for (int pos = lane; pos < nzb; pos += HW) {
-            IMPM_CHECK_IDX(kl + offb[rsl[pos]], BOXMAX);
-            const float4 v = xbox[kl + offb[rsl[pos]]];
-            xs[pos * F + 0] = v.x;
-            if (F > 1) xs[pos * F + 1] = v.y;
-            if (F > 2) xs[pos * F + 2] = v.z;
-            if (F > 3) xs[pos * F + 3] = v.w;
-          }
-        } else if (x4 != nullptr) {
+        if (x4 != nullptr) {
           // fp32 twin of x, one 16-byte record per node: one load per neighbour
           for (int pos = lane; pos < nzb; pos += HW) {
-            IMPM_CHECK_IDX(k + offt[rsl[pos]], g.N);
-            const float4 v = __ldg(reinterpret_cast<const float4*>(x4) + (k + offt[rsl[pos]]));
+            const int sl = rsl[pos];
+            IMPM_CHECK_IDX(k + offt[sl], g.N);
+            const float4 v = __ldg(reinterpret_cast<const float4*>(x4) + (k + offt[sl]));
             xs[pos * F + 0] = v.x;
             if (F > 1) xs[pos * F + 1] = v.y;
             if (F > 2) xs[pos * F + 2] = v.z;
@@ -2130,16 +2056,18 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
           }
         } else {
           for (int pos = lane; pos < nzb; pos += HW) {
-            IMPM_CHECK_IDX(k + offt[rsl[pos]], g.N);
-            const int64_t nb = static_cast<int64_t>(k + offt[rsl[pos]]) * F;
+            const int sl = rsl[pos];
+            IMPM_CHECK_IDX(k + offt[sl], g.N);
+            const int64_t nb = static_cast<int64_t>(k + offt[sl]) * F;
 #pragma unroll
             for (int d = 0; d < F; ++d) xs[pos * F + d] = static_cast<XT>(__ldg(x + nb + d));
           }
         }
       } else {
         for (int pos = lane; pos < nzb; pos += HW) {
-          IMPM_CHECK_IDX(k + offt[rsl[pos]], g.N);
-          const int64_t nb = static_cast<int64_t>(k + offt[rsl[pos]]) * F;
+          const int sl = rsl[pos];
+          IMPM_CHECK_IDX(k + offt[sl], g.N);
+          const int64_t nb = static_cast<int64_t>(k + offt[sl]) * F;
 #pragma unroll
           for (int d = 0; d < F; ++d) xs[pos * F + d] = static_cast<XT>(__ldg(x + nb + d));
         }
@@ -2215,7 +2143,6 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC 
         }
       }
       __syncwarp();
-    }
     }
   }
   if (partials) block_sum_store<1>(part, partials);

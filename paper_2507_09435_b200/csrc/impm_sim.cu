@@ -284,8 +284,6 @@ struct Sim {
   // fine-level smoother matrix in fp16 with fp32 row scales (IMPM_MG_F16=0: fp32)
   bool mg_f16 = !(std::getenv("IMPM_MG_F16") && std::atoi(std::getenv("IMPM_MG_F16")) == 0);
   // fp32 twins of the V-cycle iterates feed the fp32 level SpMV gathers
-  // level sweeps stage each row chunk's x neighbourhood in shared memory (IMPM_MG_BOX=0: per-row gathers)
-  bool mg_box = !(std::getenv("IMPM_MG_BOX") && std::atoi(std::getenv("IMPM_MG_BOX")) == 0);
   bool mg_x4 = !(std::getenv("IMPM_MG_X4") && std::atoi(std::getenv("IMPM_MG_X4")) == 0);
   bool krylov_debug = std::getenv("IMPM_DEBUG_KRYLOV") != nullptr;
   bool res_staged = !(std::getenv("IMPM_RES_UNSTAGED") && std::atoi(std::getenv("IMPM_RES_UNSTAGED")) != 0);
@@ -1300,12 +1298,11 @@ struct Sim {
       k_spmv<DD, FE, W, MODE, __half, 0, true><<<grid, W * 32, 0, s>>>(
           L.g, L.act_list, L.n_act, L.vals16, L.row_len16, L.row_slots, L.row_nzb, x, L.freem, y, dotv, parts, dflag.p,
           b, L.dinv, omega, rpw, mg_x4 ? L.twin(x) : nullptr, mg_x4 && MODE == kSpmvJacobi ? L.twin(y) : nullptr,
-          L.rscale, mg_box ? 1 : 0);
+          L.rscale);
     else if (mg_f32 && L.n_act >= 50000)
       k_spmv<DD, FE, W, MODE, float, 0, true><<<grid, W * 32, 0, s>>>(
           L.g, L.act_list, L.n_act, L.vals32, L.row_len32, L.row_slots, L.row_nzb, x, L.freem, y, dotv, parts, dflag.p,
-          b, L.dinv, omega, rpw, mg_x4 ? L.twin(x) : nullptr, mg_x4 && MODE == kSpmvJacobi ? L.twin(y) : nullptr,
-          nullptr, mg_box ? 1 : 0);
+          b, L.dinv, omega, rpw, mg_x4 ? L.twin(x) : nullptr, mg_x4 && MODE == kSpmvJacobi ? L.twin(y) : nullptr);
     else if (mg_f32)
       k_spmv<DD, FE, W, MODE, float, 0><<<grid, W * 32, 0, s>>>(L.g, L.act_list, L.n_act, L.vals32, L.row_len32,
                                                                    L.row_slots, L.row_nzb, x, L.freem, y, dotv, parts,

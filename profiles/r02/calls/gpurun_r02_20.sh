@@ -1,0 +1,14 @@
+# round 2: assembly with 16-byte tangent broadcasts; A/B vs previous build not possible in-process -> bench + suite + ncu of the assembly
+bench_line() {
+  env $1 timeout 900 python bench.py --steps 3 --warmup 3 --no-cpu --e2e-steps 0 > gpurun_out/ab.json 2> gpurun_out/ab.err
+  echo "[$1] rc=$? $(python -c "
+import json; d=json.load(open('gpurun_out/ab.json')); k=d['kernel_ms']; n=d['kernel_launches_by_class']
+print('it/s %.2f ms/step %.1f spmv %.3f ms vcycle_l0 %.3f ms/scope vcycle %.1f ms assemble %.2f tangent %.2f kry %d' % (d['value'], d['ms_per_step'], k['spmv']/n['spmv'], k['vcycle_level0']/n['vcycle_level0'], k['vcycle'], k['assemble']/n['assemble'], k['tangent']/n['tangent'], d['krylov_iterations']))")"
+}
+bench_line ""
+timeout 1800 python -m pytest tests -m gpu -q > gpurun_out/gpu_tests_20.log 2>&1; echo "tests rc=$?"; tail -3 gpurun_out/gpu_tests_20.log
+python scripts/profile_step.py cfg4 2 > gpurun_out/plain.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:k_assemble_bins_staged" --launch-skip 94 -c 1 -o gpurun_out/prof_asm2 -f python scripts/profile_step.py cfg4 2 > gpurun_out/asm2.log 2>&1
+python scripts/ncu_summary.py gpurun_out/prof_asm2.ncu-rep > gpurun_out/asm2.md; tail -1 gpurun_out/asm2.md
+ncu -i gpurun_out/prof_asm2.ncu-rep --page raw --csv > gpurun_out/asm2_raw.csv 2>/dev/null; ncu -i gpurun_out/prof_asm2.ncu-rep --page source --csv --print-source sass > gpurun_out/asm2_sass.csv 2>/dev/null
+gzip -f gpurun_out/asm2_raw.csv gpurun_out/asm2_sass.csv; rm -f gpurun_out/prof_asm2.ncu-rep
