@@ -10,7 +10,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libimpm_gpu.so")
+LIB_PATH = os.environ.get("IMPM_LIB") or os.path.join(HERE, "libimpm_gpu.so")  # IMPM_LIB: A/B builds only
 
 c_int32, c_int64, c_double, c_void_p = ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p
 

@@ -45,11 +45,12 @@ def up_to_date():
     return all(os.path.getmtime(s) <= t for s in sources())
 
 
-def build(force=False, verbose=False):
-    if not force and up_to_date():
+def build(force=False, verbose=False, out=None):
+    """out: another library path (A/B builds with IMPM_NVCC_EXTRA, loaded through IMPM_LIB)."""
+    if out is None and not force and up_to_date():
         return OUT
     extra = os.environ.get("IMPM_NVCC_EXTRA", "").split()  # tuning experiments (e.g. -DIMPM_ASM_PPL3=2)
-    cmd = [NVCC, *FLAGS, *extra, "-o", OUT, SRC, *nccl_flags()]
+    cmd = [NVCC, *FLAGS, *extra, "-o", out or OUT, SRC, *nccl_flags()]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)
@@ -79,4 +80,6 @@ def build_bar_swap(force=False):
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    # python -m paper_2507_09435_b200.build [--force] [--out PATH]
+    o = sys.argv[sys.argv.index("--out") + 1] if "--out" in sys.argv else None
+    build(force="--force" in sys.argv, verbose=True, out=o)

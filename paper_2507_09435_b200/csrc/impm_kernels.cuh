@@ -935,77 +935,82 @@ __global__ void k_tangent(GridC g, const double* __restrict__ pd, int64_t cap, i
 // ~900 flops per particle instead of nine dual-number passes of the stress
 // update; A is written through a per-warp transpose in contiguous 216-byte
 // runs (one output direction d at a time), same layout as k_tangent.
+// The neo-Hookean factors of one particle at displacement u: Fi = f^-1,
+// X = Fi b, Y = Fi b Fi^T, Z = tau Fi^T (false when det F <= 0).
+template <int SHAPE>
+__device__ __forceinline__ bool nh3_factors(const GridC& g, const double* __restrict__ pd, int64_t cap,
+                                            const double* __restrict__ xs, int p, int key, int sup,
+                                            const double* __restrict__ u, double lam, double mu, int tl, double* Fi,
+                                            double* X, double* Y, double* Z, double& V0) {
+  constexpr int D = 3;
+  int first[3], cnt[3];
+  AxisW aw[3];
+  particle_weights<D, SHAPE>(g, pd, cap, xs, p, key, sup, first, cnt, aw);
+  Mat<double, D> G = Mat<double, D>::zero();
+  for_each_support<D>(g, first, cnt, aw, [&](int node, double, const double* grad) {
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      const double uc = u[node * D + c];
+#pragma unroll
+      for (int a = 0; a < D; ++a) G(c, a) += uc * grad[a];
+    }
+  });
+  Mat<double, D> f = G;
+#pragma unroll
+  for (int a = 0; a < D; ++a) f(a, a) += 1.0;
+  Mat<double, D> F = f;
+  if (!tl) {
+    Mat<double, D> Fn;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) Fn.e[i] = pd[(PF<D>::F + i) * cap + p];
+    F = matmul(f, Fn);
+  }
+  const double J = det(F);
+  V0 = pd[PF<D>::V0 * cap + p];
+  if (!(J > 0.0)) return false;
+  const Mat<double, D> fi = inverse(f);
+  const Mat<double, D> b = matmul(F, transpose(F));
+  const double lnJ = log(J);
+#pragma unroll
+  for (int i = 0; i < 9; ++i) Fi[i] = fi.e[i];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      double x = 0.0;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) x += fi(i, a) * b(a, j);
+      X[i * 3 + j] = x;  // (Fi b)_ij
+    }
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      double y = 0.0, z = 0.0;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        y += X[i * 3 + a] * fi(j, a);  // (Fi b Fi^T)_ij
+        const double tau = mu * (b(i, a) - (i == a ? 1.0 : 0.0)) + (i == a ? lam * lnJ : 0.0);
+        z += tau * fi(j, a);  // (tau Fi^T)_ij
+      }
+      Y[i * 3 + j] = y;
+      Z[i * 3 + j] = z;
+    }
+  return true;
+}
+
 template <int SHAPE>
 __global__ void __launch_bounds__(128) k_tangent_nh3(GridC g, const double* __restrict__ pd, int64_t cap, int P,
                                                      const double* __restrict__ xs, const int* __restrict__ key,
                                                      const int* __restrict__ sup, const double* __restrict__ u,
                                                      MatParams mp, int tl, double* __restrict__ A) {
-  constexpr int D = 3;
   __shared__ double tb[4][32][28];  // [warp][particle][27 values of one direction d] (+1 pad)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int p0 = (blockIdx.x * 4 + warp) * 32;
   const int p = p0 + lane;
-  const bool live = p < P;
   double Fi[9] = {}, Y[9] = {}, X[9] = {}, Z[9] = {}, V0 = 0.0;
   const double lam = mp.lam, mu = mp.mu;
-  bool ok = false;
-  if (live) {
-    int first[3], cnt[3];
-    AxisW aw[3];
-    particle_weights<D, SHAPE>(g, pd, cap, xs, p, key[p], sup[p], first, cnt, aw);
-    Mat<double, D> G = Mat<double, D>::zero();
-    for_each_support<D>(g, first, cnt, aw, [&](int node, double, const double* grad) {
-#pragma unroll
-      for (int c = 0; c < D; ++c) {
-        const double uc = u[node * D + c];
-#pragma unroll
-        for (int a = 0; a < D; ++a) G(c, a) += uc * grad[a];
-      }
-    });
-    Mat<double, D> f = G;
-#pragma unroll
-    for (int a = 0; a < D; ++a) f(a, a) += 1.0;
-    Mat<double, D> F = f;
-    if (!tl) {
-      Mat<double, D> Fn;
-#pragma unroll
-      for (int i = 0; i < 9; ++i) Fn.e[i] = pd[(PF<D>::F + i) * cap + p];
-      F = matmul(f, Fn);
-    }
-    const double J = det(F);
-    V0 = pd[PF<D>::V0 * cap + p];
-    if (J > 0.0) {
-      ok = true;
-      const Mat<double, D> fi = inverse(f);
-      const Mat<double, D> b = matmul(F, transpose(F));
-      const double lnJ = log(J);
-#pragma unroll
-      for (int i = 0; i < 9; ++i) Fi[i] = fi.e[i];
-#pragma unroll
-      for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int j = 0; j < 3; ++j) {
-          double x = 0.0;
-#pragma unroll
-          for (int a = 0; a < 3; ++a) x += fi(i, a) * b(a, j);
-          X[i * 3 + j] = x;  // (Fi b)_ij
-        }
-#pragma unroll
-      for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int j = 0; j < 3; ++j) {
-          double y = 0.0, z = 0.0;
-#pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            y += X[i * 3 + a] * fi(j, a);  // (Fi b Fi^T)_ij
-            const double tau = mu * (b(i, a) - (i == a ? 1.0 : 0.0)) + (i == a ? lam * lnJ : 0.0);
-            z += tau * fi(j, a);  // (tau Fi^T)_ij
-          }
-          Y[i * 3 + j] = y;
-          Z[i * 3 + j] = z;
-        }
-    }
-  }
+  const bool ok = p < P && nh3_factors<SHAPE>(g, pd, cap, xs, p, key[p], sup[p], u, lam, mu, tl, Fi, X, Y, Z, V0);
   double* tw = &tb[warp][0][0];
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
@@ -1028,6 +1033,48 @@ __global__ void __launch_bounds__(128) k_tangent_nh3(GridC g, const double* __re
       if (lane < 27) A[static_cast<int64_t>(p0 + q) * 81 + d * 27 + lane] = tw[q * 28 + lane];
     __syncwarp();
   }
+}
+
+// Factored form of the same tangent for the 3D neo-Hookean assembly
+// (k_assemble_nh3f). With v = Fi^T g and Fi b Fi^T = (Fi F)(Fi F)^T = Fn Fn^T
+// (Fn = I total Lagrangian), the four terms of dP/dG above contract with the
+// node gradients g^k (index b) and g^l (index f) to
+//   J_kl = sum_p [ (e_k . e_l) I + w_l v_k^T + V0 lam v_k v_l^T ],
+//   e = sqrt(V0 mu) Fn^T g,  w = V0 (mu X^T - Z) g,
+// so per particle the assembly needs Q = {Fi, sqrt(V0 mu) Fn^T, V0 (mu X^T - Z),
+// V0 lam} (28 doubles) instead of the 81 entries of dP/dG. Same values as
+// sum_bf g^k_b A[cb][df] g^l_f up to rounding. (Carrying the particle's 1D
+// weights in Q as well, 46 doubles, measured slower: 19.8 vs 19.4 ms per cfg 4
+// tangent + assembly, and 20.0 with Q component-major.)
+constexpr int kNhQ = 28;
+template <int SHAPE>
+__global__ void __launch_bounds__(128) k_tangent_nh3q(GridC g, const double* __restrict__ pd, int64_t cap, int P,
+                                                      const double* __restrict__ xs, const int* __restrict__ key,
+                                                      const int* __restrict__ sup, const double* __restrict__ u,
+                                                      MatParams mp, int tl, double* __restrict__ Q) {
+  __shared__ double tb[4][32 * kNhQ];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int p0 = (blockIdx.x * 4 + warp) * 32;
+  const int p = p0 + lane;
+  double Fi[9] = {}, Y[9] = {}, X[9] = {}, Z[9] = {}, V0 = 0.0;
+  const double lam = mp.lam, mu = mp.mu;
+  const bool ok = p < P && nh3_factors<SHAPE>(g, pd, cap, xs, p, key[p], sup[p], u, lam, mu, tl, Fi, X, Y, Z, V0);
+  const double sq = ok ? sqrt(V0 * mu) : 0.0;
+  double* q = &tb[warp][lane * kNhQ];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const double fn = tl ? (i == j ? 1.0 : 0.0) : (ok ? pd[(PF<3>::F + j * 3 + i) * cap + p] : 0.0);
+      q[i * 3 + j] = ok ? Fi[i * 3 + j] : 0.0;
+      q[9 + i * 3 + j] = sq * fn;                                                 // E[i][j] = sqrt(V0 mu) Fn_ji
+      q[18 + i * 3 + j] = ok ? V0 * (mu * X[j * 3 + i] - Z[i * 3 + j]) : 0.0;  // [c][f]
+    }
+  q[27] = ok ? V0 * lam : 0.0;
+  __syncwarp();
+  // the warp's 32 records are one contiguous run
+  const int nq = min(32, P - p0) * kNhQ;
+  for (int e = lane; e < nq; e += 32) Q[static_cast<int64_t>(p0) * kNhQ + e] = tb[warp][e];
 }
 
 // ------------------------------------------- K6 Jacobian: structure ------
@@ -1127,6 +1174,14 @@ __device__ __forceinline__ int mask_pos(const unsigned* m, int sl) {
 __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src) {
   const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem_dst, const void* gmem_src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gmem_src) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
@@ -1705,6 +1760,285 @@ __global__ void __launch_bounds__(WARPS * 32, D == 3 ? (RMW ? 2 : IMPM_ASM_MINB)
   }
 }
 
+// 3D neo-Hookean assembly on the factored tangent (k_tangent_nh3q): same
+// colour batches, bins and block addressing as k_assemble_bins_staged (upper
+// blocks, SYM), but one CTA per bin and one block pair (k, l >= k) per thread.
+// For the bin's particles the CTA builds, per (particle, box node), e, v and
+// w (k_tangent_nh3q) in shared memory, component-major with the node index
+// fastest (the pair loop's loads are conflict-free); a pair then costs 24 FMA
+// per particle instead of the g^k A g^l contraction over 81 tangent entries.
+// The bins of a CTA are software-pipelined: while bin j is assembled, the
+// row indices of bin j+2 and the row masks, factors Q, positions and sizes of
+// bin j+1 are in flight as asynchronous copies (LDGSTS), so a bin's chain of
+// dependent loads (bin -> rows -> masks, bin -> particles) is off the
+// critical path. Bins with more than PCH particles stage chunk by chunk.
+// MIRROR: also add K_kl^T into row l (slabs); false: k_mirror_lower fills the
+// lower blocks.
+#ifndef IMPM_ASMF_WARPS
+#define IMPM_ASMF_WARPS 3  // 96 threads: 171 pairs of an 18-node box in 2 rounds, 378 (27 nodes) in 4
+#endif
+#ifndef IMPM_ASMF_MINB
+#define IMPM_ASMF_MINB 9  // 72 registers, 9 x 25 KB shared per SM (8: 80 registers, 18.3 vs 18.0 ms per cfg 4 Jacobian)
+#endif
+struct BinHdr {
+  int fl, p0, p1;
+};
+template <int SHAPE, int WARPS, int PCH, bool MIRROR>
+__global__ void __launch_bounds__(WARPS * 32, IMPM_ASMF_MINB) k_assemble_nh3f(
+    GridC g, const double* __restrict__ pd, int64_t cap, const double* __restrict__ xs,
+    const int* __restrict__ bin_start, const uint8_t* __restrict__ bflag, const double* __restrict__ Q,
+    const int* __restrict__ act_idx, const unsigned* __restrict__ row_mask, const int* __restrict__ row_nzb,
+    double* __restrict__ vals, int64_t row_len, int c0, int c1, int c2, int nb0, int nb1, int nb2) {
+  constexpr int D = 3, NK = 27, NT = WARPS * 32;
+  __shared__ double T[PCH][9][NK];     // [particle][e0..2 v0..2 w0..2][box node]
+  __shared__ double Qs[2][PCH][kNhQ];  // factors of the bin's particles (double-buffered)
+  __shared__ double XL[2][PCH][6];     // positions and half sizes (double-buffered)
+  __shared__ double W1[PCH][D][3][2];  // 1D weights [particle][axis][node][w|dw]
+  __shared__ int Hs[3][4];             // bin header: bflag word, first particle, end
+  __shared__ int Ridx[3][NK];          // row of each node of the 3x3x3 superset box (-1: none)
+  __shared__ uint4 Rmask[2][NK];
+  __shared__ int Rnzb[2][NK];
+  // index tables (no runtime integer division in the per-bin code): box
+  // shape code cc = 4 (cn0 - 2) + 2 (cn1 - 2) + (cn2 - 2); local node -> its
+  // superset index; superset index -> packed axis offsets and its 5^3 slot base
+  __shared__ uint8_t s_sup[8][NK];
+  __shared__ uint8_t s_lpk[NK];
+  __shared__ uint8_t s_b25[NK];
+  const int tid = threadIdx.x;
+  for (int e = tid; e < 8 * NK; e += NT) {
+    const int cc = e / NK, kk = e - cc * NK;
+    const int n0 = 2 + (cc >> 2), n1 = 2 + ((cc >> 1) & 1), n2 = 2 + (cc & 1);
+    const int l2 = kk % n2, l1 = (kk / n2) % n1, l0 = kk / (n2 * n1);
+    s_sup[cc][kk] = static_cast<uint8_t>(kk < n0 * n1 * n2 ? l0 * 9 + l1 * 3 + l2 : 0);
+  }
+  for (int e = tid; e < NK; e += NT) {
+    const int l0 = e / 9, l1 = (e / 3) % 3, l2 = e % 3;
+    s_lpk[e] = static_cast<uint8_t>(l0 | (l1 << 2) | (l2 << 4));
+    s_b25[e] = static_cast<uint8_t>(l0 * 25 + l1 * 5 + l2);
+  }
+  // (visible after the first __syncthreads below)
+  const int nbins = nb0 * nb1 * nb2;
+  const int G = gridDim.x;
+  auto bin_node = [&](int bi, int* bidx) {
+    int r = bi;
+    bidx[2] = 3 * (r % nb2) + c2;
+    r /= nb2;
+    bidx[1] = 3 * (r % nb1) + c1;
+    bidx[0] = 3 * (r / nb1) + c0;
+    return bidx[0] * g.stride[0] + bidx[1] * g.stride[1] + bidx[2] * g.stride[2];
+  };
+  auto read_hdr = [&](int bi, int buf) {
+    BinHdr h{0, 0, 0};
+    if (bi < nbins) {
+      int bidx[3];
+      const int b = bin_node(bi, bidx);
+      h.fl = (Hs[buf][0] >> (8 * (b & 3))) & 0xff;
+      h.p0 = Hs[buf][1];
+      h.p1 = Hs[buf][2];
+    }
+    return h;
+  };
+  // stage A (depends on the bin index only): the bin's header and the rows of
+  // the superset box nodes
+  auto issue_rows = [&](int bi, int buf) {
+    if (bi < nbins && tid < NK) {
+      int bidx[3];
+      const int b = bin_node(bi, bidx);
+      if (tid == 0) cp_async4(&Hs[buf][0], bflag + (b & ~3));  // the aligned word holding the flag byte
+      if (tid == 1) cp_async4(&Hs[buf][1], bin_start + b);
+      if (tid == 2) cp_async4(&Hs[buf][2], bin_start + b + 1);
+      const int i0 = tid / 9, i1 = (tid / 3) % 3, i2 = tid % 3;
+      if (bidx[0] + i0 < g.nodes[0] && bidx[1] + i1 < g.nodes[1] && bidx[2] + i2 < g.nodes[2])
+        cp_async4(&Ridx[buf][tid],
+                  act_idx + (bidx[0] + i0) * g.stride[0] + (bidx[1] + i1) * g.stride[1] + bidx[2] + i2);
+      else
+        Ridx[buf][tid] = -1;
+    }
+  };
+  // stage B: masks of those rows + the particles of a resident bin (needs stage A and the header)
+  auto issue_data = [&](const BinHdr& h, int abuf, int buf) {
+    if (!(h.fl & 0x80)) return;
+    if (tid < NK) {
+      const int rw = Ridx[abuf][tid];
+      if (rw >= 0) {
+        cp_async16(&Rmask[buf][tid], row_mask + static_cast<int64_t>(rw) * 4);
+        cp_async4(&Rnzb[buf][tid], row_nzb + rw);
+      }
+    }
+    const int np = h.p1 - h.p0;
+    if (np <= PCH) {
+      for (int e = tid; e < np * kNhQ; e += NT)
+        cp_async8(&Qs[buf][0][0] + e, Q + static_cast<int64_t>(h.p0) * kNhQ + e);
+      for (int e = tid; e < np * 6; e += NT) {
+        const int pl = e / 6, jj = e - pl * 6;
+        const int p = h.p0 + pl;
+        cp_async8(&XL[buf][pl][jj], jj < 3 ? xs + jj * cap + p : pd + (PF<D>::lp + jj - 3) * cap + p);
+      }
+    }
+  };
+  // the staged particles (Qs/XL[buf], np of them) -> 1D weights -> T
+  auto build_table = [&](int np, int buf, const int* bidx, const int* cn, int nk, int cc) {
+    for (int e = tid; e < np * D * 3; e += NT) {
+      const int pl = e / (D * 3), rem = e - pl * D * 3, a = rem / 3, i = rem - a * 3;
+      // (selects instead of runtime-indexed grid arrays: no stack frame)
+      const int cna = a == 0 ? cn[0] : (a == 1 ? cn[1] : cn[2]);
+      const int ba = a == 0 ? bidx[0] + g.base0 : (a == 1 ? bidx[1] : bidx[2]);
+      const double oa = a == 0 ? g.origin[0] : (a == 1 ? g.origin[1] : g.origin[2]);
+      double w = 0.0, dw = 0.0;
+      if (i < cna) {
+        // node_coord (grid.hpp:180-185) with the selected axis
+        const double xn = __dadd_rn(oa, __dmul_rn(static_cast<double>(ba + i), g.h));
+        const WeightValue wv = weight_1d<SHAPE>(XL[buf][pl][a] - xn, XL[buf][pl][3 + a], g.h);
+        w = wv.w;
+        dw = wv.dw;
+      }
+      W1[pl][a][i][0] = w;
+      W1[pl][a][i][1] = dw;
+    }
+    __syncthreads();
+    const unsigned mg = 0xFFFFFFFFu / static_cast<unsigned>(nk) + 1u;  // e / nk = umulhi(e, mg) for e < 2^16
+    for (int e = tid; e < np * nk; e += NT) {
+      const int pl = static_cast<int>(__umulhi(static_cast<unsigned>(e), mg)), k = e - pl * nk;
+      const int pk = s_lpk[s_sup[cc][k]];
+      const int l0 = pk & 3, l1 = (pk >> 2) & 3, l2 = pk >> 4;
+      const double w[3] = {W1[pl][0][l0][0], W1[pl][1][l1][0], W1[pl][2][l2][0]};
+      const double dw[3] = {W1[pl][0][l0][1], W1[pl][1][l1][1], W1[pl][2][l2][1]};
+      double W, gk[3];
+      tensor_weight<D>(w, dw, W, gk);
+      const double* q = Qs[buf][pl];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        double v = 0.0, ee = 0.0, ww = 0.0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          v = fma(q[a * 3 + i], gk[a], v);         // (Fi^T g)_i
+          ee = fma(q[9 + i * 3 + a], gk[a], ee);   // (sqrt(V0 mu) Fn^T g)_i
+          ww = fma(q[18 + i * 3 + a], gk[a], ww);  // (V0 (mu X^T - Z) g)_i
+        }
+        T[pl][i][k] = ee;
+        T[pl][3 + i][k] = v;
+        T[pl][6 + i][k] = ww;
+      }
+    }
+    __syncthreads();
+  };
+
+  int bi = blockIdx.x;
+  issue_rows(bi, 0);
+  issue_rows(bi + G, 1);
+  cp_async_wait_all();
+  __syncthreads();
+  issue_data(read_hdr(bi, 0), 0, 0);
+  for (int j = 0; bi < nbins; ++j, bi += G) {
+    const int ab = j % 3, db = j & 1;
+    cp_async_wait_all();
+    __syncthreads();  // this bin's stage B and the next bin's stage A have landed; bin j-1 is done
+    const BinHdr hc = read_hdr(bi, ab);
+    issue_data(read_hdr(bi + G, (j + 1) % 3), (j + 1) % 3, db ^ 1);
+    issue_rows(bi + 2 * G, (j + 2) % 3);
+    if (hc.fl & 0x80) {
+      int bidx[3], cn[3];
+      bin_node(bi, bidx);
+#pragma unroll
+      for (int a = 0; a < D; ++a) cn[a] = 2 + ((hc.fl >> a) & 1);
+      const int nk = cn[0] * cn[1] * cn[2];
+      const int cc = ((hc.fl & 1) << 2) | (hc.fl & 2) | ((hc.fl >> 2) & 1);
+      const int ntasks = nk * (nk + 1) / 2;
+      const bool resident = hc.p1 - hc.p0 <= PCH;
+      if (resident) build_table(hc.p1 - hc.p0, db, bidx, cn, nk, cc);
+      for (int r0 = 0; r0 < ntasks; r0 += NT) {
+        // this thread's pair: row-major over k, l = k .. nk-1
+        const int task = r0 + tid;
+        const bool has = task < ntasks;
+        int tk = 0, tl = 0;
+        if (has) {
+          // row k of the upper triangle starts at off(k) = k nk - k (k - 1) / 2:
+          // the root of off(k) = task, then an exact integer correction
+          const float b2 = static_cast<float>(2 * nk + 1);
+          tk = static_cast<int>(0.5f * (b2 - sqrtf(b2 * b2 - 8.0f * static_cast<float>(task))));
+          tk = max(0, min(nk - 1, tk));
+          if (tk * nk - tk * (tk - 1) / 2 > task) --tk;
+          if ((tk + 1) * nk - (tk + 1) * tk / 2 <= task) ++tk;
+          tl = tk + task - (tk * nk - tk * (tk - 1) / 2);
+        }
+        double acc[9];
+#pragma unroll
+        for (int e = 0; e < 9; ++e) acc[e] = 0.0;
+        for (int pc = hc.p0; pc < hc.p1; pc += PCH) {
+          const int np = min(PCH, hc.p1 - pc);
+          if (!resident) {
+            // chunk by chunk, synchronously, in this bin's half of the double
+            // buffers (the other half holds the next bin's copies)
+            __syncthreads();
+            for (int e = tid; e < np * kNhQ; e += NT)
+              (&Qs[db][0][0])[e] = __ldg(Q + static_cast<int64_t>(pc) * kNhQ + e);
+            for (int e = tid; e < np * 6; e += NT) {
+              const int pl = e / 6, jj = e - pl * 6;
+              XL[db][pl][jj] = jj < 3 ? xs[jj * cap + pc + pl] : pd[(PF<D>::lp + jj - 3) * cap + pc + pl];
+            }
+            __syncthreads();
+            build_table(np, db, bidx, cn, nk, cc);
+          }
+          if (has) {
+            for (int pl = 0; pl < np; ++pl) {
+              const double lv = Qs[db][pl][27];
+              double ek[3], vk[3], el[3], vl[3], wl[3];
+#pragma unroll
+              for (int i = 0; i < 3; ++i) {
+                ek[i] = T[pl][i][tk];
+                vk[i] = T[pl][3 + i][tk];
+                el[i] = T[pl][i][tl];
+                vl[i] = T[pl][3 + i][tl];
+                wl[i] = T[pl][6 + i][tl];
+              }
+              const double sk = fma(ek[0], el[0], fma(ek[1], el[1], ek[2] * el[2]));
+#pragma unroll
+              for (int c = 0; c < 3; ++c) {
+                const double Lc = lv * vk[c];
+#pragma unroll
+                for (int d = 0; d < 3; ++d) acc[c * 3 + d] = fma(wl[c], vk[d], fma(Lc, vl[d], acc[c * 3 + d]));
+                acc[c * 3 + c] += sk;
+              }
+            }
+          }
+        }
+        if (has) {
+          const int sk9 = s_sup[cc][tk], sl9 = s_sup[cc][tl];
+          const int sl = 62 + s_b25[sl9] - s_b25[sk9];  // slot of the offset l - k in the 5^3 box
+          const int row = Ridx[ab][sk9];
+          if (row >= 0) {
+            const uint4 m4 = Rmask[db][sk9];
+            const unsigned rm[4] = {m4.x, m4.y, m4.z, m4.w};
+            const int cp = cpad(Rnzb[db][sk9], D);
+            IMPM_CHECK_IDX((D - 1) * cp + mask_pos_r(rm, sl) * D + D - 1, row_len);
+            double* rv = vals + static_cast<int64_t>(row) * row_len + mask_pos_r(rm, sl) * D;
+#pragma unroll
+            for (int c = 0; c < D; ++c)
+#pragma unroll
+              for (int d = 0; d < D; ++d) atomicAdd(rv + c * cp + d, acc[c * D + d]);
+          }
+          if constexpr (MIRROR) {
+            const int rowl = Ridx[ab][sl9];
+            if (tl != tk && rowl >= 0) {
+              const int slm = 124 - sl;  // the mirrored offset k - l
+              const uint4 m4 = Rmask[db][sl9];
+              const unsigned ml[4] = {m4.x, m4.y, m4.z, m4.w};
+              const int cpl = cpad(Rnzb[db][sl9], D);
+              IMPM_CHECK_IDX((D - 1) * cpl + mask_pos_r(ml, slm) * D + D - 1, row_len);
+              double* rv = vals + static_cast<int64_t>(rowl) * row_len + mask_pos_r(ml, slm) * D;
+#pragma unroll
+              for (int c = 0; c < D; ++c)
+#pragma unroll
+                for (int d = 0; d < D; ++d) atomicAdd(rv + c * cpl + d, acc[d * D + c]);
+            }
+          }
+        }
+      }
+    }
+  }
+  cp_async_wait_all();  // no copy outlives the CTA
+}
+
 // Lower blocks of a symmetric J from the upper ones (the assembly ran with
 // MIRROR = false): K_ab = K_ba^T for flat(b) < flat(a). One warp per row.
 // First each lane resolves one lower block's source (row b, position of
@@ -1946,8 +2280,11 @@ __host__ __device__ constexpr int64_t row_len_of(int S, int F) {
 #define IMPM_HW16 16  // 8 measured slower (level 0: 49 vs 41 ms per load step)
 #endif
 constexpr int HW16 = IMPM_HW16;  // lanes per fp16 row on the big levels
+#ifndef IMPM_SPMV_HALF_MINB
+#define IMPM_SPMV_HALF_MINB 8  // resident 4-warp CTAs per SM the half-warp (level) variants are compiled for
+#endif
 template <int D, int F, int WARPS, int MODE = kSpmvY, class VT = double, int RPW = 16, bool HALF = false>
-__global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32)) k_spmv(GridC g, const int* __restrict__ act_list, int n_act,
+__global__ void __launch_bounds__(WARPS * 32, HALF ? IMPM_SPMV_HALF_MINB : 1024 / (WARPS * 32)) k_spmv(GridC g, const int* __restrict__ act_list, int n_act,
                                                      const VT* __restrict__ vals, int64_t row_len,
                                                      const uint8_t* __restrict__ row_slots,
                                                      const int* __restrict__ row_nzb,

@@ -239,6 +239,7 @@ struct Sim {
   DBuf<double> uty;  // accumulated vertical displacement per particle (sorted order)
 
   int spmv_blocks = kSpmvBlocks;
+  int mg_blocks = kSpmvBlocks;  // grid of the level sweeps without dot partials
   // the MG preconditioner streams fp32 copies of its level matrices (the
   // outer Krylov SpMV stays fp64, so the solve tolerance is unaffected)
   bool mg_f32 = true;
@@ -275,6 +276,8 @@ struct Sim {
   bool tangent_analytic = !(std::getenv("IMPM_TANGENT_DUAL") && std::atoi(std::getenv("IMPM_TANGENT_DUAL")) != 0);
   bool asm_rmw = std::getenv("IMPM_ASM_RMW") && std::atoi(std::getenv("IMPM_ASM_RMW")) != 0;
   bool asm_sym = !(std::getenv("IMPM_ASM_SYM") && std::atoi(std::getenv("IMPM_ASM_SYM")) == 0);
+  // 3D neo-Hookean: factored tangent + pair-per-thread assembly (IMPM_ASM_NHF=0: dP/dG + k_assemble_bins_staged)
+  bool asm_nhf = !(std::getenv("IMPM_ASM_NHF") && std::atoi(std::getenv("IMPM_ASM_NHF")) == 0);
   // symmetric J: upper blocks in the colour launches, lower ones by one
   // transpose pass (IMPM_ASM_MIRROR_PASS=0: mirrored REDs in the kernel). A
   // slab's halo nodes are not rows, so slabs keep the in-kernel mirror.
@@ -449,6 +452,9 @@ struct Sim {
     if (const char* e = std::getenv("IMPM_TANGENT_K1")) tangent_k1 = std::atoi(e) != 0;
     if (const char* e = std::getenv("IMPM_SPMV_BLOCKS"))  // tuning experiments only
       spmv_blocks = std::max(1, std::min(kSpmvMaxBlocks, std::atoi(e)));
+    mg_blocks = spmv_blocks;
+    if (const char* e = std::getenv("IMPM_MG_BLOCKS"))  // tuning experiments only
+      mg_blocks = std::max(1, std::min(kSpmvMaxBlocks, std::atoi(e)));
     sums.ensure(8);
     CK(cudaMallocHost(&h_st, sizeof(DevStatus)));
     CK(cudaMallocHost(&h_sc, sizeof(double) * kNSlots));
@@ -1039,6 +1045,10 @@ struct Sim {
   }
 
   // ------------------------------------------------------ Jacobian (K6)
+  // the factored 3D neo-Hookean path (k_tangent_nh3q + k_assemble_nh3f)
+  bool nhf_path(const MatParams& mp) const {
+    return D == 3 && mp.kind == kNeoHookean && tangent_analytic && asm_nhf && asm_sym && !asm_rmw;
+  }
   void jacobian_dev(const double* ud) {
     if (coupled) return jacobian_up(ud, up_dt);
     halo(ud);
@@ -1050,7 +1060,10 @@ struct Sim {
         constexpr int K = DD == 3 ? 3 : DD * DD;
         // plastic kinds (one return map per pass) take K = 3 directions per pass in 3D
         const bool nho = mp.kind == kNeoHookean;
-        if (DD == 3 && nho && tangent_analytic)
+        if (DD == 3 && nhf_path(mp))
+          k_tangent_nh3q<SH><<<blocks_for(P, 128), 128, 0, s>>>(g, pd.p, cap, P, xs.p, key.p, sup.p, ud, mp,
+                                                                opt.total_lagrangian, Atan.p);
+        else if (DD == 3 && nho && tangent_analytic)
           k_tangent_nh3<SH><<<blocks_for(P, 128), 128, 0, s>>>(g, pd.p, cap, P, xs.p, key.p, sup.p, ud, mp,
                                                                opt.total_lagrangian, Atan.p);
         else if (DD == 3 && tangent_k1 && nho)
@@ -1104,6 +1117,22 @@ struct Sim {
             kern<<<grid, WS * 32, dyn, s>>>(g, pd.p, cap, xs.p, bin_start.p, bflag.p, Atan.p, act_idx.p, row_mask.p,
                                             row_nzb.p, vals.p, row_len, cc[0], cc[1], cc[2], nb[0], nb[1], nb[2]);
           };
+          if constexpr (DD == 3) {
+            if (nhf_path(mp)) {
+              constexpr int WF = IMPM_ASMF_WARPS;
+              const unsigned gridf = static_cast<unsigned>(std::min(nbins, 148 * 32));
+              if (mirror_pass)
+                k_assemble_nh3f<SH, WF, 8, false><<<gridf, WF * 32, 0, s>>>(
+                    g, pd.p, cap, xs.p, bin_start.p, bflag.p, Atan.p, act_idx.p, row_mask.p, row_nzb.p, vals.p,
+                    row_len, cc[0], cc[1], cc[2], nb[0], nb[1], nb[2]);
+              else
+                k_assemble_nh3f<SH, WF, 8, true><<<gridf, WF * 32, 0, s>>>(
+                    g, pd.p, cap, xs.p, bin_start.p, bflag.p, Atan.p, act_idx.p, row_mask.p, row_nzb.p, vals.p,
+                    row_len, cc[0], cc[1], cc[2], nb[0], nb[1], nb[2]);
+              ++g_launches;
+              continue;
+            }
+          }
           if (asm_rmw) {
             if (sym)
               launch(k_assemble_bins_staged<DD, SH, PP, WS, PCH, true, true>, true);
@@ -1291,7 +1320,7 @@ struct Sim {
     // that all 148 x 32 warps get work instead of a few walking long chunks
     const int rpw = std::max(1, std::min(16, (L.n_act + spmv_blocks * W - 1) / (spmv_blocks * W)));
     const unsigned grid = parts ? spmv_blocks
-                                : static_cast<unsigned>(std::max(1, std::min(spmv_blocks, (L.n_act + rpw * W - 1) / (rpw * W))));
+                                : static_cast<unsigned>(std::max(1, std::min(mg_blocks, (L.n_act + rpw * W - 1) / (rpw * W))));
     // big levels: half-warp rows (two fp32 rows in flight per warp); the
     // denser, smaller coarse levels keep a full warp per row
     if (L.vals16)

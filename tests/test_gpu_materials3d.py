@@ -113,7 +113,7 @@ def test_cam_clay_elastic_limit_matches_hencky():
         assert np.abs(x - y).max() <= 1e-9 * np.abs(y).max()
 
 
-@pytest.mark.parametrize("material", ["hencky", "cam_clay"])
+@pytest.mark.parametrize("material", ["hencky", "cam_clay", "neo_hookean"])
 @pytest.mark.parametrize("ppc", [2, 3])
 def test_3d_assembly_resident_and_restaged_bins(ppc, material):
     """The staged assembly keeps a bin of <= 8 particles resident across its
@@ -137,8 +137,37 @@ def test_3d_assembly_resident_and_restaged_bins(ppc, material):
     u = sim.nodal_solution()
     err, J = fd_check(sim, s, u, 1e-9)
     assert err <= 1e-5, err
-    if material == "hencky":
+    if material in ("hencky", "neo_hookean"):
         assert abs(J - J.T).max() <= 1e-10 * abs(J).max()
+
+
+@pytest.mark.parametrize("tl", [False, True])
+@pytest.mark.parametrize("ppc", [2, 3])
+def test_factored_neo_hookean_assembly_matches_tangent_path(ppc, tl, monkeypatch):
+    """3D neo-Hookean J from the factored tangent (k_tangent_nh3q +
+    k_assemble_nh3f, the default) equals the J assembled from the 81-entry
+    dP/dG (IMPM_ASM_NHF=0: k_tangent_nh3 + k_assemble_bins_staged) to rounding,
+    updated and total Lagrangian, resident and restaged bins, at a deformed
+    state."""
+    import paper_2507_09435_b200 as impm
+    import golden_util as gu
+    from paper_2507_09435_b200 import workloads
+
+    prob = workloads.footing3d(cells=(8, 8, 4), ppc=ppc, h=0.5, steps=10, material="neo_hookean")
+    prob.options.total_lagrangian = tl
+    out = {}
+    for nhf in ("0", "1"):
+        monkeypatch.setenv("IMPM_ASM_NHF", nhf)  # read at sim creation
+        sim = impm.MpmSim(prob.grid, prob.particles, prob.material, prob.options)
+        sim.fixed[:] = prob.fixed
+        sim.gravity = prob.gravity
+        assert sim.step(1 / prob.load_steps).iterations <= 8
+        sim.begin_step()
+        u = np.random.default_rng(5).standard_normal(sim.n_dofs()) * 1e-3 * prob.grid.h
+        out[nhf] = sim.jacobian_csr(u, 2 / prob.load_steps)
+    (rp0, c0, v0), (rp1, c1, v1) = out["0"], out["1"]
+    assert np.array_equal(rp0, rp1) and np.array_equal(c0, c1)
+    assert gu.csr_row_scaled_err(rp0, v0, v1) <= 1e-13
 
 
 def dp_yield(prob, p):
