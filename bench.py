@@ -223,18 +223,20 @@ def kernel_table(kt, rec, info, D, P, n_nodes, peak, symmetric_nh=True):
         rows.append(r)
 
     jm = kt["tangent"][0] + kt["assemble"][0]
-    row("jacobian", ("K6 Jacobian: k_tangent_nh3 (closed-form dP/dG) + k_assemble_bins_staged (colour-batched "
-                     "BSR, upper blocks) + k_mirror_lower + k_diag_inverse") if symmetric_nh else
+    row("jacobian", ("K6 Jacobian: k_tangent_nh3q (factored closed-form tangent) + k_assemble_nh3f (bin per CTA, "
+                     "block pair per thread, colour-batched BSR upper blocks) + k_zero_rows + k_mirror_lower + "
+                     "k_diag_inverse") if symmetric_nh else
         ("K6 Jacobian: k_tangent (dual-number dP/dG) + k_assemble_bins_staged (colour-batched BSR, full blocks: "
          "nonsymmetric J) + k_diag_inverse"),
         jm, n_jac, (184 * P + 8 * ref_nnz) if n_jac else None,
-        "SURVEY 8(d) K6: 184 B/particle state + 8 B x reference-pattern nnz", "jacobian")
+        "SURVEY 8(d) K6: 184 B/particle state + 8 B x reference-pattern nnz",
+        "jacobian" if symmetric_nh else None)  # ncu traffic of the neo-Hookean Jacobian only
     row("spmv", "k_spmv<double> (compacted box-BSR y = J x, outer Krylov)", kt["spmv"][0], kt["spmv"][1],
         spmv_bytes(info, D), "stored block values x 8 + slot ids + 33 B/row", "cg")
     nres = kt["residual_particles"][1]
     row("residual", "K5 residual: k_residual_bins_staged (+ per-particle pass)", kt["residual_particles"][0] +
         kt["residual_nodes"][0], nres, (184 * P + 16 * D * n_nodes) if nres else None,
-        "SURVEY 8(d) K5: 184 B/particle + 16 F B/node", "resb")
+        "SURVEY 8(d) K5: 184 B/particle + 16 F B/node", None)
     row("commit", "K9 G2P k_commit", kt["commit"][0], kt["commit"][1], 384 * P if kt["commit"][1] else None,
         "SURVEY 8(d) K9: 184 + 200 B/particle", "commit")
     # fine level of the V-cycle: two fp16 row-scaled sweeps (residual, Jacobi)

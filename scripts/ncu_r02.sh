@@ -23,9 +23,11 @@ cap() {  # name regex skip
   rm -f $OUT/prof_$1.ncu-rep
   tail -1 $OUT/$1.md
 }
-cap asm  "k_assemble_bins_staged" 94
+cap asm  "k_assemble_nh3f" 94
 cap mir  "k_mirror_lower" 3
-cap tan  "k_tangent_nh3" 3
+cap tan  "k_tangent_nh3q" 3
+cap resp "k_residual_particles" 5
+cap resbin "k_residual_bins_staged" 120
 cap cg   "k_spmv<${I}3, ${I}3, ${I}4, ${I}0, double," 63
 cap res  "k_spmv<${I}3, ${I}3, ${I}4, ${I}2, __half, ${I}0, ${B}1>" 130
 cap jac  "k_spmv<${I}3, ${I}3, ${I}4, ${I}1, __half, ${I}0, ${B}1>" 131
