@@ -46,6 +46,16 @@ __host__ __device__ constexpr int pad4(int x) { return (x + 3) / 4 * 4; }
 // component chunk padded to an even length (16-byte aligned double2 loads).
 __host__ __device__ constexpr int cpad(int nzb, int F) { return (nzb * F + 1) & ~1; }
 __host__ __device__ constexpr int row_len_for(int S, int F) { return pad4(F * cpad(S, F)); }
+// per-component chunk length of a compacted row: fp64 rows pad to 2 values
+// (double2 loads), fp32 rows to 4 (float4 loads); both 16-byte aligned
+template <class VT>
+__host__ __device__ constexpr int chunk_len(int nzb, int F) {
+  return sizeof(VT) == 8 ? cpad(nzb, F) : (sizeof(VT) == 4 ? ((nzb * F + 3) & ~3) : ((nzb * F + 7) & ~7));
+}
+template <class VT>
+__host__ __device__ constexpr int64_t row_len_of(int S, int F) {
+  return sizeof(VT) == 8 ? row_len_for(S, F) : static_cast<int64_t>(F) * chunk_len<VT>(S, F);
+}
 
 // Particle<D> field offsets (particle.hpp:10-29)
 template <int D>
@@ -1896,7 +1906,8 @@ __global__ void __launch_bounds__(WARPS * 32, IMPM_ASMF_MINB) k_assemble_nh3f(
       W1[pl][a][i][1] = dw;
     }
     __syncthreads();
-    const unsigned mg = 0xFFFFFFFFu / static_cast<unsigned>(nk) + 1u;  // e / nk = umulhi(e, mg) for e < 2^16
+    // e / nk = umulhi(e, mg) for e < 2^16, mg = 2^32 / nk rounded up (nk is 8, 12, 18 or 27)
+    const unsigned mg = nk == 8 ? 0x20000000u : (nk == 12 ? 0x15555556u : (nk == 18 ? 0x0E38E38Fu : 0x097B425Fu));
     for (int e = tid; e < np * nk; e += NT) {
       const int pl = static_cast<int>(__umulhi(static_cast<unsigned>(e), mg)), k = e - pl * nk;
       const int pk = s_lpk[s_sup[cc][k]];
@@ -2045,12 +2056,17 @@ __global__ void __launch_bounds__(WARPS * 32, IMPM_ASMF_MINB) k_assemble_nh3f(
 // -delta in row b, its component pitch) into shared memory, so the per-value
 // loop is one load and one coalesced store. A column node that is not a row
 // (no DOF) gets a zero block.
-template <int D>
+// F16: the warp then also writes its row's fp16 smoother copy (k_vals_to_f16's
+// row scale and rounding): the row is in L2 from the mirror, so the copy
+// costs no second pass over the fp64 matrix.
+template <int D, bool F16 = false>
 __global__ void __launch_bounds__(256) k_mirror_lower(GridC g, int n_act, const int* __restrict__ act_list,
                                                       const int* __restrict__ act_idx, const int* __restrict__ row_nzb,
                                                       const uint8_t* __restrict__ row_slots,
                                                       const unsigned* __restrict__ row_mask,
-                                                      double* __restrict__ vals, int64_t row_len) {
+                                                      double* __restrict__ vals, int64_t row_len,
+                                                      __half* __restrict__ v16 = nullptr, int64_t row_len16 = 0,
+                                                      float* __restrict__ rscale = nullptr) {
   constexpr int S = ipow_c(5, D);
   constexpr int center = (S - 1) / 2;  // slot of delta = 0
   __shared__ long long src_s[8][center];
@@ -2112,6 +2128,28 @@ __global__ void __launch_bounds__(256) k_mirror_lower(GridC g, int n_act, const 
       const long long src = src_s[warp][j];
       out[c * cp + e] = src >= 0 ? vals[src + d * cpb_s[warp][j] + c] : 0.0;
     }
+  if constexpr (F16) {
+    __syncwarp();  // the lower blocks this warp stored (read back through L2: __ldcg)
+    const int cq = chunk_len<__half>(nzb, D);
+    __half* dst = v16 + static_cast<int64_t>(row) * row_len16;
+    double mx = 0.0;
+    for (int c = 0; c < D; ++c)
+      for (int e = lane; e < nzb * D; e += 32) mx = fmax(mx, fabs(__ldcg(out + c * cp + e)));
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const float sc = mx > 0.0 ? static_cast<float>(mx / 1024.0) : 1.0f;
+    const float inv = 1.0f / sc;
+    if (lane == 0) rscale[row] = sc;
+    const int h2 = cq >> 1;  // __half2 per chunk
+    for (int e = lane; e < D * h2; e += 32) {
+      const int c = e / h2, j2 = e - c * h2;
+      float2 o = make_float2(0.0f, 0.0f);
+      if (2 * j2 < nzb * D) {
+        const double2 v = __ldcg(reinterpret_cast<const double2*>(out + c * cp) + j2);
+        o = make_float2(static_cast<float>(v.x) * inv, 2 * j2 + 1 < nzb * D ? static_cast<float>(v.y) * inv : 0.0f);
+      }
+      reinterpret_cast<__half2*>(dst + c * cq)[j2] = __float22half2_rn(o);
+    }
+  }
 }
 
 // Block inverse for the smoother / block-Jacobi preconditioner, safeguarded:
@@ -2259,16 +2297,6 @@ struct SpmvTab {
 // y = x + omega Dinv (b - A x); MODE 2: residual y = b - A x.
 enum SpmvMode { kSpmvY = 0, kSpmvJacobi = 1, kSpmvResid = 2 };
 
-// per-component chunk length of a compacted row: fp64 rows pad to 2 values
-// (double2 loads), fp32 rows to 4 (float4 loads); both 16-byte aligned
-template <class VT>
-__host__ __device__ constexpr int chunk_len(int nzb, int F) {
-  return sizeof(VT) == 8 ? cpad(nzb, F) : (sizeof(VT) == 4 ? ((nzb * F + 3) & ~3) : ((nzb * F + 7) & ~7));
-}
-template <class VT>
-__host__ __device__ constexpr int64_t row_len_of(int S, int F) {
-  return sizeof(VT) == 8 ? row_len_for(S, F) : static_cast<int64_t>(F) * chunk_len<VT>(S, F);
-}
 
 // VT = double: the Jacobian itself; VT = float: the preconditioner's copy of
 // a level matrix (values rounded once, vectors and sums stay fp64); VT =
@@ -2280,6 +2308,9 @@ __host__ __device__ constexpr int64_t row_len_of(int S, int F) {
 #define IMPM_HW16 16  // 8 measured slower (level 0: 49 vs 41 ms per load step)
 #endif
 constexpr int HW16 = IMPM_HW16;  // lanes per fp16 row on the big levels
+#ifndef IMPM_SPMV_AHEAD
+#define IMPM_SPMV_AHEAD 1  // load each row's head one row ahead
+#endif
 #ifndef IMPM_SPMV_HALF_MINB
 #define IMPM_SPMV_HALF_MINB 8  // resident 4-warp CTAs per SM the half-warp (level) variants are compiled for
 #endif
@@ -2338,12 +2369,45 @@ __global__ void __launch_bounds__(WARPS * 32, HALF ? IMPM_SPMV_HALF_MINB : 1024 
     // coarse levels use short chunks so that every warp gets a row)
     const int CH = (RPW > 0 ? RPW : rows_per_warp) * WARPS;
     const int nchunks = (n_act + CH - 1) / CH;
-    for (int ci = blockIdx.x; ci < nchunks; ci += gridDim.x)
-    for (int row0 = ci * CH + warp * RW; row0 < min(n_act, (ci + 1) * CH); row0 += WARPS * RW) {
+    for (int ci = blockIdx.x; ci < nchunks; ci += gridDim.x) {
+    const int rend = min(n_act, (ci + 1) * CH);
+    // the head of a row (node, block count, row scale, the lane's first slot)
+    // is loaded one row ahead, so it is in flight while the previous row runs
+    int kq = 0, nzq = 0, slq = 0;
+    float rsq = 1.0f;
+    auto head = [&](int r) {
+      kq = 0;
+      nzq = 0;
+      slq = 0;
+      rsq = 1.0f;
+      if (r < rend) {
+        kq = act_list[r];
+        nzq = row_nzb[r];
+        slq = lane < S ? row_slots[static_cast<int64_t>(r) * S + lane] : 0;
+        if constexpr (sizeof(VT) == 2) rsq = __ldg(rscale + r);
+      }
+    };
+    // (the level sweeps: 0.518 vs 0.535 ms per level-0 scope; the fp64 CG
+    // SpMV is HBM-bound and loses 1.5% with it)
+    constexpr bool AHEAD = IMPM_SPMV_AHEAD && HALF;
+    if (AHEAD) head(ci * CH + warp * RW + sub);
+    for (int row0 = ci * CH + warp * RW; row0 < rend; row0 += WARPS * RW) {
       const int row = row0 + sub;
-      const bool live = row < min(n_act, (ci + 1) * CH);  // the last pair may be half empty
-      const int k = live ? act_list[row] : 0;
-      const int nzb = live ? row_nzb[row] : 0;
+      const bool live = row < rend;  // the last pair may be half empty
+      int k, nzb, sl0;
+      float rsc;
+      if (AHEAD) {
+        k = kq;
+        nzb = nzq;
+        sl0 = slq;
+        rsc = rsq;
+        head(row + WARPS * RW);
+      } else {
+        k = live ? act_list[row] : 0;
+        nzb = live ? row_nzb[row] : 0;
+        sl0 = 0;
+        rsc = (sizeof(VT) == 2 && live) ? __ldg(rscale + row) : 1.0f;
+      }
       const int cp = chunk_len<VT>(nzb, F);
       const int h = cp / VW, tot2 = F * h;
       const int64_t base = static_cast<int64_t>(k) * F;
@@ -2351,7 +2415,6 @@ __global__ void __launch_bounds__(WARPS * 32, HALF ? IMPM_SPMV_HALF_MINB : 1024 
       //    c's free mask, its dot / rhs operand, its own x and row c of Dinv
       bool fm = false;
       double e0 = 0.0, e1 = 0.0;
-      const float rsc = (sizeof(VT) == 2 && live) ? __ldg(rscale + row) : 1.0f;
       double di[F];
 #pragma unroll
       for (int d = 0; d < F; ++d) di[d] = 0.0;
@@ -2383,7 +2446,7 @@ __global__ void __launch_bounds__(WARPS * 32, HALF ? IMPM_SPMV_HALF_MINB : 1024 
         if (x4 != nullptr) {
           // fp32 twin of x, one 16-byte record per node: one load per neighbour
           for (int pos = lane; pos < nzb; pos += HW) {
-            const int sl = rsl[pos];
+            const int sl = AHEAD && pos == lane ? sl0 : rsl[pos];
             IMPM_CHECK_IDX(k + offt[sl], g.N);
             const float4 v = __ldg(reinterpret_cast<const float4*>(x4) + (k + offt[sl]));
             xs[pos * F + 0] = v.x;
@@ -2393,7 +2456,7 @@ __global__ void __launch_bounds__(WARPS * 32, HALF ? IMPM_SPMV_HALF_MINB : 1024 
           }
         } else {
           for (int pos = lane; pos < nzb; pos += HW) {
-            const int sl = rsl[pos];
+            const int sl = AHEAD && pos == lane ? sl0 : rsl[pos];
             IMPM_CHECK_IDX(k + offt[sl], g.N);
             const int64_t nb = static_cast<int64_t>(k + offt[sl]) * F;
 #pragma unroll
@@ -2402,7 +2465,7 @@ __global__ void __launch_bounds__(WARPS * 32, HALF ? IMPM_SPMV_HALF_MINB : 1024 
         }
       } else {
         for (int pos = lane; pos < nzb; pos += HW) {
-          const int sl = rsl[pos];
+          const int sl = AHEAD && pos == lane ? sl0 : rsl[pos];
           IMPM_CHECK_IDX(k + offt[sl], g.N);
           const int64_t nb = static_cast<int64_t>(k + offt[sl]) * F;
 #pragma unroll
@@ -2480,6 +2543,7 @@ __global__ void __launch_bounds__(WARPS * 32, HALF ? IMPM_SPMV_HALF_MINB : 1024 
         }
       }
       __syncwarp();
+    }
     }
   }
   if (partials) block_sum_store<1>(part, partials);

@@ -246,6 +246,9 @@ struct Sim {
   DBuf<float> vals32;
   DBuf<__half> vals16;  // fp16 smoother copy of the fine J (row-scaled)
   DBuf<float> rscale16;
+  // vals16 already holds the current J (written by the fused transpose pass)
+  bool f16_ready = false;
+  bool mirror_f16 = !(std::getenv("IMPM_MIRROR_F16") && std::atoi(std::getenv("IMPM_MIRROR_F16")) == 0);
   // coarse levels (Galerkin products, dense coarsest inverse) are kept for
   // the later Newton iterations of a load step: the row structure is fixed
   // within a step and J moves little, while the fine level always smooths
@@ -543,6 +546,7 @@ struct Sim {
     sync();
     step_built = false;
     matrix_valid = false;
+    f16_ready = false;
   }
   // per-particle work arrays sized by `cap` (the SoA field stride)
   void ensure_particle_buffers() {
@@ -627,6 +631,7 @@ struct Sim {
     slab = true;
     step_built = false;
     matrix_valid = false;
+    f16_ready = false;
   }
 
   // After commit_step: every owned particle goes to the rank(s) that keep it
@@ -747,6 +752,7 @@ struct Sim {
     sync();
     step_built = false;
     matrix_valid = false;
+    f16_ready = false;
   }
 
   void set_particle_field(int field, const double* vals_h) {
@@ -980,6 +986,7 @@ struct Sim {
     CK(cudaMemsetAsync(u.p, 0, sizeof(double) * NF(), s));
     if (coupled) CK(cudaMemsetAsync(prev.p, 0, sizeof(double) * NF(), s));  // p_nodes_ = 0 (porous.cpp:70)
     matrix_valid = false;
+    f16_ready = false;
     step_built = true;
     if (mg_refresh <= 1) mg_setup_step = -1;  // new row structure: rebuild the MG hierarchy
     sync();
@@ -1147,9 +1154,21 @@ struct Sim {
           }
           ++g_launches;
         }
+        f16_ready = false;
         if (upper_only) {
-          k_mirror_lower<DD><<<static_cast<unsigned>((n_act + 7) / 8), 256, 0, s>>>(
-              g, n_act, act_list.p, act_idx.p, row_nzb.p, row_slots.p, row_mask.p, vals.p, row_len);
+          if (mirror_f16 && mg_f16 && !coupled) {
+            // the transpose pass also writes the MG fine level's fp16 copy
+            const int64_t rl16 = row_len_of<__half>(ipow_c(5, DD), DD);
+            vals16.ensure(std::max<int64_t>(1, static_cast<int64_t>(n_act) * rl16));
+            rscale16.ensure(std::max(1, n_act));
+            k_mirror_lower<DD, true><<<static_cast<unsigned>((n_act + 7) / 8), 256, 0, s>>>(
+                g, n_act, act_list.p, act_idx.p, row_nzb.p, row_slots.p, row_mask.p, vals.p, row_len, vals16.p, rl16,
+                rscale16.p);
+            f16_ready = true;
+          } else {
+            k_mirror_lower<DD><<<static_cast<unsigned>((n_act + 7) / 8), 256, 0, s>>>(
+                g, n_act, act_list.p, act_idx.p, row_nzb.p, row_slots.p, row_mask.p, vals.p, row_len);
+          }
           ++g_launches;
           CKL();
         }
@@ -1397,10 +1416,12 @@ struct Sim {
     if (mg_reuse && !mg.empty() &&
         (cross_step || (mg_setup_step == step_counter && mg[0]->n_act == n_act && mg[0]->vals == vals.p))) {
       if (mg_f16 && !coupled && n_act > 0) {  // fine level: fp16 smoother copy of the current J
-        k_vals_to_f16<FE><<<kSpmvBlocks, 128, 0, s>>>(n_act, row_nzb.p, vals.p, row_len, vals16.p, mg[0]->row_len16,
-                                                        rscale16.p);
-        ++g_launches;
-        CKL();
+        if (!f16_ready) {
+          k_vals_to_f16<FE><<<kSpmvBlocks, 128, 0, s>>>(n_act, row_nzb.p, vals.p, row_len, vals16.p,
+                                                          mg[0]->row_len16, rscale16.p);
+          ++g_launches;
+          CKL();
+        }
       } else if (mg_f32 && n_act > 0) {  // fine level: fp32 copy of the current J
         k_vals_to_f32<FE><<<kSpmvBlocks, 128, 0, s>>>(n_act, row_nzb.p, vals.p, row_len, vals32.p, mg[0]->row_len32,
                                                         mg_f16sim);
@@ -1441,7 +1462,7 @@ struct Sim {
       rscale16.ensure(std::max(1, n_act));
       L0->vals16 = vals16.p;
       L0->rscale = rscale16.p;
-      if (n_act > 0) {
+      if (n_act > 0 && !f16_ready) {
         k_vals_to_f16<FE><<<kSpmvBlocks, 128, 0, s>>>(n_act, row_nzb.p, vals.p, row_len, vals16.p, L0->row_len16,
                                                         rscale16.p);
         ++g_launches;
