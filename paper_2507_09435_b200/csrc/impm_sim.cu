@@ -268,6 +268,8 @@ struct Sim {
   // (default 3; a solve on stale levels that fails or overruns 4x the last
   // iteration count is retried once on a freshly built hierarchy)
   int mg_refresh = std::getenv("IMPM_MG_REFRESH") ? std::atoi(std::getenv("IMPM_MG_REFRESH")) : 3;
+  // re-estimate the smoother's lambda_max every mg_power_every load steps (A/B experiments)
+  int mg_power_every = std::getenv("IMPM_MG_POWER_EVERY") ? std::max(1, std::atoi(std::getenv("IMPM_MG_POWER_EVERY"))) : 5;
   double exact_rtol = 1e-13;         // Krylov target of an exact-equivalent Newton step
   int exact_newton_env = -1;         // IMPM_EXACT_NEWTON: -1 = by material
   bool exact_newton = false;         // set per material at create / set_material
@@ -1598,7 +1600,8 @@ struct Sim {
     // ... and it moves little between load steps too: omega * lambda_est =
     // 4 / 3.3 leaves a wide margin below the divergence limit 2, so the
     // estimate is refreshed every 5 load steps (or when the depth changes)
-    const bool need_power = mg_power_step < 0 || step_counter - mg_power_step >= 5 || mg_lam_host.size() != mg.size();
+    const bool need_power =
+        mg_power_step < 0 || step_counter - mg_power_step >= mg_power_every || mg_lam_host.size() != mg.size();
     mg_lam.ensure(std::max<size_t>(mg.size(), 1));
     if (need_power) {
       Prof::Scope psp(&prof, kcMgPower);
