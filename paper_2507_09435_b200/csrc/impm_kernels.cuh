@@ -1785,10 +1785,10 @@ __global__ void __launch_bounds__(WARPS * 32, D == 3 ? (RMW ? 2 : IMPM_ASM_MINB)
 // MIRROR: also add K_kl^T into row l (slabs); false: k_mirror_lower fills the
 // lower blocks.
 #ifndef IMPM_ASMF_WARPS
-#define IMPM_ASMF_WARPS 3  // 96 threads: 171 pairs of an 18-node box in 2 rounds, 378 (27 nodes) in 4
+#define IMPM_ASMF_WARPS 6  // 192 threads: the 171 pairs of an 18-node box in one round (ms per cfg 4 Jacobian, assembly + transpose: 3 warps 19.25, 6 warps 18.92, 8 warps 19.43; 4 warps 0.3 below 3)
 #endif
 #ifndef IMPM_ASMF_MINB
-#define IMPM_ASMF_MINB 9  // 72 registers, 9 x 25 KB shared per SM (8: 80 registers, 18.3 vs 18.0 ms per cfg 4 Jacobian)
+#define IMPM_ASMF_MINB 4  // 80 registers, 4 x 25 KB shared per SM
 #endif
 struct BinHdr {
   int fl, p0, p1;
@@ -2132,23 +2132,28 @@ __global__ void __launch_bounds__(256) k_mirror_lower(GridC g, int n_act, const 
     __syncwarp();  // the lower blocks this warp stored (read back through L2: __ldcg)
     const int cq = chunk_len<__half>(nzb, D);
     __half* dst = v16 + static_cast<int64_t>(row) * row_len16;
+    // two passes over the row (the second hits L2), double2 per lane, no
+    // per-element index division
+    const int n2 = cp >> 1, h2 = cq >> 1;  // double2 / __half2 per chunk (h2 >= n2)
     double mx = 0.0;
     for (int c = 0; c < D; ++c)
-      for (int e = lane; e < nzb * D; e += 32) mx = fmax(mx, fabs(__ldcg(out + c * cp + e)));
+      for (int j2 = lane; j2 < n2; j2 += 32) {
+        const double2 v = __ldcg(reinterpret_cast<const double2*>(out + c * cp) + j2);
+        mx = fmax(mx, fmax(fabs(v.x), 2 * j2 + 1 < nzb * D ? fabs(v.y) : 0.0));  // (the pad is not a value)
+      }
     for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     const float sc = mx > 0.0 ? static_cast<float>(mx / 1024.0) : 1.0f;
     const float inv = 1.0f / sc;
     if (lane == 0) rscale[row] = sc;
-    const int h2 = cq >> 1;  // __half2 per chunk
-    for (int e = lane; e < D * h2; e += 32) {
-      const int c = e / h2, j2 = e - c * h2;
-      float2 o = make_float2(0.0f, 0.0f);
-      if (2 * j2 < nzb * D) {
-        const double2 v = __ldcg(reinterpret_cast<const double2*>(out + c * cp) + j2);
-        o = make_float2(static_cast<float>(v.x) * inv, 2 * j2 + 1 < nzb * D ? static_cast<float>(v.y) * inv : 0.0f);
+    for (int c = 0; c < D; ++c)
+      for (int j2 = lane; j2 < h2; j2 += 32) {
+        float2 o = make_float2(0.0f, 0.0f);
+        if (2 * j2 < nzb * D) {
+          const double2 v = __ldcg(reinterpret_cast<const double2*>(out + c * cp) + j2);
+          o = make_float2(static_cast<float>(v.x) * inv, 2 * j2 + 1 < nzb * D ? static_cast<float>(v.y) * inv : 0.0f);
+        }
+        reinterpret_cast<__half2*>(dst + c * cq)[j2] = __float22half2_rn(o);
       }
-      reinterpret_cast<__half2*>(dst + c * cq)[j2] = __float22half2_rn(o);
-    }
   }
 }
 
