@@ -2132,28 +2132,23 @@ __global__ void __launch_bounds__(256) k_mirror_lower(GridC g, int n_act, const 
     __syncwarp();  // the lower blocks this warp stored (read back through L2: __ldcg)
     const int cq = chunk_len<__half>(nzb, D);
     __half* dst = v16 + static_cast<int64_t>(row) * row_len16;
-    // two passes over the row (the second hits L2), double2 per lane, no
-    // per-element index division
-    const int n2 = cp >> 1, h2 = cq >> 1;  // double2 / __half2 per chunk (h2 >= n2)
     double mx = 0.0;
     for (int c = 0; c < D; ++c)
-      for (int j2 = lane; j2 < n2; j2 += 32) {
-        const double2 v = __ldcg(reinterpret_cast<const double2*>(out + c * cp) + j2);
-        mx = fmax(mx, fmax(fabs(v.x), 2 * j2 + 1 < nzb * D ? fabs(v.y) : 0.0));  // (the pad is not a value)
-      }
+      for (int e = lane; e < nzb * D; e += 32) mx = fmax(mx, fabs(__ldcg(out + c * cp + e)));
     for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     const float sc = mx > 0.0 ? static_cast<float>(mx / 1024.0) : 1.0f;
     const float inv = 1.0f / sc;
     if (lane == 0) rscale[row] = sc;
-    for (int c = 0; c < D; ++c)
-      for (int j2 = lane; j2 < h2; j2 += 32) {
-        float2 o = make_float2(0.0f, 0.0f);
-        if (2 * j2 < nzb * D) {
-          const double2 v = __ldcg(reinterpret_cast<const double2*>(out + c * cp) + j2);
-          o = make_float2(static_cast<float>(v.x) * inv, 2 * j2 + 1 < nzb * D ? static_cast<float>(v.y) * inv : 0.0f);
-        }
-        reinterpret_cast<__half2*>(dst + c * cq)[j2] = __float22half2_rn(o);
+    const int h2 = cq >> 1;  // __half2 per chunk
+    for (int e = lane; e < D * h2; e += 32) {
+      const int c = e / h2, j2 = e - c * h2;
+      float2 o = make_float2(0.0f, 0.0f);
+      if (2 * j2 < nzb * D) {
+        const double2 v = __ldcg(reinterpret_cast<const double2*>(out + c * cp) + j2);
+        o = make_float2(static_cast<float>(v.x) * inv, 2 * j2 + 1 < nzb * D ? static_cast<float>(v.y) * inv : 0.0f);
       }
+      reinterpret_cast<__half2*>(dst + c * cq)[j2] = __float22half2_rn(o);
+    }
   }
 }
 
