@@ -2339,7 +2339,12 @@ __global__ void __launch_bounds__(WARPS * 32, HALF ? IMPM_SPMV_HALF_MINB : 1024 
   // double2 per lane buffered ahead of the x gathers (the Jacobi sweep keeps
   // its Dinv row and rhs in registers too: smaller head under the 64-reg cap)
   // fp32 rows carry half the bytes (~5 float4 per lane at 73 blocks/row)
-  constexpr int NB = sizeof(VT) == 8 ? (MODE == kSpmvJacobi ? 4 : 6) : (MODE == kSpmvJacobi ? 4 : 6);
+#ifndef IMPM_SPMV16_NB
+#define IMPM_SPMV16_NB 0  // 0: as fp32/fp64; > 0: buffered 16-byte loads per lane of the fp16 sweeps
+#endif
+  constexpr int NB = (sizeof(VT) == 2 && IMPM_SPMV16_NB > 0) ? IMPM_SPMV16_NB
+                     : sizeof(VT) == 8                     ? (MODE == kSpmvJacobi ? 4 : 6)
+                                                           : (MODE == kSpmvJacobi ? 4 : 6);
   // lanes per row: fp32 rows carry half the bytes, so on big levels (HALF) a
   // half-warp streams one row and each warp keeps two rows (two latency
   // chains) in flight
