@@ -609,53 +609,6 @@ __global__ void k_residual_particles(GridC g, const double* __restrict__ pd, int
     }
 }
 
-// Residual phase B (nodes): deterministic pull over the particles of the
-// 3^D candidate bins, masked to free DOFs, + partial sums of r.r
-template <int D, int SHAPE>
-__global__ void k_residual_nodes(GridC g, const double* __restrict__ pd, int64_t cap,
-                                 const double* __restrict__ xs, const int* __restrict__ bin_start,
-                                 const int* __restrict__ sup, const double* __restrict__ Pst,
-                                 const double* __restrict__ bext, const int* __restrict__ act_flag,
-                                 const uint8_t* __restrict__ freem, double load_scale, double* __restrict__ r,
-                                 double* __restrict__ partials) {
-  double rr[1] = {0.0};
-  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < g.N; n += gridDim.x * blockDim.x) {
-    double acc[3] = {0.0, 0.0, 0.0};
-    if (act_flag[n]) {
-      int idx[3];
-      unflat<D>(g, n, idx);
-      for_each_particle_of_node<D>(g, idx, bin_start, sup, [&](int p, const int*) {
-        double w[3], dw[3];
-#pragma unroll
-        for (int a = 0; a < D; ++a) {
-          const WeightValue wv = weight_1d<SHAPE>(xs[a * cap + p] - node_coord(g, a, idx[a]),
-                                                  pd[(PF<D>::lp + a) * cap + p], g.h);
-          w[a] = wv.w;
-          dw[a] = wv.dw;
-        }
-        double W, grad[3];
-        tensor_weight<D>(w, dw, W, grad);
-        const double* Pp = Pst + static_cast<int64_t>(p) * D * D;
-#pragma unroll
-        for (int c = 0; c < D; ++c) {
-          double fint = grad[0] * Pp[c * D];
-#pragma unroll
-          for (int b = 1; b < D; ++b) fint += grad[b] * Pp[c * D + b];
-          const double fext = W * bext[c * cap + p] * load_scale;
-          acc[c] += fint - fext;
-        }
-      });
-    }
-#pragma unroll
-    for (int c = 0; c < D; ++c) {
-      const double v = freem[n * D + c] ? acc[c] : 0.0;
-      r[n * D + c] = v;
-      rr[0] += v * v;
-    }
-  }
-  block_sum_store<1>(rr, partials);
-}
-
 // Residual phase B, bin-centric push in 3^D colour batches (bins of one
 // colour have disjoint supports): a warp owns a bin, lane k < nk owns box
 // node k and sums the bin's particle contributions
