@@ -270,6 +270,12 @@ struct Sim {
   int mg_refresh = std::getenv("IMPM_MG_REFRESH") ? std::atoi(std::getenv("IMPM_MG_REFRESH")) : 3;
   // re-estimate the smoother's lambda_max every mg_power_every load steps (A/B experiments)
   int mg_power_every = std::getenv("IMPM_MG_POWER_EVERY") ? std::max(1, std::atoi(std::getenv("IMPM_MG_POWER_EVERY"))) : 5;
+  // safety factor on the power estimate in omega = 4 / (3 s lambda): cfg 4 driver window,
+  // Newton it/s (Krylov it): s = 1.2 12.05 (719), 1.1 12.33 (686), 1.0 12.69 (656),
+  // 0.95 12.57 (670), 0.9 11.42 (stale-level retries), 0.8 3.37 (smoother diverges)
+  double mg_omega_safety = std::getenv("IMPM_MG_OMEGA_SAFETY") ? std::atof(std::getenv("IMPM_MG_OMEGA_SAFETY")) : 1.0;
+  // smoothing sweeps on the levels below the fine one (0: as the fine level; A/B experiments)
+  int mg_nu_coarse = std::getenv("IMPM_MG_NU_COARSE") ? std::atoi(std::getenv("IMPM_MG_NU_COARSE")) : 0;
   double exact_rtol = 1e-13;         // Krylov target of an exact-equivalent Newton step
   int exact_newton_env = -1;         // IMPM_EXACT_NEWTON: -1 = by material
   bool exact_newton = false;         // set per material at create / set_material
@@ -1598,7 +1604,7 @@ struct Sim {
     // lambda_max(Dinv A) moves little between the Newton iterations of one
     // load step: estimate it on the first setup of the step, then reuse
     // ... and it moves little between load steps too: omega * lambda_est =
-    // 4 / 3.3 leaves a wide margin below the divergence limit 2, so the
+    // 4 / 3 leaves a margin below the divergence limit 2, so the
     // estimate is refreshed every 5 load steps (or when the depth changes)
     const bool need_power =
         mg_power_step < 0 || step_counter - mg_power_step >= mg_power_every || mg_lam_host.size() != mg.size();
@@ -1634,7 +1640,7 @@ struct Sim {
       for (size_t l = 0; l + 1 < mg.size(); ++l) {
         MgLevel& L = *mg[l];
         const int64_t n = static_cast<int64_t>(L.g.N) * FE;
-        L.omega = 4.0 / (3.0 * 1.1 * (lam[l] > 0 ? lam[l] : 1.0));
+        L.omega = 4.0 / (3.0 * mg_omega_safety * (lam[l] > 0 ? lam[l] : 1.0));
         CK(cudaMemsetAsync(L.t, 0, sizeof(double) * n, s));
         CK(cudaMemsetAsync(L.bvec.p, 0, sizeof(double) * n, s));
         CK(cudaMemsetAsync(L.r.p, 0, sizeof(double) * n, s));
@@ -1739,7 +1745,8 @@ struct Sim {
       }
       return;
     }
-    const int nu = mg_smooth_env > 0 ? mg_smooth_env : (opt.mg_smooth > 0 ? opt.mg_smooth : 1);
+    const int nu0 = mg_smooth_env > 0 ? mg_smooth_env : (opt.mg_smooth > 0 ? opt.mg_smooth : 1);
+    const int nu = l > 0 && mg_nu_coarse > 0 ? mg_nu_coarse : nu0;
     MgLevel& C = *mg[l + 1];
     {
       Prof::Scope ps(&prof, lcls);
