@@ -274,6 +274,8 @@ struct Sim {
   // Newton it/s (Krylov it): s = 1.2 12.05 (719), 1.1 12.33 (686), 1.0 12.69 (656),
   // 0.95 12.57 (670), 0.9 11.42 (stale-level retries), 0.8 3.37 (smoother diverges)
   double mg_omega_safety = std::getenv("IMPM_MG_OMEGA_SAFETY") ? std::atof(std::getenv("IMPM_MG_OMEGA_SAFETY")) : 1.0;
+  double mg_omega_safety_coarse =
+      std::getenv("IMPM_MG_OMEGA_SAFETY_COARSE") ? std::atof(std::getenv("IMPM_MG_OMEGA_SAFETY_COARSE")) : 0.0;
   // smoothing sweeps on the levels below the fine one (0: as the fine level; A/B experiments)
   int mg_nu_coarse = std::getenv("IMPM_MG_NU_COARSE") ? std::atoi(std::getenv("IMPM_MG_NU_COARSE")) : 0;
   double exact_rtol = 1e-13;         // Krylov target of an exact-equivalent Newton step
@@ -1640,7 +1642,8 @@ struct Sim {
       for (size_t l = 0; l + 1 < mg.size(); ++l) {
         MgLevel& L = *mg[l];
         const int64_t n = static_cast<int64_t>(L.g.N) * FE;
-        L.omega = 4.0 / (3.0 * mg_omega_safety * (lam[l] > 0 ? lam[l] : 1.0));
+        const double sf = l > 0 && mg_omega_safety_coarse > 0.0 ? mg_omega_safety_coarse : mg_omega_safety;
+        L.omega = 4.0 / (3.0 * sf * (lam[l] > 0 ? lam[l] : 1.0));
         CK(cudaMemsetAsync(L.t, 0, sizeof(double) * n, s));
         CK(cudaMemsetAsync(L.bvec.p, 0, sizeof(double) * n, s));
         CK(cudaMemsetAsync(L.r.p, 0, sizeof(double) * n, s));
