@@ -432,6 +432,15 @@ __device__ __forceinline__ void block_sum_store(double (&v)[NV], double* __restr
   }
 }
 
+// block partials of an int64 array (exact in fp64 while every partial < 2^53)
+__global__ void k_sum_i64(int64_t n, const int64_t* __restrict__ v, double* __restrict__ partials) {
+  double s[1] = {0.0};
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    s[0] += static_cast<double>(v[i]);
+  block_sum_store<1>(s, partials);
+}
+
 // sums NV rows of `nb` partials in fixed order into out[0..NV)
 template <int NV>
 __global__ void k_finalize_sum(const double* __restrict__ partials, int nb, double* __restrict__ out) {

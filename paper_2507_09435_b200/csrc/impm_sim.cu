@@ -59,13 +59,22 @@ struct DBuf {
   ~DBuf() {
     if (p) cudaFree(p);
   }
+  // a buffer that has to grow gets 1/8 headroom: the active set of a load
+  // ramp grows a little every step, and a cudaFree + cudaMalloc of the 6 GB
+  // matrix (an implicit device sync) each time costs milliseconds
   void ensure(size_t n) {
     if (n <= cap && p) return;
+    const bool regrow = p != nullptr;
     if (p) CK(cudaFree(p));
     p = nullptr;
     size_t c = std::max<size_t>(n, 1);
+    if (regrow) c += static_cast<size_t>(static_cast<double>(c) * buf_slack());
     CK(cudaMalloc(&p, c * sizeof(T)));
     cap = c;
+  }
+  static double buf_slack() {
+    static const double f = std::getenv("IMPM_BUF_SLACK") ? std::atof(std::getenv("IMPM_BUF_SLACK")) : 0.125;
+    return f;
   }
   T* get() const { return p; }
 };
@@ -2115,13 +2124,15 @@ struct Sim {
       k_csr_count<DD, FE><<<blocks_for(n_dofs), kThreads, 0, s>>>(g, n_dofs, node_of.p, dof_of.p, rowlen.p); ++g_launches;
       CKL();
     });
-    int64_t tot = 0;
-    // sum on host (small, once per step)
-    std::vector<int64_t> h(n_dofs);
-    CK(cudaMemcpyAsync(h.data(), rowlen.p, sizeof(int64_t) * n_dofs, cudaMemcpyDeviceToHost, s));
+    // summed on the device (the host loop over 3 M row lengths and their
+    // 25 MB download cost ~5 ms per load step at cfg 4); rank-local on a slab
+    k_sum_i64<<<kRedBlocks, kThreads, 0, s>>>(n_dofs, rowlen.p, partials.p); ++g_launches;
+    k_finalize_sum<1><<<1, 1024, 0, s>>>(partials.p, kRedBlocks, sums.p); ++g_launches;
+    CKL();
+    double h = 0.0;
+    CK(cudaMemcpyAsync(&h, sums.p, sizeof(double), cudaMemcpyDeviceToHost, s));
     sync();
-    for (auto v : h) tot += v;
-    return ref_nnz_cache = tot;
+    return ref_nnz_cache = std::llround(h);
   }
 
   // newton_attempt (mpm_solver.hpp:281-355); u already holds u_init
