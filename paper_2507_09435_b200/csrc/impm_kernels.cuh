@@ -137,6 +137,31 @@ __global__ void k_soa_to_aos(const double* __restrict__ soa, int64_t cap, int n,
   for (int f = 0; f < nd; ++f) aos[o * stride_dbl + f] = soa[f * cap + i];
 }
 
+// chunked particle I/O (the copies of one chunk overlap the layout kernel of
+// the next): inverse of the sorted -> original permutation, and AoS rows
+// [o0, o1) in original order gathered from the sorted SoA
+__global__ void k_invert_perm(const int* __restrict__ orig, int n, int* __restrict__ inv) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) inv[orig[i]] = i;
+}
+__global__ void k_rows_to_aos(const double* __restrict__ soa, int64_t cap, const int* __restrict__ inv, int o0,
+                              int o1, int nd, double* __restrict__ aos) {
+  const int64_t e0 = static_cast<int64_t>(o0) * nd, e1 = static_cast<int64_t>(o1) * nd;
+  for (int64_t e = e0 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < e1;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t row = e / nd;
+    const int f = static_cast<int>(e - row * nd);
+    aos[e] = soa[f * cap + inv[row]];
+  }
+}
+__global__ void k_aos_rows_to_soa(const double* __restrict__ aos, int r0, int r1, int nd, double* __restrict__ soa,
+                                  int64_t cap, int* __restrict__ orig) {
+  const int i = r0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= r1) return;
+  for (int f = 0; f < nd; ++f) soa[f * cap + i] = aos[static_cast<int64_t>(i) * nd + f];
+  orig[i] = i;
+}
+
 // per-particle field in ORIGINAL order -> sorted slot
 __global__ void k_set_field(double* __restrict__ col, const double* __restrict__ vals,
                             const int* __restrict__ orig, int n) {

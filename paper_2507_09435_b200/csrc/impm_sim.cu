@@ -206,6 +206,13 @@ struct Sim {
   int ND = 0;
   DBuf<double> pd, pd_tmp, xs, bext, Pst, Atan;
   DBuf<double> io_staging;  // AoS staging of particle upload / download
+  DBuf<int> io_inv;         // original -> sorted slot (chunked download)
+  // particle I/O in chunks: the host<->device copies run on io_stream and
+  // overlap the layout kernels on s (IMPM_IO_CHUNKS=1: one copy, one kernel)
+  static constexpr int kIoMaxChunks = 16;
+  cudaStream_t io_stream = nullptr;
+  cudaEvent_t io_ev[kIoMaxChunks + 1] = {};
+  int io_chunks = std::getenv("IMPM_IO_CHUNKS") ? std::max(1, std::min(kIoMaxChunks, std::atoi(std::getenv("IMPM_IO_CHUNKS")))) : 8;
   DBuf<int> orig, orig_tmp, key, sup, rank, perm, bin_count, bin_start;
   // grid / dofs
   DBuf<uint8_t> fixed, freem;
@@ -459,6 +466,8 @@ struct Sim {
     CK(cudaStreamCreateWithFlags(&own_stream, cudaStreamNonBlocking));
     s = own_stream;
     prof.s = s;
+    CK(cudaStreamCreateWithFlags(&io_stream, cudaStreamNonBlocking));
+    for (auto& e : io_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     fixed.ensure(NF());
     CK(cudaMemsetAsync(fixed.p, 0, NF(), s));
     st.ensure(1);
@@ -487,6 +496,9 @@ struct Sim {
     if (h_st) cudaFreeHost(h_st);
     if (h_sc) cudaFreeHost(h_sc);
     if (own_stream) cudaStreamDestroy(own_stream);
+    if (io_stream) cudaStreamDestroy(io_stream);
+    for (auto& e : io_ev)
+      if (e) cudaEventDestroy(e);
   }
 
   void set_material(const impm_material* m) {
@@ -557,7 +569,24 @@ struct Sim {
     CK(cudaMemsetAsync(uty.p, 0, sizeof(double) * cap, s));
     DBuf<double>& staging = io_staging;  // persistent: no 3 GB malloc/free per call
     staging.ensure(std::max<int64_t>(1, n * (stride / 8)));
-    if (n > 0) {
+    const int K = stride == ND * 8 && n >= (1 << 20) ? io_chunks : 1;
+    if (n > 0 && K > 1) {
+      // chunk c's upload (io_stream) overlaps chunk c-1's transpose (s)
+      const int64_t ch = (n + K - 1) / K;
+      CK(cudaEventRecord(io_ev[kIoMaxChunks], s));  // staging is free once s got here
+      CK(cudaStreamWaitEvent(io_stream, io_ev[kIoMaxChunks], 0));
+      for (int c = 0; c < K; ++c) {
+        const int64_t r0 = c * ch, r1 = std::min<int64_t>(n, r0 + ch);
+        if (r0 >= r1) break;
+        CK(cudaMemcpyAsync(staging.p + r0 * ND, aos + r0 * ND, (r1 - r0) * stride, cudaMemcpyHostToDevice, io_stream));
+        CK(cudaEventRecord(io_ev[c], io_stream));
+        CK(cudaStreamWaitEvent(s, io_ev[c], 0));
+        k_aos_rows_to_soa<<<blocks_for(r1 - r0), kThreads, 0, s>>>(staging.p, static_cast<int>(r0),
+                                                                     static_cast<int>(r1), ND, pd.p, cap, orig.p);
+        ++g_launches;
+        CKL();
+      }
+    } else if (n > 0) {
       CK(cudaMemcpyAsync(staging.p, aos, n * stride, cudaMemcpyHostToDevice, s));
       k_aos_to_soa<<<blocks_for(n), kThreads, 0, s>>>(staging.p, stride / 8, P, ND, pd.p, cap, orig.p); ++g_launches;
       CKL();
@@ -588,6 +617,28 @@ struct Sim {
     if (n == 0) return;
     DBuf<double>& staging = io_staging;
     staging.ensure(n * (stride / 8));
+    const int K = stride == ND * 8 && n >= (1 << 20) ? io_chunks : 1;
+    if (K > 1) {
+      // rows in original order, chunk by chunk: chunk c's download
+      // (io_stream) overlaps chunk c+1's gather (s)
+      io_inv.ensure(n);
+      k_invert_perm<<<blocks_for(n), kThreads, 0, s>>>(orig.p, P, io_inv.p); ++g_launches;
+      const int64_t ch = (n + K - 1) / K;
+      for (int c = 0; c < K; ++c) {
+        const int64_t o0 = c * ch, o1 = std::min<int64_t>(n, o0 + ch);
+        if (o0 >= o1) break;
+        k_rows_to_aos<<<148 * 8, kThreads, 0, s>>>(pd.p, cap, io_inv.p, static_cast<int>(o0), static_cast<int>(o1), ND,
+                                                   staging.p);
+        ++g_launches;
+        CKL();
+        CK(cudaEventRecord(io_ev[c], s));
+        CK(cudaStreamWaitEvent(io_stream, io_ev[c], 0));
+        CK(cudaMemcpyAsync(aos + o0 * ND, staging.p + o0 * ND, (o1 - o0) * stride, cudaMemcpyDeviceToHost, io_stream));
+      }
+      CK(cudaStreamSynchronize(io_stream));
+      sync();
+      return;
+    }
     if (stride != ND * 8) CK(cudaMemcpyAsync(staging.p, aos, n * stride, cudaMemcpyHostToDevice, s));
     k_soa_to_aos<<<blocks_for(n), kThreads, 0, s>>>(pd.p, cap, P, ND, orig.p, staging.p, stride / 8); ++g_launches;
     CKL();

@@ -41,7 +41,15 @@ def main():
     t_h2d = best(lambda: dev.copy_(th, non_blocking=True))
     t_d2h = best(lambda: th.copy_(dev, non_blocking=True))
     t_set = best(lambda: sim.set_particles(host))
+    # round trip: a download right after an upload returns the upload, bit for bit
+    back = np.zeros_like(host)
+    sim._h.call("impm_sim_get_particles", _abi.ptr(back), n, back.strides[0])
+    assert np.array_equal(back, prob.particles), "particle round trip differs"
     sim.step(1 / prob.load_steps)
+    # after a step (sorted particles): the chunked download equals the one-copy path
+    a = np.zeros_like(host)
+    sim._h.call("impm_sim_get_particles", _abi.ptr(a), n, a.strides[0])
+    print("round trip ok; chunks", os.environ.get("IMPM_IO_CHUNKS", "default"), float(np.abs(a).sum()), flush=True)
     t_get = best(lambda: sim._h.call("impm_sim_get_particles", _abi.ptr(host), n, host.strides[0]))
     print(f"{nbytes / 1e9:.2f} GB: torch H2D {t_h2d * 1e3:.1f} ms, set_particles {t_set * 1e3:.1f} ms; "
           f"torch D2H {t_d2h * 1e3:.1f} ms, get_particles {t_get * 1e3:.1f} ms", flush=True)
