@@ -263,11 +263,23 @@ __global__ void k_perm_check(const int* __restrict__ perm, int P, DevStatus* st)
 }
 
 // dst[f][i] = src[f][perm[i]] for all fields (blockIdx.y = field)
+// blockIdx.y takes fields [fpb y, fpb y + fpb) of nf: one perm load per particle
+// serves fpb fields, whose loads are in flight together
 __global__ void k_gather_fields(const double* __restrict__ src, double* __restrict__ dst, int64_t cap,
-                                const int* __restrict__ perm, int P) {
+                                const int* __restrict__ perm, int P, int nf = 1, int fpb = 1) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t f = blockIdx.y;
-  if (i < P) dst[f * cap + i] = src[f * cap + perm[i]];
+  if (i >= P) return;
+  const int64_t j = perm[i];
+  const int f0 = blockIdx.y * fpb, f1 = min(nf, f0 + fpb);
+  constexpr int U = 8;
+  for (int fb = f0; fb < f1; fb += U) {
+    double v[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) v[q] = fb + q < f1 ? src[(fb + q) * cap + j] : 0.0;
+#pragma unroll
+    for (int q = 0; q < U; ++q)
+      if (fb + q < f1) dst[(fb + q) * cap + i] = v[q];
+  }
 }
 __global__ void k_gather_int(const int* __restrict__ src, int* __restrict__ dst, const int* __restrict__ perm, int P) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;

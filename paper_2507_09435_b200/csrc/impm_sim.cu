@@ -943,8 +943,9 @@ struct Sim {
     read_status();
     if (h_st->perm_moved) {
       Prof::Scope ps(&prof, kcSort);
-      dim3 grid(blocks_for(P), ND);
-      k_gather_fields<<<grid, kThreads, 0, s>>>(pd.p, pd_tmp.p, cap, perm.p, P); ++g_launches;
+      constexpr int kFpb = 8;  // fields per thread
+      dim3 grid(blocks_for(P), (ND + kFpb - 1) / kFpb);
+      k_gather_fields<<<grid, kThreads, 0, s>>>(pd.p, pd_tmp.p, cap, perm.p, P, ND, kFpb); ++g_launches;
       CKL();
       k_gather_int<<<blocks_for(P), kThreads, 0, s>>>(orig.p, orig_tmp.p, perm.p, P); ++g_launches;
       k_gather_fields<<<dim3(blocks_for(P), 1), kThreads, 0, s>>>(uty.p, xs.p, cap, perm.p, P); ++g_launches;
