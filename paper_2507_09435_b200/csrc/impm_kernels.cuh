@@ -598,7 +598,10 @@ __device__ __forceinline__ StressOut<T> update_stress(const MatParams& mp, const
 // nominal stress P = V sigma f_inc^{-T} so that the node-side gather is
 // r_{k,c} = sum_b grad_{k,b} P_{cb} - w_k b_c s  (mpm_solver.hpp:164-208).
 template <int D, int SHAPE, bool NHO>
-__global__ void k_residual_particles(GridC g, const double* __restrict__ pd, int64_t cap, int P,
+#ifndef IMPM_RESP_MINB
+#define IMPM_RESP_MINB 4  // resident 256-thread CTAs per SM (64 registers): 0.94 vs 1.06 ms per cfg 4 residual at 1 (80 registers); 5: 1.15
+#endif
+__global__ void __launch_bounds__(256, IMPM_RESP_MINB) k_residual_particles(GridC g, const double* __restrict__ pd, int64_t cap, int P,
                                      const double* __restrict__ xs, const int* __restrict__ key,
                                      const int* __restrict__ sup, const int* __restrict__ orig,
                                      const double* __restrict__ u, MatParams mp, int tl,
@@ -1057,6 +1060,7 @@ __global__ void __launch_bounds__(128) k_tangent_nh3(GridC g, const double* __re
 // tangent + assembly, and 20.0 with Q component-major.)
 constexpr int kNhQ = 28;
 template <int SHAPE>
+// (min-blocks hints measured: none 1.27 ms per cfg 4 tangent, 1: 1.50, 8: 1.31)
 __global__ void __launch_bounds__(128) k_tangent_nh3q(GridC g, const double* __restrict__ pd, int64_t cap, int P,
                                                       const double* __restrict__ xs, const int* __restrict__ key,
                                                       const int* __restrict__ sup, const double* __restrict__ u,
@@ -3365,7 +3369,10 @@ __global__ void k_dot1(int64_t n, const int* __restrict__ done, const double* __
 
 // --------------------------------------------------------------- K9 G2P --
 template <int D, int SHAPE, bool NHO>
-__global__ void k_commit(GridC g, double* __restrict__ pd, int64_t cap, int P, const double* __restrict__ xs,
+#ifndef IMPM_COMMIT_MINB
+#define IMPM_COMMIT_MINB 4  // resident 256-thread CTAs per SM (64 registers): 1.16 vs 1.26 ms per cfg 4 commit
+#endif
+__global__ void __launch_bounds__(256, IMPM_COMMIT_MINB) k_commit(GridC g, double* __restrict__ pd, int64_t cap, int P, const double* __restrict__ xs,
                          const int* __restrict__ key, const int* __restrict__ sup, const int* __restrict__ orig,
                          const double* __restrict__ u, MatParams mp, int tl, DevStatus* st) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
