@@ -751,8 +751,16 @@ __global__ void __launch_bounds__(WARPS * 32) k_residual_bins(
 // node lanes sum from shared memory in the same fixed particle order (bitwise
 // the values of k_residual_bins). Removes the per-particle load->sync->FMA
 // latency chain of the unstaged loop.
+#ifndef IMPM_RESB_MINB
+#define IMPM_RESB_MINB 0  // 0: the compiler's register choice
+#endif
+#if IMPM_RESB_MINB > 0
+#define IMPM_RESB_LB(T) __launch_bounds__(T, IMPM_RESB_MINB)
+#else
+#define IMPM_RESB_LB(T) __launch_bounds__(T)
+#endif
 template <int D, int SHAPE, int WARPS, int PCH>
-__global__ void __launch_bounds__(WARPS * 32) k_residual_bins_staged(
+__global__ void IMPM_RESB_LB(WARPS * 32) k_residual_bins_staged(
     GridC g, const double* __restrict__ pd, int64_t cap, const double* __restrict__ xs,
     const int* __restrict__ bin_start, const uint8_t* __restrict__ bflag, const double* __restrict__ Pst,
     const double* __restrict__ bext, double load_scale, double* __restrict__ r, int c0, int c1, int c2, int nb0,
@@ -3073,8 +3081,16 @@ __global__ void __launch_bounds__(WARPS * 32) k_galerkin_ap(GridC gf, GridC gc, 
 // over the 3^D fine rows i in supp(P_I); lanes own coarse box slots J.
 // Compacts nonzero blocks, sets the coarse free mask from the diagonal and
 // the masked block inverse.
+#ifndef IMPM_PTAP_MINB
+#define IMPM_PTAP_MINB 0  // 0: the compiler's register choice
+#endif
+#if IMPM_PTAP_MINB > 0
+#define IMPM_PTAP_LB(T) __launch_bounds__(T, IMPM_PTAP_MINB)
+#else
+#define IMPM_PTAP_LB(T) __launch_bounds__(T)
+#endif
 template <int D, int F, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32) k_galerkin_ptap(GridC gf, GridC gc, const int* __restrict__ f_act_idx,
+__global__ void IMPM_PTAP_LB(WARPS * 32) k_galerkin_ptap(GridC gf, GridC gc, const int* __restrict__ f_act_idx,
                                                               const uint8_t* __restrict__ f_freem,
                                                               const double* __restrict__ T,
                                                               const int* __restrict__ c_act_list, int c_n_act,
