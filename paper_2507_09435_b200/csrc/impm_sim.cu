@@ -283,7 +283,9 @@ struct Sim {
   // rebuild the coarse MG levels every mg_refresh load steps (A/B experiments)
   // (default 3; a solve on stale levels that fails or overruns 4x the last
   // iteration count is retried once on a freshly built hierarchy)
-  int mg_refresh = std::getenv("IMPM_MG_REFRESH") ? std::atoi(std::getenv("IMPM_MG_REFRESH")) : 3;
+  // (cfg 4 at omega safety 1.0, Newton it/s: driver window 3: 13.12, 5: 13.00, 6: 13.35, 8: 12.94;
+  // default window 3: 14.08, 6: 14.86; the capped stale-level solve keeps the Krylov counts)
+  int mg_refresh = std::getenv("IMPM_MG_REFRESH") ? std::atoi(std::getenv("IMPM_MG_REFRESH")) : 6;
   // re-estimate the smoother's lambda_max every mg_power_every load steps (A/B experiments)
   int mg_power_every = std::getenv("IMPM_MG_POWER_EVERY") ? std::max(1, std::atoi(std::getenv("IMPM_MG_POWER_EVERY"))) : 5;
   // safety factor on the power estimate in omega = 4 / (3 s lambda): cfg 4 driver window,
